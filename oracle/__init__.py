@@ -1,0 +1,179 @@
+"""The CPU ORACLE (test infrastructure only).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+leg may import this package. The product path (paper_2308_07173_b200) never does.
+
+Python side: ctypes marshalling of numpy arrays into oracle/oracle.c (plain C,
+fp64, brute force), which holds every piece of the method's arithmetic.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OK, EINVAL, EK, EDEGENERATE = 0, -1, -2, -6
+LIN_REUSE_CORR = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc -O2 -ffp-contract=off -fopenmp)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+               "-shared", "-Wall", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+class AlignParams(ctypes.Structure):
+    _fields_ = [("max_iter", ctypes.c_int), ("lm", ctypes.c_int), ("rot_eps", ctypes.c_double),
+                ("trans_eps", ctypes.c_double), ("max_corr_dist", ctypes.c_float)]
+
+
+class AlignResult(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_double * 16), ("iterations", ctypes.c_int), ("converged", ctypes.c_int),
+                ("error", ctypes.c_double), ("inliers", ctypes.c_int64)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i64, i32, f32, f64 = ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_double
+        L.oracle_knn.argtypes = [P, i64, P, i64, i32, P, P, i32]
+        L.oracle_d2.argtypes = [P, P]
+        L.oracle_d2.restype = f32
+        L.oracle_jacobi3.argtypes = [P, P, P]
+        L.oracle_covariance.argtypes = [P, i64, P, i64, i32, f64, P, P, P, i32]
+        L.oracle_linearize.argtypes = [P, P, i64, P, P, i64, P, f32, i32, P, P, P, i32]
+        L.oracle_se3_exp.argtypes = [P, P]
+        L.oracle_se3_exp.restype = None
+        L.oracle_ldlt_solve6.argtypes = [P, P, P]
+        L.oracle_align.argtypes = [P, P, i64, P, P, i64, P, ctypes.POINTER(AlignParams),
+                                   ctypes.POINTER(AlignResult), i32]
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, what):
+        super().__init__(f"{what} failed with code {code}")
+        self.code = code
+
+
+def knn(tgt, q, k, nthreads=0):
+    """O1: (nbr int32 [m,k], d2 float32 [m,k]) -- brute force over all targets."""
+    tgt, q = _f32(tgt), _f32(q)
+    m = q.shape[0]
+    nbr = np.empty((m, k), np.int32)
+    d2 = np.empty((m, k), np.float32)
+    rc = lib().oracle_knn(_ptr(tgt), tgt.shape[0], _ptr(q), m, k, _ptr(nbr), _ptr(d2), nthreads)
+    if rc != OK:
+        raise OracleError(rc, "oracle_knn")
+    return nbr, d2
+
+
+def d2(q, p):
+    q, p = _f32(q), _f32(p)
+    return float(lib().oracle_d2(_ptr(q), _ptr(p)))
+
+
+def jacobi3(S):
+    S = np.ascontiguousarray(S, dtype=np.float64).reshape(3, 3)
+    lam = np.empty(3)
+    V = np.empty((3, 3))
+    lib().oracle_jacobi3(_ptr(S), _ptr(lam), _ptr(V))
+    return lam, V
+
+
+def covariance(xyz, nbr, eps=1e-3, nthreads=0):
+    """O2: (cov fp64 [m,6], gap [m], S6 [m,6])."""
+    xyz = _f32(xyz)
+    nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+    m, k = nbr.shape
+    cov = np.empty((m, 6))
+    gap = np.empty(m)
+    S6 = np.empty((m, 6))
+    rc = lib().oracle_covariance(_ptr(xyz), xyz.shape[0], _ptr(nbr), m, k, eps, _ptr(cov), _ptr(gap),
+                                 _ptr(S6), nthreads)
+    if rc != OK:
+        raise OracleError(rc, "oracle_covariance")
+    return cov, gap, S6
+
+
+def linearize(src, src_cov, tgt, tgt_cov, T, max_corr_dist=1.0, corr=None, nthreads=0):
+    """O3: (out29, absum29, corr). With corr given: REUSE_CORR (no search)."""
+    src, tgt = _f32(src), _f32(tgt)
+    src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    out = np.empty(29)
+    ab = np.empty(29)
+    flags = 0
+    if corr is not None:
+        corr = np.ascontiguousarray(corr, dtype=np.int32).copy()
+        flags = LIN_REUSE_CORR
+    else:
+        corr = np.empty(src.shape[0], np.int32)
+    rc = lib().oracle_linearize(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
+                                _ptr(T), max_corr_dist, flags, _ptr(out), _ptr(ab), _ptr(corr), nthreads)
+    if rc != OK:
+        raise OracleError(rc, "oracle_linearize")
+    return out, ab, corr
+
+
+def se3_exp(delta):
+    delta = np.ascontiguousarray(delta, dtype=np.float64)
+    T = np.empty((4, 4))
+    lib().oracle_se3_exp(_ptr(delta), _ptr(T))
+    return T
+
+
+def ldlt_solve6(A, y):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    x = np.empty(6)
+    rc = lib().oracle_ldlt_solve6(_ptr(A), _ptr(y), _ptr(x))
+    if rc != 0:
+        raise OracleError(rc, "oracle_ldlt_solve6")
+    return x
+
+
+def align(src, src_cov, tgt, tgt_cov, T0, max_iter=64, lm=True, rot_eps=1e-6, trans_eps=1e-5,
+          max_corr_dist=1.0, nthreads=0):
+    """O4: returns dict(T, iterations, converged, error, inliers)."""
+    src, tgt = _f32(src), _f32(tgt)
+    src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
+    T0 = np.ascontiguousarray(T0, dtype=np.float64)
+    p = AlignParams(max_iter, int(lm), rot_eps, trans_eps, max_corr_dist)
+    r = AlignResult()
+    rc = lib().oracle_align(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
+                            _ptr(T0), ctypes.byref(p), ctypes.byref(r), nthreads)
+    if rc != OK:
+        raise OracleError(rc, "oracle_align")
+    return dict(T=np.array(r.T[:]).reshape(4, 4), iterations=r.iterations, converged=bool(r.converged),
+                error=r.error, inliers=r.inliers)
+
+
+def pack_cov(cov6):
+    """fp64 [m,6] -> fp32 [m,6] (the library's covariance storage)."""
+    return np.ascontiguousarray(np.asarray(cov6, dtype=np.float64).astype(np.float32))
