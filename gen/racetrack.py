@@ -460,3 +460,21 @@ def uniform_cloud(n: int, seed: int, lo: float = -10.0, hi: float = 10.0, offset
     rng = np.random.default_rng(np.random.SeedSequence([seed, 6]))
     p = rng.uniform(lo, hi, (n, 3)) + np.asarray(offset)
     return np.ascontiguousarray(p.astype(np.float32))
+
+
+def random_covariances(n: int, seed: int, lo: float = 1e-3, hi: float = 1.0) -> np.ndarray:
+    """Generic SPD 3x3 inputs (xx, xy, xz, yy, yz, zz) fp32 [n, 6]: Q diag(l) Q^T with
+    Q a uniform random rotation (unit quaternion) and l log-uniform in [lo, hi].
+    Input synthesis only (the covariance estimator is not involved)."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 8]))
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    Q = np.stack([
+        np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)], -1),
+        np.stack([2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)], -1),
+        np.stack([2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)], -1)], -2)
+    lam = np.exp(rng.uniform(np.log(lo), np.log(hi), (n, 3)))
+    C = np.einsum("nij,nj,nkj->nik", Q, lam, Q)
+    out = np.stack([C[:, 0, 0], C[:, 0, 1], C[:, 0, 2], C[:, 1, 1], C[:, 1, 2], C[:, 2, 2]], -1)
+    return np.ascontiguousarray(out.astype(np.float32))

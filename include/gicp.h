@@ -1,0 +1,194 @@
+/*
+ * gicp.h -- C ABI of the B200-native GICP hot path (libgicp_b200.so).
+ *
+ * The paper (arxiv 2308.07173, §III-C1 "Efficient registration method",
+ * l.377-435) models scans P, Q as Gaussian clouds p_i ~ N(p_i, C^p_i) (l.380),
+ * defines d_i = q_i - T p_i (eq_trans_err, l.382-387) and registers by
+ * T = argmin sum_i d_i^T (C^q_i + R C^p_i R^T)^-1 d_i (eq_trans_likelihood,
+ * l.396-402, read with '+' and the inverse: DESIGN.md readings R1/R2). Its GPU
+ * contribution is "nearest points search and covariance computation" (l.413,
+ * l.798) -- the calls below -- plus the per-iteration linearisation this build
+ * adds.
+ *
+ * Conventions for every call:
+ *  - Pointers are DEVICE pointers (CUDA global memory of the current device)
+ *    unless marked (host). Point clouds are fp32 xyz, [n][3] row-major, 4-byte
+ *    aligned. Covariances are fp32 [n][6] = (xx, xy, xz, yy, yz, zz).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    knn / covariances / linearize are stream-ordered and asynchronous with
+ *    respect to the host; build_index and align are synchronous.
+ *  - Ownership: the caller owns every buffer it passes in and every output
+ *    buffer; the library never frees them. An index owns a private device copy
+ *    of its points (the caller may free xyz after gicp_build_index returns) plus
+ *    scratch; it is immutable after build except for that scratch, so calls on
+ *    one index must be serialised by the caller (one stream at a time).
+ *  - Errors: argument errors are detected synchronously and returned as a
+ *    negative code; gicp_last_error() gives a thread-local message. Kernel
+ *    launch failures return GICP_ECUDA. Outputs never contain NaN for finite
+ *    inputs.
+ */
+#ifndef GICP_B200_H
+#define GICP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GICP_KMAX 32
+
+enum {
+    GICP_OK = 0,
+    GICP_EINVAL = -1,      /* null pointer, n <= 0, bad cell size / radius, non-finite coordinates */
+    GICP_EK = -2,          /* k < 1 || k > GICP_KMAX || k > n_target */
+    GICP_ERANGE = -3,      /* the voxel grid would exceed 2^21 cells per axis */
+    GICP_ENOMEM = -4,      /* device allocation failed */
+    GICP_ECUDA = -5,       /* a CUDA runtime call or kernel launch failed */
+    GICP_EDEGENERATE = -6  /* fewer than 6 gated correspondences */
+};
+
+typedef struct gicp_index_s* gicp_index;
+
+/* Thread-local message describing the last failure of this thread ("" if none). */
+const char* gicp_last_error(void);
+
+/* Library ABI version (major * 100 + minor). */
+int gicp_version(void);
+
+/* ---------------------------------------------------------------------------
+ * gicp_build_index -- the spatial structure behind "GPU-based nearest points
+ * search" ("GPU-hash data structure", l.477): a uniform voxel
+ * grid built by radix sort on cell keys.
+ *   xyz        [n][3] fp32 target cloud (device). Must be finite (checked).
+ *   n          number of points, 1 <= n < 2^31.
+ *   cell_size  voxel edge in metres (> 0), or 0 for an automatic choice
+ *              (about 1.15 x the expected 20-NN radius, from the occupancy of a
+ *              trial grid).
+ *   out (host) receives the new index on success.
+ * Synchronous (returns after the build completed on `stream`).
+ * Errors: EINVAL (null, n <= 0, cell_size < 0 / non-finite, non-finite xyz),
+ *         ERANGE (grid too fine for the bounding box), ENOMEM, ECUDA.
+ * ------------------------------------------------------------------------- */
+int gicp_build_index(const float* xyz, int64_t n, float cell_size, void* stream, gicp_index* out);
+
+/* Releases the index and all device memory it owns. NULL is a no-op. */
+void gicp_index_free(gicp_index idx);
+
+typedef struct {
+    int64_t n;            /* points */
+    int64_t n_cells;      /* occupied voxels */
+    float cell_size;      /* metres */
+    float origin[3];      /* grid origin (bounding-box minimum) */
+    int32_t dims[3];      /* voxels per axis */
+    int64_t device_bytes; /* device memory owned by the index */
+} gicp_index_info;
+
+/* Host-side description of an index. Errors: EINVAL. */
+int gicp_get_index_info(gicp_index idx, gicp_index_info* info /* host */);
+
+/* ---------------------------------------------------------------------------
+ * gicp_knn -- exact k nearest neighbours of external queries ("finding
+ * corresponding points"). For each query i, the k smallest
+ * keys (d2, j) over ALL n target points, where
+ *   dx = qx - px; dy = qy - py; dz = qz - pz;  d2 = fmaf(dz,dz, fmaf(dy,dy, dx*dx))
+ * in fp32 round-to-nearest (reading R9), ties broken by the target's
+ * ORIGINAL index j. Rows ascend by (d2, j).
+ *   q      [m][3] fp32 queries (device); a non-finite query yields nbr = -1, d2 = +inf.
+ *   nbr    [m][k] int32 out: original target indices.
+ *   d2     [m][k] fp32 out: squared distances.
+ * Errors: EINVAL (null, m < 0), EK. m = 0 is a no-op.
+ * ------------------------------------------------------------------------- */
+int gicp_knn(gicp_index idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, void* stream);
+
+/* As gicp_knn with the index's own points as the queries, rows in the points'
+ * original order (the query itself is its own first neighbour unless an exact
+ * duplicate with a smaller index exists). nbr/d2 are [n][k]. */
+int gicp_knn_self(gicp_index idx, int k, int32_t* nbr, float* d2, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * gicp_covariances -- per-point covariance C_i for the Gaussian model (PAPER.md
+ * l.380, l.404 "computing covariance when estimate the C^p_i and C^q_i"):
+ *   mu = (1/k) sum_j x_nbr[i][j];  S = (1/k) sum_j (x - mu)(x - mu)^T;
+ *   eigenvalues of S replaced by (eps, 1, 1) in ascending order (GICP plane
+ *   regularisation, reading R7): C = I - (1 - eps) n n^T with n the
+ *   smallest-eigenvalue eigenvector; n = +z when all k neighbours coincide (R11).
+ *   xyz    [n][3] fp32 cloud that nbr indexes (device).
+ *   nbr    [m][k] int32 (device), each in [0, n).
+ *   eps    regularisation, 0 < eps <= 1 (1e-3 in GICP).
+ *   cov    [m][6] fp32 out.
+ * Errors: EINVAL (null, n <= 0, m < 0, eps out of range), EK. Out-of-range
+ * nbr entries are a caller error (undefined results, no fault: clamped).
+ * ------------------------------------------------------------------------- */
+int gicp_covariances(const float* xyz, int64_t n, const int32_t* nbr, int64_t m, int k, float eps, float* cov,
+                     void* stream);
+
+/* Fused kNN + covariance over the index's own points in one kernel (the hot
+ * path of the headline workload). Outputs as gicp_knn_self + gicp_covariances;
+ * nbr and d2 may be NULL to skip writing them. */
+int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, float* d2, float* cov, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * gicp_linearize -- one GICP linearisation at pose T (PAPER.md eq_trans_err
+ * l.382-387, eq_trans_likelihood l.396-402; readings R1-R4, R12):
+ *   p'  = R p + t in fp64 (a-th row: fma(R_a2, p_z, fma(R_a1, p_y, fma(R_a0, p_x, t_a))))
+ *   s   = fl32(p');  j* = argmin_j (d2(s, q_j), j) over ALL targets (d2 as gicp_knn)
+ *   inlier iff d2 < fl32(r*r);   d = q_j* - p';  M = (C^q_j* + R C^p_i R^T)^-1
+ *   J = [skew(p') | -I3] (left perturbation T <- Exp(delta) T, delta = (omega, v))
+ *   out29 = sum over inliers of J^T M J (21 upper-triangle entries, row-major),
+ *           J^T M d (6), d^T M d (1), inlier count (1)  -- fp64, deterministic
+ *           fixed-order reduction (bitwise reproducible run to run).
+ *   src, src_cov  [ns][3], [ns][6] fp32 (device).
+ *   tgt           index built on the target cloud; tgt_cov [nt][6] fp32 in the
+ *                 target's ORIGINAL order (device).
+ *   T (host)      4x4 row-major fp64 (rigid).
+ *   max_corr_dist gate r in metres (> 0).
+ *   flags         GICP_LIN_REUSE_CORR: skip the search and use corr[] as given
+ *                 (entries < 0 are outliers); GICP_LIN_ERROR_ONLY: only e and the
+ *                 count are accumulated (H and b are written as 0).
+ *   out29         device fp64 [29] out.
+ *   corr          [ns] int32 out (j* or -1), nullable unless REUSE_CORR.
+ * Errors: EINVAL (null, ns < 0, r <= 0), ENOMEM (scratch), ECUDA.
+ * ------------------------------------------------------------------------- */
+enum { GICP_LIN_REUSE_CORR = 1, GICP_LIN_ERROR_ONLY = 2 };
+
+int gicp_linearize(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, const float* tgt_cov,
+                   const double T[16] /* host */, float max_corr_dist, int flags, double* out29, int32_t* corr,
+                   void* stream);
+
+/* ---------------------------------------------------------------------------
+ * gicp_align -- host Levenberg-Marquardt over gicp_linearize (T = argmin ...,
+ * PAPER.md l.396-402; the optimiser is DESIGN.md reading R13):
+ *   per iteration: linearize at T (search), lambda init 1e-9 max diag(H), up to
+ *   10 inner trials solving (H + lambda I) delta = -b (LDL^T), T' = Exp(delta) T,
+ *   e' = linearize(T', REUSE_CORR, ERROR_ONLY), gain rho = (e - e')/(delta^T
+ *   (lambda delta - b)); accept iff rho > 0 (lambda *= max(1/3, 1 - (2 rho - 1)^3))
+ *   else lambda *= nu, nu *= 2; converged when max|delta_omega| < rot_eps and
+ *   max|delta_v| < trans_eps. lm = 0 gives plain Gauss-Newton.
+ * Synchronous. Errors: EINVAL, EDEGENERATE (< 6 inliers), ENOMEM, ECUDA.
+ * Non-convergence is not an error (result->converged = 0).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int max_iter;        /* 64 */
+    int lm;              /* 1 = Levenberg-Marquardt, 0 = Gauss-Newton */
+    double rot_eps;      /* 1e-6 rad */
+    double trans_eps;    /* 1e-5 m */
+    float max_corr_dist; /* 1.0 m */
+} gicp_align_params;
+
+typedef struct {
+    double T[16];        /* final pose, row-major */
+    int iterations;      /* outer iterations run */
+    int converged;       /* 1 if the step criterion was met */
+    double error;        /* cost at the final pose (last accepted evaluation) */
+    int64_t inliers;     /* inliers of the last linearisation */
+} gicp_align_result;
+
+int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, const float* tgt_cov,
+               const double T0[16] /* host */, const gicp_align_params* params /* host */,
+               gicp_align_result* result /* host */, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GICP_B200_H */

@@ -1,0 +1,221 @@
+"""paper_2308_07173_b200 -- thin Python binding of libgicp_b200.so (include/gicp.h).
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA
+kernels. torch provides device memory and the current stream. There is no CPU
+fallback: if the shared library is missing this import fails loudly.
+
+Names follow the C ABI: build_index, knn, knn_self, covariances, knn_cov_self,
+linearize, align (§III-C1, l.377-435).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgicp_b200.so")
+
+OK, EINVAL, EK, ERANGE, ENOMEM, ECUDA, EDEGENERATE = 0, -1, -2, -3, -4, -5, -6
+LIN_REUSE_CORR, LIN_ERROR_ONLY = 1, 2
+KMAX = 32
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
+                      "There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class IndexInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_cells", ctypes.c_int64), ("cell_size", ctypes.c_float),
+                ("origin", ctypes.c_float * 3), ("dims", ctypes.c_int32 * 3), ("device_bytes", ctypes.c_int64)]
+
+
+class AlignParams(ctypes.Structure):
+    _fields_ = [("max_iter", ctypes.c_int), ("lm", ctypes.c_int), ("rot_eps", ctypes.c_double),
+                ("trans_eps", ctypes.c_double), ("max_corr_dist", ctypes.c_float)]
+
+
+class AlignResult(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_double * 16), ("iterations", ctypes.c_int), ("converged", ctypes.c_int),
+                ("error", ctypes.c_double), ("inliers", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_i64, _i32, _f32 = ctypes.c_int64, ctypes.c_int, ctypes.c_float
+_lib.gicp_last_error.restype = ctypes.c_char_p
+_lib.gicp_version.restype = _i32
+_lib.gicp_build_index.argtypes = [_P, _i64, _f32, _P, ctypes.POINTER(_P)]
+_lib.gicp_index_free.argtypes = [_P]
+_lib.gicp_index_free.restype = None
+_lib.gicp_get_index_info.argtypes = [_P, ctypes.POINTER(IndexInfo)]
+_lib.gicp_knn.argtypes = [_P, _P, _i64, _i32, _P, _P, _P]
+_lib.gicp_knn_self.argtypes = [_P, _i32, _P, _P, _P]
+_lib.gicp_covariances.argtypes = [_P, _i64, _P, _i64, _i32, _f32, _P, _P]
+_lib.gicp_knn_cov_self.argtypes = [_P, _i32, _f32, _P, _P, _P, _P]
+_lib.gicp_linearize.argtypes = [_P, _P, _i64, _P, _P, _P, _f32, _i32, _P, _P, _P]
+_lib.gicp_align.argtypes = [_P, _P, _i64, _P, _P, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
+                            _P]
+
+EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
+           "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align"]
+
+
+class GicpError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise GicpError(rc, _lib.gicp_last_error().decode())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _pts(t: torch.Tensor, name: str) -> torch.Tensor:
+    if t.dtype != torch.float32 or t.dim() != 2 or t.shape[1] != 3:
+        raise ValueError(f"{name} must be float32 [n, 3]")
+    return t.contiguous()
+
+
+class Index:
+    """An index owned by the library (gicp_build_index). Keeps a device copy."""
+
+    def __init__(self, handle: ctypes.c_void_p, device: torch.device):
+        self._h = handle
+        self.device = device
+        info = IndexInfo()
+        _check(_lib.gicp_get_index_info(self._h, ctypes.byref(info)))
+        self.n = int(info.n)
+        self.n_cells = int(info.n_cells)
+        self.cell_size = float(info.cell_size)
+        self.origin = tuple(info.origin)
+        self.dims = tuple(info.dims)
+        self.device_bytes = int(info.device_bytes)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            _lib.gicp_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def build_index(xyz: torch.Tensor, cell_size: float = 0.0) -> Index:
+    xyz = _pts(xyz, "xyz")
+    h = ctypes.c_void_p()
+    _check(_lib.gicp_build_index(_dptr(xyz), xyz.shape[0], float(cell_size), _stream(), ctypes.byref(h)))
+    return Index(h, xyz.device)
+
+
+def knn(index: Index, q: torch.Tensor, k: int, out=None):
+    q = _pts(q, "q")
+    m = q.shape[0]
+    nbr, d2 = out if out is not None else (torch.empty((m, k), dtype=torch.int32, device=q.device),
+                                           torch.empty((m, k), dtype=torch.float32, device=q.device))
+    _check(_lib.gicp_knn(index.handle, _dptr(q), m, k, _dptr(nbr), _dptr(d2), _stream()))
+    return nbr, d2
+
+
+def knn_self(index: Index, k: int, out=None):
+    nbr, d2 = out if out is not None else (torch.empty((index.n, k), dtype=torch.int32, device=index.device),
+                                           torch.empty((index.n, k), dtype=torch.float32, device=index.device))
+    _check(_lib.gicp_knn_self(index.handle, k, _dptr(nbr), _dptr(d2), _stream()))
+    return nbr, d2
+
+
+def covariances(xyz: torch.Tensor, nbr: torch.Tensor, eps: float = 1e-3, out=None):
+    xyz = _pts(xyz, "xyz")
+    if nbr.dtype != torch.int32 or nbr.dim() != 2:
+        raise ValueError("nbr must be int32 [m, k]")
+    nbr = nbr.contiguous()
+    m, k = nbr.shape
+    cov = out if out is not None else torch.empty((m, 6), dtype=torch.float32, device=xyz.device)
+    _check(_lib.gicp_covariances(_dptr(xyz), xyz.shape[0], _dptr(nbr), m, k, float(eps), _dptr(cov), _stream()))
+    return cov
+
+
+def knn_cov_self(index: Index, k: int, eps: float = 1e-3, with_nbr: bool = True, out=None):
+    n = index.n
+    if out is not None:
+        nbr, d2, cov = out
+    else:
+        cov = torch.empty((n, 6), dtype=torch.float32, device=index.device)
+        nbr = torch.empty((n, k), dtype=torch.int32, device=index.device) if with_nbr else None
+        d2 = torch.empty((n, k), dtype=torch.float32, device=index.device) if with_nbr else None
+    _check(_lib.gicp_knn_cov_self(index.handle, k, float(eps), _dptr(nbr), _dptr(d2), _dptr(cov), _stream()))
+    return nbr, d2, cov
+
+
+def _T(T) -> np.ndarray:
+    T = np.ascontiguousarray(np.asarray(T, dtype=np.float64).reshape(4, 4))
+    return T
+
+
+def linearize(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, tgt_cov: torch.Tensor, T, max_corr_dist=1.0,
+              corr: torch.Tensor | None = None, reuse_corr: bool = False, error_only: bool = False, out=None):
+    """Returns (out29 float64 device tensor [29], corr int32 device tensor [ns])."""
+    src = _pts(src, "src")
+    ns = src.shape[0]
+    Th = _T(T)
+    out29 = out if out is not None else torch.empty(29, dtype=torch.float64, device=src.device)
+    if corr is None:
+        if reuse_corr:
+            raise ValueError("reuse_corr needs corr")
+        corr = torch.empty(ns, dtype=torch.int32, device=src.device)
+    flags = (LIN_REUSE_CORR if reuse_corr else 0) | (LIN_ERROR_ONLY if error_only else 0)
+    _check(_lib.gicp_linearize(_dptr(src), _dptr(src_cov.contiguous()), ns, tgt.handle, _dptr(tgt_cov.contiguous()),
+                               Th.ctypes.data_as(_P), float(max_corr_dist), flags, _dptr(out29), _dptr(corr),
+                               _stream()))
+    return out29, corr
+
+
+@dataclass
+class AlignInfo:
+    iterations: int
+    converged: bool
+    error: float
+    inliers: int
+
+
+def align(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, tgt_cov: torch.Tensor, T0, max_iter=64, lm=True,
+          rot_eps=1e-6, trans_eps=1e-5, max_corr_dist=1.0):
+    src = _pts(src, "src")
+    T0h = _T(T0)
+    p = AlignParams(int(max_iter), int(bool(lm)), float(rot_eps), float(trans_eps), float(max_corr_dist))
+    r = AlignResult()
+    _check(_lib.gicp_align(_dptr(src), _dptr(src_cov.contiguous()), src.shape[0], tgt.handle,
+                           _dptr(tgt_cov.contiguous()), T0h.ctypes.data_as(_P), ctypes.byref(p), ctypes.byref(r),
+                           _stream()))
+    T = np.array(r.T[:], dtype=np.float64).reshape(4, 4)
+    return T, AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers))
+
+
+def version() -> int:
+    return int(_lib.gicp_version())

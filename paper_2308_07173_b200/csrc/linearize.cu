@@ -1,0 +1,380 @@
+// linearize.cu -- gicp_linearize: gated 1-NN correspondence, Mahalanobis residual,
+// Jacobian and the deterministic fp64 reduction of H (21), b (6), e, count.
+//
+// Paper: d_i = q_i - T p_i (eq_trans_err), cost
+// sum d_i^T (C^q_i + R C^p_i R^T)^-1 d_i (eq_trans_err_dist / eq_trans_likelihood,
+// l.388-402, readings R1-R4, R12). Per source point (one thread each,
+// PPT points per thread, fixed mapping):
+//   p' = R p + t in fp64 (FMA chain of the header), s = fl32(p')
+//   j* = argmin over ALL targets of (d2(s, q_j), j): voxel-grid search with the
+//        conservative stop rule of knn.cu, pruned at the gate r
+//   inlier iff d2 < fl32(r*r); d = q - p' (fp64 -> fp32);
+//   A = C^q + R C^p R^T, M = A^-1 (fp32 adjugate), J = [skew(p') | -I]
+//   H += J^T M J, b += J^T M d, e += d^T M d  (fp64 accumulators)
+// Reduction: per-thread fp64 sums -> warp shuffle tree -> block tree -> block
+// partials [nblocks][29] -> the last block to finish sums them in block order.
+// Every step has a fixed order, so out29 is bitwise reproducible and independent
+// of the SM count / scheduling.
+#include "gicp_internal.cuh"
+
+namespace gicp {
+namespace {
+
+constexpr int kLinBlock = 256;
+constexpr int kPPT = 4;                       // points per thread
+constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: defines the partition)
+constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
+constexpr float kRel = 1.0f - 1.0f / (1 << 20);
+constexpr int kMaxRing = 16;
+
+struct Pose {
+    double R[9];
+    double t[3];
+    float Rf[9];
+};
+
+__constant__ signed char c_off27l[27][3] = {
+    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
+    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
+    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
+    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+
+__device__ __forceinline__ float gap_axis(int d, float f, float s, float slack) {
+    float gap = 0.0f;
+    if (d < 0) gap = (float)(-d - 1) * s + f - slack;
+    if (d > 0) gap = (float)(d - 1) * s + (s - f) - slack;
+    return fmaxf(gap, 0.0f);
+}
+
+// Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) among all
+// targets whenever that d2 < r2; bp = its coordinates.
+__device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const HashEntry* __restrict__ H,
+                                          const Grid& g, float qx, float qy, float qz, float r2,
+                                          unsigned long long& best, float3& bp, int& overflow) {
+    best = kEmptyKey;
+    overflow = 0;
+    const int cx = cell_coord(qx, g.ox, g.inv_cell), cy = cell_coord(qy, g.oy, g.inv_cell),
+              cz = cell_coord(qz, g.oz, g.inv_cell);
+    const double sd = (double)g.cell;
+    const float fx = (float)((double)qx - ((double)g.ox + (double)cx * sd));
+    const float fy = (float)((double)qy - ((double)g.oy + (double)cy * sd));
+    const float fz = (float)((double)qz - ((double)g.oz + (double)cz * sd));
+    const float s = g.cell, slack = g.slack;
+    auto bound = [&]() { return fminf(__uint_as_float((unsigned)(best >> 32)), r2); };
+    auto scan = [&](int2 rng) {
+        for (int j = rng.x; j < rng.y; ++j) {
+            const float4 p = __ldg(pts + j);
+            const float d2 = dist2(qx, qy, qz, p.x, p.y, p.z);
+            const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
+            if (key < best) {
+                best = key;
+                bp = make_float3(p.x, p.y, p.z);
+            }
+        }
+    };
+    for (int c = 0; c < 27; ++c) {
+        const int dx = c_off27l[c][0], dy = c_off27l[c][1], dz = c_off27l[c][2];
+        const float gx = gap_axis(dx, fx, s, slack), gy = gap_axis(dy, fy, s, slack), gz = gap_axis(dz, fz, s, slack);
+        const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+        if (lb2 * kRel > bound()) continue;
+        scan(cell_lookup(H, g, cx + dx, cy + dy, cz + dz));
+    }
+    const int R0 = max(max(max(-cx, cx - (g.nx - 1)), max(-cy, cy - (g.ny - 1))), max(-cz, cz - (g.nz - 1)));
+    int R = 1;
+    while (true) {
+        const float mx = fminf(fx + R * s, (R + 1) * s - fx);
+        const float my = fminf(fy + R * s, (R + 1) * s - fy);
+        const float mz = fminf(fz + R * s, (R + 1) * s - fz);
+        const float m = fminf(mx, fminf(my, mz)) - slack;
+        if (m > 0.0f && bound() < m * m * kRel) break;
+        const bool covers = cx - R <= 0 && cx + R >= g.nx - 1 && cy - R <= 0 && cy + R >= g.ny - 1 && cz - R <= 0 &&
+                            cz + R >= g.nz - 1;
+        if (covers) break;
+        ++R;
+        if (R < R0) R = R0;
+        if (R > max(R0, 1) + kMaxRing) {
+            overflow = 1;
+            return;
+        }
+        const int z0 = max(-R, -cz), z1 = min(R, g.nz - 1 - cz);
+        const int y0 = max(-R, -cy), y1 = min(R, g.ny - 1 - cy);
+        const int x0 = max(-R, -cx), x1 = min(R, g.nx - 1 - cx);
+        for (int dz = z0; dz <= z1; ++dz) {
+            const float gz = gap_axis(dz, fz, s, slack);
+            for (int dy = y0; dy <= y1; ++dy) {
+                const float gy = gap_axis(dy, fy, s, slack);
+                if (__fmaf_rn(gz, gz, gy * gy) * kRel > bound()) continue;
+                auto visit = [&](int dx) {
+                    const float gx = gap_axis(dx, fx, s, slack);
+                    const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                    if (lb2 * kRel > bound()) return;
+                    scan(cell_lookup(H, g, cx + dx, cy + dy, cz + dz));
+                };
+                if (dz == -R || dz == R || dy == -R || dy == R) {
+                    for (int dx = x0; dx <= x1; ++dx) visit(dx);
+                } else {
+                    if (-R >= x0) visit(-R);
+                    if (R <= x1) visit(R);
+                }
+            }
+        }
+    }
+}
+
+// brute-force fallback for overflowed searches (the caller handles one point)
+__device__ __forceinline__ void nn_bruteforce(const float4* __restrict__ pts, int64_t n, float qx, float qy, float qz,
+                                              unsigned long long& best, float3& bp) {
+    best = kEmptyKey;
+    for (int64_t j = 0; j < n; ++j) {
+        const float4 p = __ldg(pts + j);
+        const float d2 = dist2(qx, qy, qz, p.x, p.y, p.z);
+        const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
+        if (key < best) {
+            best = key;
+            bp = make_float3(p.x, p.y, p.z);
+        }
+    }
+}
+
+__device__ __forceinline__ void load_cov6(const float* __restrict__ c, int64_t row, float o[6]) {
+    const float2* p = reinterpret_cast<const float2*>(c + row * 6);
+    const float2 a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = b.x;
+    o[3] = b.y;
+    o[4] = d.x;
+    o[5] = d.y;
+}
+
+// per-point terms of one inlier, accumulated into fp64 acc[28]
+template <bool ERROR_ONLY>
+__device__ __forceinline__ void accumulate_point(const Pose& P, const double pp[3], float qx, float qy, float qz,
+                                                 const float cp[6], const float cq[6], double acc[kNumAcc]) {
+    const float dx = (float)((double)qx - pp[0]);
+    const float dy = (float)((double)qy - pp[1]);
+    const float dz = (float)((double)qz - pp[2]);
+    // A = C^q + R C^p R^T
+    const float* R = P.Rf;
+    const float C[9] = {cp[0], cp[1], cp[2], cp[1], cp[3], cp[4], cp[2], cp[4], cp[5]};
+    float RC[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) RC[3 * a + b] = R[3 * a] * C[b] + R[3 * a + 1] * C[3 + b] + R[3 * a + 2] * C[6 + b];
+    float A[6];  // upper: 00 01 02 11 12 22
+    A[0] = cq[0] + (RC[0] * R[0] + RC[1] * R[1] + RC[2] * R[2]);
+    A[1] = cq[1] + (RC[0] * R[3] + RC[1] * R[4] + RC[2] * R[5]);
+    A[2] = cq[2] + (RC[0] * R[6] + RC[1] * R[7] + RC[2] * R[8]);
+    A[3] = cq[3] + (RC[3] * R[3] + RC[4] * R[4] + RC[5] * R[5]);
+    A[4] = cq[4] + (RC[3] * R[6] + RC[4] * R[7] + RC[5] * R[8]);
+    A[5] = cq[5] + (RC[6] * R[6] + RC[7] * R[7] + RC[8] * R[8]);
+    // M = A^-1 by the adjugate (A SPD, cond <= 1/eps)
+    const float m00 = A[3] * A[5] - A[4] * A[4];
+    const float m01 = A[2] * A[4] - A[1] * A[5];
+    const float m02 = A[1] * A[4] - A[2] * A[3];
+    const float m11 = A[0] * A[5] - A[2] * A[2];
+    const float m12 = A[1] * A[2] - A[0] * A[4];
+    const float m22 = A[0] * A[3] - A[1] * A[1];
+    const float det = A[0] * m00 + A[1] * m01 + A[2] * m02;
+    const float id = 1.0f / det;
+    const float M00 = m00 * id, M01 = m01 * id, M02 = m02 * id, M11 = m11 * id, M12 = m12 * id, M22 = m22 * id;
+    const float mdx = M00 * dx + M01 * dy + M02 * dz;
+    const float mdy = M01 * dx + M11 * dy + M12 * dz;
+    const float mdz = M02 * dx + M12 * dy + M22 * dz;
+    acc[27] += (double)(dx * mdx + dy * mdy + dz * mdz);
+    if (ERROR_ONLY) return;
+    const float px = (float)pp[0], py = (float)pp[1], pz = (float)pp[2];
+    // P = skew(p') = [[0,-z,y],[z,0,-x],[-y,x,0]];  MP = M P
+    const float MP00 = M01 * pz - M02 * py, MP01 = -M00 * pz + M02 * px, MP02 = M00 * py - M01 * px;
+    const float MP10 = M11 * pz - M12 * py, MP11 = -M01 * pz + M12 * px, MP12 = M01 * py - M11 * px;
+    const float MP20 = M12 * pz - M22 * py, MP21 = -M02 * pz + M22 * px, MP22 = M02 * py - M12 * px;
+    // H_ww = P^T (M P), P^T = -P: rows of P^T: [0, z, -y], [-z, 0, x], [y, -x, 0]
+    const float H00 = pz * MP10 - py * MP20;
+    const float H01 = pz * MP11 - py * MP21;
+    const float H02 = pz * MP12 - py * MP22;
+    const float H11 = -pz * MP01 + px * MP21;
+    const float H12 = -pz * MP02 + px * MP22;
+    const float H22 = py * MP02 - px * MP12;
+    // H_wv = -P^T M = (M P)^T  (since P^T M = -(M P)^T ... with M symmetric: (MP)^T = P^T M)
+    // J = [P | -I]: J^T M J = [[P^T M P, -P^T M], [-M P, M]]; -P^T M = -(MP)^T
+    const float H03 = -MP00, H04 = -MP10, H05 = -MP20;
+    const float H13 = -MP01, H14 = -MP11, H15 = -MP21;
+    const float H23 = -MP02, H24 = -MP12, H25 = -MP22;
+    // b = J^T M d = [P^T M d; -M d];  P^T (Md) = -p' x Md
+    const float b0 = pz * mdy - py * mdz;
+    const float b1 = -pz * mdx + px * mdz;
+    const float b2 = py * mdx - px * mdy;
+    const float v[27] = {H00, H01, H02, H03, H04, H05, H11, H12, H13, H14, H15, H22,   H23,   H24,
+                         H25, M00, M01, M02, M11, M12, M22, b0,  b1,  b2,  -mdx, -mdy, -mdz};
+#pragma unroll
+    for (int c = 0; c < 27; ++c) acc[c] += (double)v[c];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    return v;
+}
+
+template <bool REUSE, bool ERROR_ONLY>
+__global__ void __launch_bounds__(kLinBlock) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
+                                                         int64_t ns, const float4* __restrict__ pts,
+                                                         const float4* __restrict__ pts_orig,
+                                                         const HashEntry* __restrict__ H, Grid g, int64_t nt,
+                                                         const float* __restrict__ tgt_cov, Pose P, float r2,
+                                                         int32_t* __restrict__ corr, double* __restrict__ partials,
+                                                         unsigned* __restrict__ done, double* __restrict__ out29) {
+    double acc[kNumAcc];
+#pragma unroll
+    for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
+    double cnt = 0.0;
+    const int64_t base = (int64_t)blockIdx.x * kPPB + threadIdx.x;
+#pragma unroll 1
+    for (int k = 0; k < kPPT; ++k) {
+        const int64_t i = base + (int64_t)k * kLinBlock;
+        if (i >= ns) break;
+        const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
+        double pp[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            pp[a] = __fma_rn(P.R[3 * a + 2], pz, __fma_rn(P.R[3 * a + 1], py, __fma_rn(P.R[3 * a], px, P.t[a])));
+        int orig;
+        float qx, qy, qz;
+        if (REUSE) {
+            orig = corr[i];
+            if (orig < 0 || orig >= nt) continue;
+            const float4 q = __ldg(pts_orig + orig);
+            qx = q.x;
+            qy = q.y;
+            qz = q.z;
+        } else {
+            const float sx = (float)pp[0], sy = (float)pp[1], sz = (float)pp[2];
+            unsigned long long best;
+            float3 bp = make_float3(0.f, 0.f, 0.f);
+            int ovf;
+            nn_search(pts, H, g, sx, sy, sz, r2, best, bp, ovf);
+            if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp);
+            const float bd2 = __uint_as_float((unsigned)(best >> 32));
+            orig = (best != kEmptyKey && bd2 < r2) ? (int)(best & 0xffffffffu) : -1;
+            if (corr) corr[i] = orig;
+            if (orig < 0) continue;
+            qx = bp.x;
+            qy = bp.y;
+            qz = bp.z;
+        }
+        float cp[6], cq[6];
+        load_cov6(src_cov, i, cp);
+        load_cov6(tgt_cov, orig, cq);
+        accumulate_point<ERROR_ONLY>(P, pp, qx, qy, qz, cp, cq, acc);
+        cnt += 1.0;
+    }
+    // warp tree
+    __shared__ double sh[kLinBlock / 32][kNumAcc + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < kNumAcc; ++c) {
+        if (ERROR_ONLY && c < 27) continue;
+        const double v = warp_sum(acc[c]);
+        if (lane == 0) sh[wid][c] = v;
+    }
+    {
+        const double v = warp_sum(cnt);
+        if (lane == 0) sh[wid][kNumAcc] = v;
+    }
+    __syncthreads();
+    // block tree: thread c sums component c over the 8 warps in order
+    if (threadIdx.x < kNumAcc + 1) {
+        const int c = threadIdx.x;
+        double v = 0.0;
+        if (!(ERROR_ONLY && c < 27)) {
+#pragma unroll
+            for (int w = 0; w < kLinBlock / 32; ++w) v += sh[w][c];
+        }
+        partials[(int64_t)blockIdx.x * (kNumAcc + 1) + c] = v;
+    }
+    // last block: fixed-order sum of all block partials
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(done, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // 29 components x 8 sub-ranges (fixed split of the block index range)
+    constexpr int kSub = 8;
+    __shared__ double part[kSub][kNumAcc + 1];
+    const int nb = gridDim.x;
+    if (threadIdx.x < kSub * (kNumAcc + 1)) {
+        const int c = threadIdx.x % (kNumAcc + 1), sub = threadIdx.x / (kNumAcc + 1);
+        const int chunk = (nb + kSub - 1) / kSub;
+        const int b0 = sub * chunk, b1 = min(nb, b0 + chunk);
+        double v = 0.0;
+        for (int b = b0; b < b1; ++b) v += __ldcg(partials + (int64_t)b * (kNumAcc + 1) + c);
+        part[sub][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kNumAcc + 1) {
+        const int c = threadIdx.x;
+        double v = 0.0;
+#pragma unroll
+        for (int sub = 0; sub < kSub; ++sub) v += part[sub][c];
+        out29[c] = v;
+    }
+    if (threadIdx.x == 0) *done = 0u;
+}
+
+__global__ void k_zero29(double* out29) {
+    if (threadIdx.x < 29) out29[threadIdx.x] = 0.0;
+}
+
+}  // namespace
+
+int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
+                     const float* tgt_cov, const double T[16], float max_corr_dist, int flags, double* out29,
+                     int32_t* corr, cudaStream_t s) {
+    if (ns == 0) {
+        k_zero29<<<1, 32, 0, s>>>(out29);
+        return check_cuda(cudaGetLastError(), "linearize launch");
+    }
+    Pose P;
+    for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) {
+            P.R[3 * a + b] = T[4 * a + b];
+            P.Rf[3 * a + b] = (float)T[4 * a + b];
+        }
+        P.t[a] = T[4 * a + 3];
+    }
+    volatile float r2v = max_corr_dist * max_corr_dist;  // fp32 product
+    const float r2 = r2v;
+    const int64_t nb = (ns + kPPB - 1) / kPPB;
+    void* scratch = nullptr;
+    const size_t bytes = (size_t)nb * (kNumAcc + 1) * sizeof(double) + 256;
+    if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(GICP_ENOMEM, "linearize scratch allocation failed");
+    }
+    unsigned* done = (unsigned*)scratch;
+    double* partials = (double*)((char*)scratch + 256);
+    int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset");
+    if (rc == GICP_OK) {
+        const bool reuse = flags & GICP_LIN_REUSE_CORR, eonly = flags & GICP_LIN_ERROR_ONLY;
+#define GICP_LIN_ARGS                                                                                      \
+    src, src_cov, ns, tgt->pts, tgt->pts_orig, tgt->hash, tgt->g, tgt->n, tgt_cov, P, r2, corr, partials, done, \
+        out29
+        if (reuse && eonly)
+            k_linearize<true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+        else if (reuse)
+            k_linearize<true, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+        else if (eonly)
+            k_linearize<false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+        else
+            k_linearize<false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+#undef GICP_LIN_ARGS
+        rc = check_cuda(cudaGetLastError(), "linearize launch");
+    }
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+}  // namespace gicp

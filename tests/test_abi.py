@@ -1,0 +1,60 @@
+"""CPU-side checks of the boundary: the C-ABI library builds for sm_100a, loads, and
+exports every symbol include/gicp.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "gicp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gicp_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2308_07173_b200 import build
+    path = build.build()
+    return path
+
+
+def test_header_declares_the_north_star_calls():
+    d = _declared()
+    for name in ["gicp_build_index", "gicp_knn", "gicp_covariances", "gicp_linearize", "gicp_align"]:
+        assert name in d
+
+
+def test_library_exports_every_declared_symbol(lib):
+    L = ctypes.CDLL(lib)
+    for name in _declared():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\b(gicp_[a-z0-9_]+)\b", out))
+    assert set(_declared()) <= exported
+    # nothing else leaks from the C++ implementation
+    assert not [s for s in re.findall(r" T (\S+)", out) if s.startswith("_ZN4gicp")]
+
+
+def test_binary_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_binding_exports_match(lib):
+    import paper_2308_07173_b200 as g
+    assert set(g.EXPORTS) == set(_declared())
+    assert g.version() >= 100
+
+
+def test_product_path_does_not_touch_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2308_07173_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "oracle/" not in txt and "liboracle" not in txt, f
