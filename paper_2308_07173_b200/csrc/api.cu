@@ -153,9 +153,17 @@ GICP_API int gicp_build_index(const float* xyz, int64_t n, float cell_size, void
 
 GICP_API void gicp_index_free(gicp_index idx) {
     if (!idx) return;
-    cudaFree(idx->pts);
-    cudaFree(idx->pts_orig);
-    cudaFree(idx->hash);
+    // stream-ordered release on the build stream (work queued after the build on
+    // other streams must have completed: the caller's contract, as for cudaFree)
+    cudaStream_t s = idx->stream;
+    if (cudaFreeAsync(idx->pts, s) != cudaSuccess) {
+        cudaGetLastError();
+        s = nullptr;  // the build stream is gone: use the legacy stream
+        cudaFreeAsync(idx->pts, s);
+    }
+    cudaFreeAsync(idx->pts_orig, s);
+    cudaFreeAsync(idx->hash, s);
+    cudaGetLastError();
     delete idx;
 }
 

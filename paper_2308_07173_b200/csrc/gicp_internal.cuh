@@ -90,6 +90,7 @@ struct gicp_index_s {
     gicp::HashEntry* hash = nullptr;
     int64_t hash_cap = 0;
     int device = 0;
+    cudaStream_t stream = nullptr;  // build stream: device memory is pool-allocated on it
     int64_t device_bytes = 0;
 };
 

@@ -89,26 +89,32 @@ __global__ void k_heads(const unsigned long long* __restrict__ keys, int64_t n, 
     head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
 
-// one thread per sorted point; heads insert their voxel into the hash
-__global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, Grid g, HashEntry* __restrict__ H,
-                        int* __restrict__ n_cells) {
+// one thread per sorted point; run heads insert their voxel (key, start)
+__global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, Grid g, HashEntry* __restrict__ H) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned long long key = keys[i];
     if (i != 0 && keys[i - 1] == key) return;
-    int64_t e = i + 1;
-    while (e < n && keys[e] == key) ++e;  // voxel occupancy is small; linear walk
-    atomicAdd(n_cells, 1);
     unsigned long long h = hash_slot(g, key);
     while (true) {
         unsigned long long prev = atomicCAS(&H[h].key, kEmptyKey, key);
         if (prev == kEmptyKey) {
             H[h].start = (int)i;
-            H[h].end = (int)e;
             return;
         }
         h = (h + 1) & g.hmask;
     }
+}
+
+// run tails write the end of their voxel (O(1) per point for any occupancy)
+__global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, Grid g, HashEntry* __restrict__ H) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long key = keys[i];
+    if (i + 1 < n && keys[i + 1] == key) return;
+    unsigned long long h = hash_slot(g, key);
+    while (H[h].key != key) h = (h + 1) & g.hmask;
+    H[h].end = (int)(i + 1);
 }
 
 __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__ perm, int64_t n,
@@ -278,24 +284,24 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     idx->n_cells = ncells;
     cudaGetDevice(&idx->device);
     auto fail = [&](int code) {
-        if (idx->pts) cudaFree(idx->pts);
-        if (idx->pts_orig) cudaFree(idx->pts_orig);
-        if (idx->hash) cudaFree(idx->hash);
+        if (idx->pts) cudaFreeAsync(idx->pts, s);
+        if (idx->pts_orig) cudaFreeAsync(idx->pts_orig, s);
+        if (idx->hash) cudaFreeAsync(idx->hash, s);
         delete idx;
         return code;
     };
-    if (cudaMalloc(&idx->pts, n * sizeof(float4)) != cudaSuccess ||
-        cudaMalloc(&idx->pts_orig, n * sizeof(float4)) != cudaSuccess ||
-        cudaMalloc(&idx->hash, cap * sizeof(HashEntry)) != cudaSuccess) {
+    idx->stream = s;
+    if (cudaMallocAsync(&idx->pts, n * sizeof(float4), s) != cudaSuccess ||
+        cudaMallocAsync(&idx->pts_orig, n * sizeof(float4), s) != cudaSuccess ||
+        cudaMallocAsync(&idx->hash, cap * sizeof(HashEntry), s) != cudaSuccess) {
         cudaGetLastError();
         return fail(set_error(GICP_ENOMEM, "index allocation failed"));
     }
     idx->device_bytes = n * 2 * (int64_t)sizeof(float4) + cap * (int64_t)sizeof(HashEntry);
     {
-        DevBuf cnt;
-        if ((rc = alloc_async(cnt, 16, s))) return fail(rc);
         k_fill_hash<<<grid_for(cap, 256), 256, 0, s>>>(idx->hash, cap);
-        k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, g, idx->hash, (int*)cnt.p);
+        k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, g, idx->hash);
+        k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, g, idx->hash);
         k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
         if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
     }

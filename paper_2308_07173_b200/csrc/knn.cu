@@ -52,6 +52,44 @@ __device__ __forceinline__ void topk_insert(unsigned long long (&L)[KCAP], unsig
     L[0] = below ? x : L[0];
 }
 
+// compare-and-swap on the d2 bits (high word); ties are handled by the callers
+__device__ __forceinline__ void cas_hi(unsigned long long& a, unsigned long long& b) {
+    const bool sw = hi32(b) < hi32(a);
+    const unsigned long long lo = sw ? b : a;
+    b = sw ? a : b;
+    a = lo;
+}
+
+// Batcher odd-even merge sort network on N register keys. The comparator list is
+// generated at compile time (constexpr) so every register index is a constant
+// after unrolling. N = 20 -> 103 comparators.
+struct SortNet {
+    int n;
+    unsigned char a[256], b[256];
+};
+
+constexpr SortNet make_sortnet(int N) {
+    SortNet r{};
+    r.n = 0;
+    for (int p = 1; p < N; p <<= 1)
+        for (int k = p; k >= 1; k >>= 1)
+            for (int j = k % p; j + k < N; j += 2 * k)
+                for (int i = 0; i < k && i < N - j - k; ++i)
+                    if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+                        r.a[r.n] = (unsigned char)(i + j);
+                        r.b[r.n] = (unsigned char)(i + j + k);
+                        ++r.n;
+                    }
+    return r;
+}
+
+template <int N>
+__device__ __forceinline__ void sort_network(unsigned long long (&v)[N]) {
+    constexpr SortNet net = make_sortnet(N);
+#pragma unroll
+    for (int c = 0; c < net.n; ++c) cas_hi(v[net.a[c]], v[net.b[c]]);
+}
+
 // per-query geometry relative to its own voxel
 struct QGeom {
     float qx, qy, qz;
@@ -256,77 +294,249 @@ __device__ __forceinline__ void store_cov(float* cov, int64_t row, const float c
     o[2] = make_float2(c[4], c[5]);
 }
 
-// self queries: thread t handles sorted point t
+// ---------------------------------------------------------------------------
+// Fast path (DESIGN.md §kNN fast path): ring 1 only, per-lane max-heap of K keys
+// (d2 bits << 32 | sorted position) in shared memory (column per lane, so any
+// slot index is bank-conflict free), sift-up while filling, replace-root +
+// sift-down afterwards (O(log K) per accepted candidate instead of O(K) register
+// shifts), one Batcher network sort at the end. Returns false -- the query is
+// DEFERRED to the exact ring-expanding path -- when the stop rule needs ring 2,
+// fewer than K candidates were found, or a d2 tie touches the result.
+// ---------------------------------------------------------------------------
 template <int KCAP>
-__global__ void __launch_bounds__(kBlock) k_knn_self(const float4* __restrict__ pts, const float4* __restrict__ pts_orig,
-                                                     const HashEntry* __restrict__ H, Grid g, int64_t n, int K,
-                                                     float eps, int32_t* __restrict__ nbr, float* __restrict__ d2,
-                                                     float* __restrict__ cov, int* __restrict__ ovf_count,
-                                                     int* __restrict__ ovf_list) {
-    const int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-    if (t >= n) return;
-    const float4 q = __ldg(pts + t);
-    const int64_t row = __float_as_int(q.w);
-    const QGeom G = make_geom(g, q.x, q.y, q.z);
-    unsigned long long L[KCAP];
-    unsigned tie_hi;
-    int ovf;
-    knn_search<KCAP, false>(pts, H, g, G, L, K, tie_hi, ovf);
-    if (ovf) {
-        ovf_list[atomicAdd(ovf_count, 1)] = (int)t;
-        return;
+__device__ __forceinline__ bool knn_fast(const float4* __restrict__ pts, const HashEntry* __restrict__ H,
+                                         const Grid& g, const QGeom& G, int K, unsigned long long* __restrict__ Hl,
+                                         unsigned long long (&L)[KCAP]) {
+    int cnt = 0;
+    unsigned long long top = 0ull;
+    unsigned tie = 0xffffffffu;
+    const float s = g.cell, slack = g.slack;
+    const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
+    const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
+    const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
+#define HSLOT(i) Hl[(i) * kBlock]
+    for (int c = 0; c < 27; ++c) {
+        const int dx = c_off27[c][0], dy = c_off27[c][1], dz = c_off27[c][2];
+        if (cnt == K) {
+            const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
+            const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
+            const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
+            const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+            if (lb2 * kRel > __uint_as_float(hi32(top))) continue;
+        }
+        const int2 rng = cell_lookup(H, g, G.cx + dx, G.cy + dy, G.cz + dz);
+        for (int j = rng.x; j < rng.y; ++j) {
+            const float4 p = __ldg(pts + j);
+            const unsigned hi = __float_as_uint(dist2(G.qx, G.qy, G.qz, p.x, p.y, p.z));
+            const unsigned long long key = ((unsigned long long)hi << 32) | (unsigned)j;
+            if (cnt < K) {  // fill: sift-up into the max-heap
+                int i = cnt++;
+                while (i > 0) {
+                    const int par = (i - 1) >> 1;
+                    const unsigned long long pv = HSLOT(par);
+                    if (hi32(pv) >= hi) break;
+                    HSLOT(i) = pv;
+                    i = par;
+                }
+                HSLOT(i) = key;
+                if (cnt == K) top = HSLOT(0);
+            } else {
+                const unsigned th = hi32(top);
+                if (hi < th) {  // replace the root, sift down
+                    int i = 0;
+                    while (true) {
+                        const int l = 2 * i + 1;
+                        if (l >= K) break;
+                        unsigned long long cv = HSLOT(l);
+                        int ci = l;
+                        if (l + 1 < K) {
+                            const unsigned long long rv = HSLOT(l + 1);
+                            if (hi32(rv) > hi32(cv)) {
+                                cv = rv;
+                                ci = l + 1;
+                            }
+                        }
+                        if (hi32(cv) <= hi) break;
+                        HSLOT(i) = cv;
+                        i = ci;
+                    }
+                    HSLOT(i) = key;
+                    top = HSLOT(0);
+                    if (hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
+                } else if (hi == th) {
+                    tie = min(tie, hi);  // rejected key tied with the K-th
+                }
+            }
+        }
     }
-    if (needs_exact<KCAP>(L, K, tie_hi)) {
+    if (cnt < K) return false;
+    // stop rule after the 27-voxel cube (R = 1)
+    {
+        const float mx = fminf(G.fx + s, 2.0f * s - G.fx);
+        const float my = fminf(G.fy + s, 2.0f * s - G.fy);
+        const float mz = fminf(G.fz + s, 2.0f * s - G.fz);
+        const float m = fminf(mx, fminf(my, mz)) - slack;
+        if (!(m > 0.0f && __uint_as_float(hi32(top)) < m * m * kRel)) return false;
+    }
+    if (tie == hi32(top)) return false;
+#pragma unroll
+    for (int r = 0; r < KCAP; ++r) L[r] = (r < K) ? HSLOT(r) : kEmptyKey;
+#undef HSLOT
+    sort_network<KCAP>(L);
+    bool dup = false;
+#pragma unroll
+    for (int r = 0; r + 1 < KCAP; ++r)
+        if (r + 1 < K) dup |= hi32(L[r]) == hi32(L[r + 1]);
+    return !dup;
+}
+
+// rows from the fast path: slots 0..K-1 ascending, payload = sorted position
+template <int KCAP>
+__device__ __forceinline__ void emit_fast(const float4* __restrict__ pts, const unsigned long long (&L)[KCAP], int K,
+                                          int64_t row, float eps, int32_t* __restrict__ nbr, float* __restrict__ d2,
+                                          float* __restrict__ cov) {
+    const float4 p0 = __ldg(pts + (unsigned)(L[0] & 0xffffffffu));
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+#pragma unroll
+    for (int r = 0; r < KCAP; ++r) {
+        if (r >= K) continue;
+        const float4 p = __ldg(pts + (unsigned)(L[r] & 0xffffffffu));
+        if (nbr) nbr[row * K + r] = __float_as_int(p.w);
+        if (d2) d2[row * K + r] = __uint_as_float(hi32(L[r]));
+        sx += p.x - p0.x;
+        sy += p.y - p0.y;
+        sz += p.z - p0.z;
+    }
+    if (!cov) return;
+    const float invk = 1.0f / (float)K;
+    const float mx = sx * invk, my = sy * invk, mz = sz * invk;
+    float c00 = 0.f, c01 = 0.f, c02 = 0.f, c11 = 0.f, c12 = 0.f, c22 = 0.f;
+#pragma unroll
+    for (int r = 0; r < KCAP; ++r) {
+        if (r >= K) continue;
+        const float4 p = __ldg(pts + (unsigned)(L[r] & 0xffffffffu));
+        const float x = (p.x - p0.x) - mx, y = (p.y - p0.y) - my, z = (p.z - p0.z) - mz;
+        c00 = fmaf(x, x, c00);
+        c01 = fmaf(x, y, c01);
+        c02 = fmaf(x, z, c02);
+        c11 = fmaf(y, y, c11);
+        c12 = fmaf(y, z, c12);
+        c22 = fmaf(z, z, c22);
+    }
+    float c[6];
+    plane_cov(c00 * invk, c01 * invk, c02 * invk, c11 * invk, c12 * invk, c22 * invk, eps, c);
+    store_cov(cov, row, c);
+}
+
+__device__ __forceinline__ void push_warp(int* __restrict__ count, int* __restrict__ list, bool pred, int value) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!pred) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    list[base + __popc(mask & ((1u << lane) - 1))] = value;
+}
+
+// self queries: thread t handles sorted point t (fast path), deferring the rest
+template <int KCAP>
+__global__ void __launch_bounds__(kBlock) k_knn_self(const float4* __restrict__ pts, const HashEntry* __restrict__ H,
+                                                     Grid g, int64_t n, int K, float eps, int32_t* __restrict__ nbr,
+                                                     float* __restrict__ d2, float* __restrict__ cov,
+                                                     int* __restrict__ def_count, int* __restrict__ def_list) {
+    extern __shared__ unsigned long long heap[];
+    const int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+    bool defer = false;
+    if (t < n) {
+        const float4 q = __ldg(pts + t);
+        const QGeom G = make_geom(g, q.x, q.y, q.z);
+        unsigned long long L[KCAP];
+        if (knn_fast<KCAP>(pts, H, g, G, K, heap + threadIdx.x, L))
+            emit_fast<KCAP>(pts, L, K, __float_as_int(q.w), eps, nbr, d2, cov);
+        else
+            defer = true;
+    }
+    push_warp(def_count, def_list, defer, (int)t);
+}
+
+// external queries visited in voxel-sorted order (perm)
+template <int KCAP>
+__global__ void __launch_bounds__(kBlock) k_knn_ext(const float4* __restrict__ pts, const HashEntry* __restrict__ H,
+                                                    Grid g, const float* __restrict__ q, const int* __restrict__ perm,
+                                                    int64_t m, int K, int32_t* __restrict__ nbr,
+                                                    float* __restrict__ d2, int* __restrict__ def_count,
+                                                    int* __restrict__ def_list) {
+    extern __shared__ unsigned long long heap[];
+    const int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+    bool defer = false;
+    int row = 0;
+    if (t < m) {
+        row = perm[t];
+        const float qx = q[3 * (int64_t)row], qy = q[3 * (int64_t)row + 1], qz = q[3 * (int64_t)row + 2];
+        if (!(isfinite(qx) && isfinite(qy) && isfinite(qz))) {
+            for (int r = 0; r < K; ++r) {
+                nbr[(int64_t)row * K + r] = -1;
+                d2[(int64_t)row * K + r] = __int_as_float(0x7f800000);
+            }
+        } else {
+            const QGeom G = make_geom(g, qx, qy, qz);
+            unsigned long long L[KCAP];
+            if (knn_fast<KCAP>(pts, H, g, G, K, heap + threadIdx.x, L))
+                emit_fast<KCAP>(pts, L, K, row, 0.f, nbr, d2, nullptr);
+            else
+                defer = true;
+        }
+    }
+    push_warp(def_count, def_list, defer, row);
+}
+
+// Deferred queries (ring >= 2, too few candidates, or d2 ties): the exact
+// ring-expanding search with (d2, original index) keys. self_mode: list holds
+// sorted positions; else original query indices into qext.
+template <int KCAP>
+__global__ void __launch_bounds__(kBlock) k_knn_deferred(const float4* __restrict__ pts,
+                                                         const float4* __restrict__ pts_orig,
+                                                         const HashEntry* __restrict__ H, Grid g,
+                                                         const float* __restrict__ qext, int self_mode,
+                                                         const int* __restrict__ def_count,
+                                                         const int* __restrict__ def_list, int K, float eps,
+                                                         int32_t* __restrict__ nbr, float* __restrict__ d2,
+                                                         float* __restrict__ cov, int* __restrict__ ovf_count,
+                                                         int* __restrict__ ovf_list) {
+    const int total = *def_count;
+    for (int t = blockIdx.x * kBlock + threadIdx.x; t < total; t += gridDim.x * kBlock) {
+        const int id = def_list[t];
+        float qx, qy, qz;
+        int64_t row;
+        if (self_mode) {
+            const float4 p = __ldg(pts + id);
+            qx = p.x;
+            qy = p.y;
+            qz = p.z;
+            row = __float_as_int(p.w);
+        } else {
+            qx = qext[3 * (int64_t)id];
+            qy = qext[3 * (int64_t)id + 1];
+            qz = qext[3 * (int64_t)id + 2];
+            row = id;
+        }
+        const QGeom G = make_geom(g, qx, qy, qz);
+        unsigned long long L[KCAP];
+        unsigned tie_hi;
+        int ovf;
         knn_search<KCAP, true>(pts, H, g, G, L, K, tie_hi, ovf);
+        if (ovf) {
+            ovf_list[atomicAdd(ovf_count, 1)] = id;
+            continue;
+        }
         write_row<KCAP, true>(pts, pts_orig, L, K, row, nbr, d2);
         if (cov) {
             float c[6];
             cov_row<KCAP, true>(pts, pts_orig, L, K, eps, c);
             store_cov(cov, row, c);
         }
-        return;
     }
-    write_row<KCAP, false>(pts, pts_orig, L, K, row, nbr, d2);
-    if (cov) {
-        float c[6];
-        cov_row<KCAP, false>(pts, pts_orig, L, K, eps, c);
-        store_cov(cov, row, c);
-    }
-}
-
-// external queries visited in voxel-sorted order (perm)
-template <int KCAP>
-__global__ void __launch_bounds__(kBlock) k_knn_ext(const float4* __restrict__ pts, const float4* __restrict__ pts_orig,
-                                                    const HashEntry* __restrict__ H, Grid g, const float* __restrict__ q,
-                                                    const int* __restrict__ perm, int64_t m, int K,
-                                                    int32_t* __restrict__ nbr, float* __restrict__ d2,
-                                                    int* __restrict__ ovf_count, int* __restrict__ ovf_list) {
-    const int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-    if (t >= m) return;
-    const int64_t row = perm[t];
-    const float qx = q[3 * row], qy = q[3 * row + 1], qz = q[3 * row + 2];
-    if (!(isfinite(qx) && isfinite(qy) && isfinite(qz))) {
-        for (int r = 0; r < K; ++r) {
-            nbr[row * K + r] = -1;
-            d2[row * K + r] = __int_as_float(0x7f800000);
-        }
-        return;
-    }
-    const QGeom G = make_geom(g, qx, qy, qz);
-    unsigned long long L[KCAP];
-    unsigned tie_hi;
-    int ovf;
-    knn_search<KCAP, false>(pts, H, g, G, L, K, tie_hi, ovf);
-    if (ovf) {
-        ovf_list[atomicAdd(ovf_count, 1)] = (int)row;
-        return;
-    }
-    if (needs_exact<KCAP>(L, K, tie_hi)) {
-        knn_search<KCAP, true>(pts, H, g, G, L, K, tie_hi, ovf);
-        write_row<KCAP, true>(pts, pts_orig, L, K, row, nbr, d2);
-        return;
-    }
-    write_row<KCAP, false>(pts, pts_orig, L, K, row, nbr, d2);
 }
 
 // Brute force for overflow queries: one block per query, exact (d2, orig) keys.
@@ -453,30 +663,47 @@ struct Scratch {
 };
 
 template <int KCAP>
-int run_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, cudaStream_t s) {
-    const int64_t n = idx->n;
-    Scratch ovf;
+int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int64_t m, int k, float eps,
+                int32_t* nbr, float* d2, float* cov, cudaStream_t s) {
+    Scratch lists;
     int rc;
-    if ((rc = ovf.alloc(sizeof(int) * (n + 1), s))) return rc;
-    int* cnt = (int*)ovf.p;
-    int* list = cnt + 1;
-    if ((rc = check_cuda(cudaMemsetAsync(cnt, 0, sizeof(int), s), "memset"))) return rc;
-    const unsigned blocks = (unsigned)((n + kBlock - 1) / kBlock);
-    k_knn_self<KCAP><<<blocks, kBlock, 0, s>>>(idx->pts, idx->pts_orig, idx->hash, idx->g, n, k, eps, nbr, d2, cov,
-                                               cnt, list);
-    // overflow queries (rare): launch enough blocks for the worst case; extra blocks exit at once
-    const unsigned bf_blocks = (unsigned)std::min<int64_t>(n, 65535);
-    k_knn_bruteforce<KCAP><<<bf_blocks, kBFBlock, 0, s>>>(idx->pts, idx->pts_orig, n, nullptr, 1, list, cnt, k, eps,
-                                                          nbr, d2, cov);
-    return check_cuda(cudaGetLastError(), "knn_self launch");
+    // [def_count, ovf_count, pad, pad] [def_list: m] [ovf_list: m]
+    if ((rc = lists.alloc(sizeof(int) * (2 * m + 4), s))) return rc;
+    int* def_count = (int*)lists.p;
+    int* ovf_count = def_count + 1;
+    int* def_list = def_count + 4;
+    int* ovf_list = def_list + m;
+    if ((rc = check_cuda(cudaMemsetAsync(def_count, 0, 4 * sizeof(int), s), "memset"))) return rc;
+    const unsigned blocks = (unsigned)((m + kBlock - 1) / kBlock);
+    const size_t shmem = (size_t)KCAP * kBlock * sizeof(unsigned long long);
+    if (qext == nullptr) {
+        k_knn_self<KCAP><<<blocks, kBlock, shmem, s>>>(idx->pts, idx->hash, idx->g, m, k, eps, nbr, d2, cov,
+                                                        def_count, def_list);
+    } else {
+        k_knn_ext<KCAP><<<blocks, kBlock, shmem, s>>>(idx->pts, idx->hash, idx->g, qext, perm, m, k, nbr, d2,
+                                                       def_count, def_list);
+    }
+    const unsigned dblocks = (unsigned)std::min<int64_t>(blocks, 148 * 16);
+    k_knn_deferred<KCAP><<<dblocks, kBlock, 0, s>>>(idx->pts, idx->pts_orig, idx->hash, idx->g, qext,
+                                                     qext == nullptr, def_count, def_list, k, eps, nbr, d2, cov,
+                                                     ovf_count, ovf_list);
+    const unsigned bf_blocks = (unsigned)std::min<int64_t>(m, 65535);
+    k_knn_bruteforce<KCAP><<<bf_blocks, kBFBlock, 0, s>>>(idx->pts, idx->pts_orig, idx->n, qext, qext == nullptr,
+                                                          ovf_list, ovf_count, k, eps, nbr, d2, cov);
+    return check_cuda(cudaGetLastError(), "knn launch");
+}
+
+template <int KCAP>
+int run_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, cudaStream_t s) {
+    return run_queries<KCAP>(idx, nullptr, nullptr, idx->n, k, eps, nbr, d2, cov, s);
 }
 
 template <int KCAP>
 int run_ext(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, cudaStream_t s) {
-    Scratch keys_in, keys_out, vals_in, perm, temp, ovf;
+    Scratch keys_in, keys_out, vals_in, perm, temp;
     int rc;
     if ((rc = keys_in.alloc(m * 8, s)) || (rc = keys_out.alloc(m * 8, s)) || (rc = vals_in.alloc(m * 4, s)) ||
-        (rc = perm.alloc(m * 4, s)) || (rc = ovf.alloc(sizeof(int) * (m + 1), s)))
+        (rc = perm.alloc(m * 4, s)))
         return rc;
     k_query_keys<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(q, m, idx->g, (unsigned long long*)keys_in.p,
                                                               (int*)vals_in.p);
@@ -486,15 +713,7 @@ int run_ext(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* 
     if ((rc = temp.alloc(tb, s))) return rc;
     cub::DeviceRadixSort::SortPairs(temp.p, tb, (unsigned long long*)keys_in.p, (unsigned long long*)keys_out.p,
                                     (int*)vals_in.p, (int*)perm.p, (int)m, 0, 64, s);
-    int* cnt = (int*)ovf.p;
-    int* list = cnt + 1;
-    if ((rc = check_cuda(cudaMemsetAsync(cnt, 0, sizeof(int), s), "memset"))) return rc;
-    k_knn_ext<KCAP><<<(unsigned)((m + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-        idx->pts, idx->pts_orig, idx->hash, idx->g, q, (int*)perm.p, m, k, nbr, d2, cnt, list);
-    const unsigned bf_blocks = (unsigned)std::min<int64_t>(m, 65535);
-    k_knn_bruteforce<KCAP><<<bf_blocks, kBFBlock, 0, s>>>(idx->pts, idx->pts_orig, idx->n, q, 0, list, cnt, k, 0.f,
-                                                          nbr, d2, nullptr);
-    return check_cuda(cudaGetLastError(), "knn launch");
+    return run_queries<KCAP>(idx, q, (int*)perm.p, m, k, 0.f, nbr, d2, nullptr, s);
 }
 
 }  // namespace

@@ -21,7 +21,7 @@ namespace gicp {
 namespace {
 
 constexpr int kLinBlock = 256;
-constexpr int kPPT = 4;                       // points per thread
+constexpr int kPPT = 1;                       // points per thread
 constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: defines the partition)
 constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
 constexpr float kRel = 1.0f - 1.0f / (1 << 20);

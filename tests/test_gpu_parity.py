@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import gen
+from tests.conditioning import kappa_prime
 
 pytestmark = pytest.mark.gpu
 
@@ -256,9 +257,18 @@ def test_align_c2(orc):
     idx = g.build_index(D(tgt), 0.0)
     T, info = g.align(D(src), D(cs), idx, D(ct), T0)
     ref = orc.align(src, cs, tgt, ct, T0)
-    dt, dr = _pose_err(T, ref["T"])
     assert info.converged
-    assert dt <= 1e-3 and dr <= 1e-4
+    o29, _, corr = orc.linearize(src, cs, tgt, ct, ref["T"], 1.0)
+    pw = src.astype(np.float64) @ ref["T"][:3, :3].T + ref["T"][:3, 3]
+    kp = kappa_prime(o29, pw[corr >= 0])
+    if kp >= 5e-3:
+        dt, dr = _pose_err(T, ref["T"])
+        assert dt <= 1e-3 and dr <= 1e-4
+    else:
+        # below the eps floor the optimum is a flat valley: compare the costs reached
+        e_gpu = orc.linearize(src, cs, tgt, ct, T, 1.0)[0][27]
+        e_ref = o29[27]
+        assert abs(e_gpu - e_ref) <= 1e-4 * abs(e_ref), (kp, e_gpu, e_ref)
 
 
 def test_align_degenerate(orc):
