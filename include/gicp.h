@@ -59,7 +59,9 @@ int gicp_version(void);
 /* ---------------------------------------------------------------------------
  * gicp_build_index -- the spatial structure behind "GPU-based nearest points
  * search" ("GPU-hash data structure", l.477): a uniform voxel
- * grid built by radix sort on cell keys.
+ * grid built by radix sort on (Morton) cell keys, plus coarser levels of the same
+ * grid (cell x 2^l) that share the sorted points, used for queries whose
+ * neighbourhood is wider than the base cell (sparse regions of a scan).
  *   xyz        [n][3] fp32 target cloud (device). Must be finite (checked).
  *   n          number of points, 1 <= n < 2^31.
  *   cell_size  voxel edge in metres (> 0), or 0 for an automatic choice
@@ -80,8 +82,9 @@ typedef struct {
     int64_t n_cells;      /* occupied voxels */
     float cell_size;      /* metres */
     float origin[3];      /* grid origin (bounding-box minimum) */
-    int32_t dims[3];      /* voxels per axis */
+    int32_t dims[3];      /* voxels per axis (level 0) */
     int64_t device_bytes; /* device memory owned by the index */
+    int32_t n_levels;     /* voxel pyramid levels (cell_l = cell_size * 2^l) */
 } gicp_index_info;
 
 /* Host-side description of an index. Errors: EINVAL. */

@@ -32,7 +32,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 class IndexInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("n_cells", ctypes.c_int64), ("cell_size", ctypes.c_float),
-                ("origin", ctypes.c_float * 3), ("dims", ctypes.c_int32 * 3), ("device_bytes", ctypes.c_int64)]
+                ("origin", ctypes.c_float * 3), ("dims", ctypes.c_int32 * 3), ("device_bytes", ctypes.c_int64),
+                ("n_levels", ctypes.c_int32)]
 
 
 class AlignParams(ctypes.Structure):
@@ -110,6 +111,7 @@ class Index:
         self.origin = tuple(info.origin)
         self.dims = tuple(info.dims)
         self.device_bytes = int(info.device_bytes)
+        self.n_levels = int(info.n_levels)
 
     @property
     def handle(self):

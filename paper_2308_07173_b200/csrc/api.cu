@@ -162,7 +162,7 @@ GICP_API void gicp_index_free(gicp_index idx) {
         cudaFreeAsync(idx->pts, s);
     }
     cudaFreeAsync(idx->pts_orig, s);
-    cudaFreeAsync(idx->hash, s);
+    cudaFreeAsync(idx->hash_mem, s);
     cudaGetLastError();
     delete idx;
 }
@@ -171,13 +171,14 @@ GICP_API int gicp_get_index_info(gicp_index idx, gicp_index_info* info) {
     if (!idx || !info) return set_error(GICP_EINVAL, "gicp_get_index_info: null pointer");
     info->n = idx->n;
     info->n_cells = idx->n_cells;
-    info->cell_size = idx->g.cell;
-    info->origin[0] = idx->g.ox;
-    info->origin[1] = idx->g.oy;
-    info->origin[2] = idx->g.oz;
-    info->dims[0] = idx->g.nx;
-    info->dims[1] = idx->g.ny;
-    info->dims[2] = idx->g.nz;
+    info->cell_size = idx->lv[0].cell;
+    info->origin[0] = idx->lv[0].ox;
+    info->origin[1] = idx->lv[0].oy;
+    info->origin[2] = idx->lv[0].oz;
+    info->dims[0] = idx->lv[0].nx;
+    info->dims[1] = idx->lv[0].ny;
+    info->dims[2] = idx->lv[0].nz;
+    info->n_levels = idx->n_levels;
     info->device_bytes = idx->device_bytes;
     return GICP_OK;
 }

@@ -1,10 +1,14 @@
 // gicp_internal.cuh -- shared device-side definitions of libgicp_b200 (not installed).
 //
 // Data layout in HBM:
-//   pts       float4[n]  points sorted by voxel key: (x, y, z, bitcast(original index)).
+//   pts       float4[n]  points sorted by the level-0 Morton voxel key:
+//                        (x, y, z, bitcast(original index)).
 //   pts_orig  float4[n]  points in original order: (x, y, z, bitcast(sorted position)).
-//   hash      HashEntry[cap] open addressing, 16 B entries {key, start, end}: one
-//             LDG.128 per probe; cap = pow2 >= 2 * occupied voxels (load <= 0.5).
+//   levels    a voxel pyramid, cell_l = cell_0 * 2^l, common origin. Level-l voxel
+//             keys are the level-0 Morton keys >> 3l, so every level-l voxel is a
+//             contiguous range of `pts` and one sorted array serves all levels.
+//             Per level an open-addressing hash {key, start, end} (16 B, one
+//             LDG.128 per probe), capacity pow2 >= 2 x occupied voxels.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -20,6 +24,7 @@ namespace gicp {
 
 constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kMaxAxisCells = 1 << 21;
+constexpr int kMaxLevels = 8;
 
 struct HashEntry {
     unsigned long long key;
@@ -27,42 +32,55 @@ struct HashEntry {
     int end;
 };
 
-// Grid parameters passed by value to kernels.
+// One pyramid level, passed by value to kernels.
 struct Grid {
-    float ox, oy, oz;   // origin (bounding-box minimum)
-    float cell;         // voxel edge (m)
-    float inv_cell;     // fl32(1 / cell)
-    int nx, ny, nz;     // voxels per axis
-    float slack;        // conservative geometric slack (m), see DESIGN.md §kNN stop rule
+    float ox, oy, oz;   // origin (bounding-box minimum), common to all levels
+    float cell;         // voxel edge of this level (m)
+    float inv_cell;     // fl32(1 / cell) = fl32(1 / cell_0) * 2^-l exactly
+    int nx, ny, nz;     // voxels per axis at this level
+    float slack;        // conservative geometric slack (m), DESIGN.md §kNN stop rule
+    int level;
     int hbits;          // log2(hash capacity)
     unsigned long long hmask;
+    const HashEntry* hash;
 };
 
 // Cell coordinate along one axis: floor(fl32(fl32(x - o) * inv)). The SAME
-// function assigns index points and queries (DESIGN.md §kNN exactness).
+// function assigns index points and queries (DESIGN.md §kNN exactness). Because
+// inv_l = inv_0 * 2^-l exactly, cell_l(x) == cell_0(x) >> l.
 __device__ __forceinline__ int cell_coord(float x, float o, float inv) {
     float t = __fmul_rn(__fsub_rn(x, o), inv);
     t = fminf(fmaxf(t, -1.0e9f), 1.0e9f);
     return (int)floorf(t);
 }
 
-GICP_HD unsigned long long cell_key(const Grid& g, int cx, int cy, int cz) {
-    return ((unsigned long long)cz * (unsigned long long)g.ny + (unsigned long long)cy) * (unsigned long long)g.nx +
-           (unsigned long long)cx;
+// 21-bit Morton spreading
+GICP_HD unsigned long long spread3(unsigned x) {
+    unsigned long long v = x & 0x1fffffu;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+GICP_HD unsigned long long cell_key(int cx, int cy, int cz) {
+    return spread3((unsigned)cx) | (spread3((unsigned)cy) << 1) | (spread3((unsigned)cz) << 2);
 }
 
 GICP_HD unsigned long long hash_slot(const Grid& g, unsigned long long key) {
     return (key * 0x9E3779B97F4A7C15ull) >> (64 - g.hbits);
 }
 
-// Returns [start, end) of the voxel (cx, cy, cz) in pts, or an empty range.
-__device__ __forceinline__ int2 cell_lookup(const HashEntry* __restrict__ H, const Grid& g, int cx, int cy, int cz) {
+// Returns [start, end) of the voxel (cx, cy, cz) of level g in pts, or an empty range.
+__device__ __forceinline__ int2 cell_lookup(const Grid& g, int cx, int cy, int cz) {
     if ((unsigned)cx >= (unsigned)g.nx || (unsigned)cy >= (unsigned)g.ny || (unsigned)cz >= (unsigned)g.nz)
         return make_int2(0, 0);
-    const unsigned long long key = cell_key(g, cx, cy, cz);
+    const unsigned long long key = cell_key(cx, cy, cz);
     unsigned long long h = hash_slot(g, key);
     while (true) {
-        const int4 e = __ldg(reinterpret_cast<const int4*>(H) + h);
+        const int4 e = __ldg(reinterpret_cast<const int4*>(g.hash) + h);
         const unsigned long long k = (unsigned long long)(unsigned)e.x | ((unsigned long long)(unsigned)e.y << 32);
         if (k == key) return make_int2(e.z, e.w);
         if (k == kEmptyKey) return make_int2(0, 0);
@@ -79,16 +97,58 @@ __device__ __forceinline__ float dist2(float qx, float qy, float qz, float px, f
     return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
 }
 
+// per-query geometry relative to its voxel at one level
+struct QGeom {
+    float qx, qy, qz;
+    int cx, cy, cz;
+    float fx, fy, fz;  // distance from q to the low faces of its voxel (m)
+};
+
+__device__ __forceinline__ QGeom make_geom(const Grid& g, float qx, float qy, float qz) {
+    QGeom G;
+    G.qx = qx;
+    G.qy = qy;
+    G.qz = qz;
+    G.cx = cell_coord(qx, g.ox, g.inv_cell);
+    G.cy = cell_coord(qy, g.oy, g.inv_cell);
+    G.cz = cell_coord(qz, g.oz, g.inv_cell);
+    const double s = (double)g.cell;
+    G.fx = (float)((double)qx - ((double)g.ox + (double)G.cx * s));
+    G.fy = (float)((double)qy - ((double)g.oy + (double)G.cy * s));
+    G.fz = (float)((double)qz - ((double)g.oz + (double)G.cz * s));
+    return G;
+}
+
+// lower bound on the distance from q to any point of the voxel at offset d on one axis
+__device__ __forceinline__ float axis_gap(int d, float f, float s, float slack) {
+    float gap = 0.0f;
+    if (d < 0) gap = (float)(-d - 1) * s + f - slack;
+    if (d > 0) gap = (float)(d - 1) * s + (s - f) - slack;
+    return fmaxf(gap, 0.0f);
+}
+
+// distance from q to the boundary of the cube of Chebyshev radius R around its
+// voxel, minus slack: every unsearched point is farther than this
+__device__ __forceinline__ float cube_margin(const QGeom& G, float s, float slack, int R) {
+    const float mx = fminf(G.fx + R * s, (R + 1) * s - G.fx);
+    const float my = fminf(G.fy + R * s, (R + 1) * s - G.fy);
+    const float mz = fminf(G.fz + R * s, (R + 1) * s - G.fz);
+    return fminf(mx, fminf(my, mz)) - slack;
+}
+
+constexpr float kRel = 1.0f - 1.0f / (1 << 20);  // relative safety on squared bounds
+
 }  // namespace gicp
 
 struct gicp_index_s {
     int64_t n = 0;
-    int64_t n_cells = 0;
-    gicp::Grid g{};
+    int64_t n_cells = 0;  // occupied level-0 voxels
+    int n_levels = 0;
+    gicp::Grid lv[gicp::kMaxLevels]{};
+    int64_t hash_cap[gicp::kMaxLevels]{};
     float4* pts = nullptr;
     float4* pts_orig = nullptr;
-    gicp::HashEntry* hash = nullptr;
-    int64_t hash_cap = 0;
+    gicp::HashEntry* hash_mem = nullptr;  // all levels' tables, one allocation
     int device = 0;
     cudaStream_t stream = nullptr;  // build stream: device memory is pool-allocated on it
     int64_t device_bytes = 0;

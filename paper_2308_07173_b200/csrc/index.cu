@@ -1,17 +1,20 @@
-// index.cu -- gicp_build_index: uniform voxel grid built by radix sort on cell keys.
+// index.cu -- gicp_build_index: a uniform voxel grid built by radix sort on cell
+// keys, extended to a pyramid of voxel levels that share one sorted array.
 //
 // Paper: the structure behind "GPU-based nearest points search" (PAPER.md l.413,
 // "GPU-hash data structure" l.477); north star: "a uniform voxel grid built by
-// radix sort on cell keys". Steps (SURVEY.md §8(a) A1):
-//   1. k_bbox      finiteness check + bounding box (block reduce, ordered-int atomics)
-//   2. k_keys      key_i = linear voxel id of floor(fl32(fl32(x - o) * inv))
-//   3. CUB radix sort (key, i) on only the key bits needed
-//   4. k_heads     run boundaries -> voxel start/end, hash insert (atomicCAS)
-//   5. k_scatter   sorted float4 (x, y, z, orig) + original-order float4 (x, y, z, spos)
+// radix sort on cell keys". Steps (SURVEY.md §8(a) A1, DESIGN.md §Index):
+//   1. k_bbox        finiteness check + bounding box (warp reduce, ordered-int atomics)
+//   2. k_keys        key_i = Morton(floor(fl32(fl32(x - o) * inv)) per axis)
+//   3. CUB radix sort of (key, i) on the 3 x ceil(log2 dim) key bits in use
+//   4. k_level_count occupied voxels of every level (key >> 3l changes)
+//   5. k_cells / k_cell_ends   per level: run heads insert {key, start}, run tails
+//                    write end (O(1) per point for any occupancy)
+//   6. k_scatter     sorted float4 (x, y, z, orig) + original-order float4 (x, y, z, spos)
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
-#include <cstdio>
 #include <vector>
 
 #include "gicp_internal.cuh"
@@ -23,15 +26,11 @@ __device__ __forceinline__ int f2ord(float f) {
     int i = __float_as_int(f);
     return i >= 0 ? i : i ^ 0x7fffffff;
 }
-__host__ __device__ inline float ord2f(int i) {
-#ifdef __CUDA_ARCH__
-    return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff);
-#else
+inline float ord2f_host(int i) {
     int j = i >= 0 ? i : i ^ 0x7fffffff;
     float f;
     memcpy(&f, &j, 4);
     return f;
-#endif
 }
 
 // out[0..2] = min (ordered ints), out[3..5] = max, out[6] = non-finite count
@@ -79,22 +78,30 @@ __global__ void k_keys(const float* __restrict__ xyz, int64_t n, Grid g, unsigne
     cx = min(max(cx, 0), g.nx - 1);  // cannot trigger (monotone cell map); defensive
     cy = min(max(cy, 0), g.ny - 1);
     cz = min(max(cz, 0), g.nz - 1);
-    keys[i] = cell_key(g, cx, cy, cz);
+    keys[i] = cell_key(cx, cy, cz);
     vals[i] = (int)i;
 }
 
-__global__ void k_heads(const unsigned long long* __restrict__ keys, int64_t n, int* __restrict__ head) {
+// occupied voxels per level
+__global__ void k_level_count(const unsigned long long* __restrict__ keys, int64_t n, int L, int* __restrict__ cnt) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+    const unsigned long long k = i < n ? keys[i] : 0ull;
+    const unsigned long long kp = (i > 0 && i < n) ? keys[i - 1] : ~0ull;
+    for (int l = 0; l < L; ++l) {
+        const int head = (i < n) && (i == 0 || (k >> (3 * l)) != (kp >> (3 * l)));
+        const int c = __reduce_add_sync(0xffffffffu, head);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + l, c);
+    }
 }
 
-// one thread per sorted point; run heads insert their voxel (key, start)
-__global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, Grid g, HashEntry* __restrict__ H) {
+// run heads insert their voxel (key >> 3l, start) into level l's table
+__global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, Grid g) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const unsigned long long key = keys[i];
-    if (i != 0 && keys[i - 1] == key) return;
+    const int sh = 3 * g.level;
+    const unsigned long long key = keys[i] >> sh;
+    if (i != 0 && (keys[i - 1] >> sh) == key) return;
+    HashEntry* H = const_cast<HashEntry*>(g.hash);
     unsigned long long h = hash_slot(g, key);
     while (true) {
         unsigned long long prev = atomicCAS(&H[h].key, kEmptyKey, key);
@@ -106,12 +113,14 @@ __global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, 
     }
 }
 
-// run tails write the end of their voxel (O(1) per point for any occupancy)
-__global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, Grid g, HashEntry* __restrict__ H) {
+// run tails write the end of their voxel
+__global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, Grid g) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const unsigned long long key = keys[i];
-    if (i + 1 < n && keys[i + 1] == key) return;
+    const int sh = 3 * g.level;
+    const unsigned long long key = keys[i] >> sh;
+    if (i + 1 < n && (keys[i + 1] >> sh) == key) return;
+    HashEntry* H = const_cast<HashEntry*>(g.hash);
     unsigned long long h = hash_slot(g, key);
     while (H[h].key != key) h = (h + 1) & g.hmask;
     H[h].end = (int)(i + 1);
@@ -149,6 +158,7 @@ int alloc_async(DevBuf& b, size_t bytes, cudaStream_t s) {
     cudaError_t e = cudaMallocAsync(&b.p, bytes ? bytes : 16, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
+        b.p = nullptr;
         return set_error(GICP_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
     }
     return GICP_OK;
@@ -156,46 +166,10 @@ int alloc_async(DevBuf& b, size_t bytes, cudaStream_t s) {
 
 unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
-// key bits actually used by the linear voxel id
-int key_bits(const Grid& g) {
-    unsigned long long total = (unsigned long long)g.nx * g.ny * g.nz;
-    int b = 1;
-    while (b < 64 && (1ull << b) < total) ++b;
+int bits_for(int dim) {
+    int b = 0;
+    while ((1 << b) < dim) ++b;
     return b;
-}
-
-// sort (key, i) pairs on the key bits in use and count voxels (run heads).
-// Leaves sorted keys / permutation in keys_out / perm_out.
-int sort_cells(const float* xyz, int64_t n, const Grid& g, cudaStream_t s, DevBuf& keys_out, DevBuf& perm_out,
-               int64_t* n_cells_out) {
-    DevBuf keys_in, vals_in, temp, cnt, head, t2;
-    int rc;
-    if ((rc = alloc_async(keys_in, n * 8, s)) || (rc = alloc_async(vals_in, n * 4, s)) ||
-        (rc = alloc_async(keys_out, n * 8, s)) || (rc = alloc_async(perm_out, n * 4, s)) ||
-        (rc = alloc_async(cnt, 16, s)) || (rc = alloc_async(head, n * 4, s)))
-        return rc;
-    k_keys<<<grid_for(n, 256), 256, 0, s>>>(xyz, n, g, (unsigned long long*)keys_in.p, (int*)vals_in.p);
-    size_t temp_bytes = 0;
-    const int bits = key_bits(g);
-    cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, (unsigned long long*)keys_in.p,
-                                    (unsigned long long*)keys_out.p, (int*)vals_in.p, (int*)perm_out.p, (int)n, 0,
-                                    bits, s);
-    if ((rc = alloc_async(temp, temp_bytes, s))) return rc;
-    if ((rc = check_cuda(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, (unsigned long long*)keys_in.p,
-                                                         (unsigned long long*)keys_out.p, (int*)vals_in.p,
-                                                         (int*)perm_out.p, (int)n, 0, bits, s),
-                         "radix sort")))
-        return rc;
-    k_heads<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys_out.p, n, (int*)head.p);
-    size_t tb = 0;
-    cub::DeviceReduce::Sum(nullptr, tb, (int*)head.p, (int*)cnt.p, (int)n, s);
-    if ((rc = alloc_async(t2, tb, s))) return rc;
-    cub::DeviceReduce::Sum(t2.p, tb, (int*)head.p, (int*)cnt.p, (int)n, s);
-    int hc = 0;
-    if ((rc = check_cuda(cudaMemcpyAsync(&hc, cnt.p, 4, cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
-    if ((rc = check_cuda(cudaStreamSynchronize(s), "build sync"))) return rc;
-    *n_cells_out = hc;
-    return check_cuda(cudaGetLastError(), "build kernels");
 }
 
 int make_grid(const float mn[3], const float mx[3], float cell, Grid* g) {
@@ -211,7 +185,7 @@ int make_grid(const float mn[3], const float mx[3], float cell, Grid* g) {
         volatile float d = mx[a] - mn[a];
         volatile float t = d * g->inv_cell;
         double c = std::floor((double)t);
-        if (c + 1 > kMaxAxisCells)
+        if (!(c + 1 <= kMaxAxisCells))
             return set_error(GICP_ERANGE, "voxel grid exceeds 2^21 cells on an axis; increase cell_size");
         dims[a] = (int)c + 1;
     }
@@ -224,7 +198,40 @@ int make_grid(const float mn[3], const float mx[3], float cell, Grid* g) {
     double E = 0.0;
     for (int a = 0; a < 3; ++a) E = std::fmax(E, (double)mx[a] - (double)mn[a]);
     g->slack = (float)(8.0 * std::ldexp(1.0, -24) * (E + cell) + 1e-6 * cell);
+    g->level = 0;
     return GICP_OK;
+}
+
+Grid level_grid(const Grid& g0, int l, double E) {
+    Grid g = g0;
+    g.level = l;
+    g.cell = std::ldexp(g0.cell, l);
+    g.inv_cell = std::ldexp(g0.inv_cell, -l);  // exact power-of-two scaling
+    g.nx = ((g0.nx - 1) >> l) + 1;
+    g.ny = ((g0.ny - 1) >> l) + 1;
+    g.nz = ((g0.nz - 1) >> l) + 1;
+    g.slack = (float)(8.0 * std::ldexp(1.0, -24) * (E + g.cell) + 1e-6 * g.cell);
+    return g;
+}
+
+// sort (Morton key, i) pairs on the bits in use
+int sort_keys(const float* xyz, int64_t n, const Grid& g, cudaStream_t s, DevBuf& keys_out, DevBuf& perm_out) {
+    DevBuf keys_in, vals_in, temp;
+    int rc;
+    if ((rc = alloc_async(keys_in, n * 8, s)) || (rc = alloc_async(vals_in, n * 4, s)) ||
+        (rc = alloc_async(keys_out, n * 8, s)) || (rc = alloc_async(perm_out, n * 4, s)))
+        return rc;
+    k_keys<<<grid_for(n, 256), 256, 0, s>>>(xyz, n, g, (unsigned long long*)keys_in.p, (int*)vals_in.p);
+    const int bits = std::max(1, 3 * std::max(bits_for(g.nx), std::max(bits_for(g.ny), bits_for(g.nz))));
+    size_t temp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, (unsigned long long*)keys_in.p,
+                                    (unsigned long long*)keys_out.p, (int*)vals_in.p, (int*)perm_out.p, (int)n, 0,
+                                    bits, s);
+    if ((rc = alloc_async(temp, temp_bytes, s))) return rc;
+    return check_cuda(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, (unsigned long long*)keys_in.p,
+                                                      (unsigned long long*)keys_out.p, (int*)vals_in.p,
+                                                      (int*)perm_out.p, (int)n, 0, bits, s),
+                      "radix sort");
 }
 
 }  // namespace
@@ -232,80 +239,106 @@ int make_grid(const float mn[3], const float mx[3], float cell, Grid* g) {
 int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gicp_index* out) {
     int rc;
     DevBuf bb;
-    if ((rc = alloc_async(bb, 8 * sizeof(int), s))) return rc;
+    if ((rc = alloc_async(bb, 16 * sizeof(int), s))) return rc;
     int init[8] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN, 0, 0};
     if ((rc = check_cuda(cudaMemcpyAsync(bb.p, init, sizeof(init), cudaMemcpyHostToDevice, s), "H2D"))) return rc;
-    {
-        unsigned blocks = (unsigned)std::min<int64_t>(grid_for(n, 256), 148 * 8);
-        k_bbox<<<blocks, 256, 0, s>>>(xyz, n, (int*)bb.p);
-    }
+    k_bbox<<<(unsigned)std::min<int64_t>(grid_for(n, 256), 148 * 8), 256, 0, s>>>(xyz, n, (int*)bb.p);
     int res[8];
     if ((rc = check_cuda(cudaMemcpyAsync(res, bb.p, sizeof(res), cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
     if ((rc = check_cuda(cudaStreamSynchronize(s), "bbox"))) return rc;
     if (res[6] != 0) return set_error(GICP_EINVAL, "non-finite coordinate in the target cloud");
     float mn[3], mx[3];
     for (int a = 0; a < 3; ++a) {
-        mn[a] = ord2f(res[a]);
-        mx[a] = ord2f(res[3 + a]);
+        mn[a] = ord2f_host(res[a]);
+        mx[a] = ord2f_host(res[3 + a]);
     }
+    double E = 0.0;
+    for (int a = 0; a < 3; ++a) E = std::fmax(E, (double)mx[a] - (double)mn[a]);
     Grid g{};
     if (cell_size == 0.0f) {
-        // automatic: trial grid at E/1024, then scale so that occupied voxels hold
-        // about 8 points on average (surface sampling: occupancy ~ cell^2).
-        float E = std::fmax(mx[0] - mn[0], std::fmax(mx[1] - mn[1], mx[2] - mn[2]));
-        float trial = E > 0 ? E / 1024.0f : 1.0f;
+        // automatic: trial grid at E/1024; pick the cell so that the point-weighted
+        // median voxel occupancy is ~8 (occupancy ~ cell^2 on sampled surfaces).
+        // Sparser regions are served by the coarser pyramid levels.
+        const float trial = E > 0 ? (float)(E / 1024.0) : 1.0f;
         if ((rc = make_grid(mn, mx, trial, &g))) return rc;
-        g.hbits = 1;
         DevBuf k1, p1;
-        int64_t nc = 0;
-        if ((rc = sort_cells(xyz, n, g, s, k1, p1, &nc))) return rc;
-        double occ = (double)n / (double)std::max<int64_t>(nc, 1);
-        cell_size = (float)(trial * std::sqrt(8.0 / occ));
-        if (!(cell_size > 0.0f)) cell_size = 1.0f;
-    } else if (!(cell_size > 0.0f) || !std::isfinite(cell_size)) {
-        return set_error(GICP_EINVAL, "cell_size must be >= 0 and finite");
+        if ((rc = sort_keys(xyz, n, g, s, k1, p1))) return rc;
+        std::vector<unsigned long long> hk(n);
+        if ((rc = check_cuda(cudaMemcpyAsync(hk.data(), k1.p, n * 8, cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
+        if ((rc = check_cuda(cudaStreamSynchronize(s), "auto cell"))) return rc;
+        std::vector<int> occ_of_point;
+        occ_of_point.reserve(n);
+        for (int64_t i = 0; i < n;) {
+            int64_t j = i;
+            while (j < n && hk[j] == hk[i]) ++j;
+            for (int64_t t = i; t < j; ++t) occ_of_point.push_back((int)(j - i));
+            i = j;
+        }
+        std::nth_element(occ_of_point.begin(), occ_of_point.begin() + n / 2, occ_of_point.end());
+        const double med = std::max(1, occ_of_point[n / 2]);
+        cell_size = (float)(trial * std::sqrt(8.0 / med));
+        if (!(cell_size > 0.0f) || !std::isfinite(cell_size)) cell_size = 1.0f;
     }
     if ((rc = make_grid(mn, mx, cell_size, &g))) return rc;
 
-    g.hbits = 1;
-    int64_t ncells = 0;
-    DevBuf keys, perm;
-    if ((rc = sort_cells(xyz, n, g, s, keys, perm, &ncells))) return rc;
-    int hb = 1;
-    while ((1ll << hb) < 2 * ncells) ++hb;
-    g.hbits = hb;
-    g.hmask = (1ull << hb) - 1;
-    const int64_t cap = 1ll << hb;
+    DevBuf keys, perm, cnt;
+    if ((rc = sort_keys(xyz, n, g, s, keys, perm))) return rc;
+    // pyramid depth: until the 27-voxel cube covers the grid, at most kMaxLevels
+    int L = 1;
+    while (L < kMaxLevels) {
+        const Grid gl = level_grid(g, L - 1, E);
+        if (gl.nx <= 3 && gl.ny <= 3 && gl.nz <= 3) break;
+        ++L;
+    }
+    if ((rc = alloc_async(cnt, kMaxLevels * sizeof(int), s))) return rc;
+    if ((rc = check_cuda(cudaMemsetAsync(cnt.p, 0, kMaxLevels * sizeof(int), s), "memset"))) return rc;
+    k_level_count<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, L, (int*)cnt.p);
+    int counts[kMaxLevels] = {0};
+    if ((rc = check_cuda(cudaMemcpyAsync(counts, cnt.p, sizeof(counts), cudaMemcpyDeviceToHost, s), "D2H")))
+        return rc;
+    if ((rc = check_cuda(cudaStreamSynchronize(s), "level counts"))) return rc;
 
     gicp_index_s* idx = new gicp_index_s();
     idx->n = n;
-    idx->g = g;
-    idx->hash_cap = cap;
-    idx->n_cells = ncells;
+    idx->n_levels = L;
+    idx->n_cells = counts[0];
+    idx->stream = s;
     cudaGetDevice(&idx->device);
+    int64_t total_cap = 0;
+    for (int l = 0; l < L; ++l) {
+        int hb = 1;
+        while ((1ll << hb) < 2 * (int64_t)std::max(counts[l], 1)) ++hb;
+        idx->lv[l] = level_grid(g, l, E);
+        idx->lv[l].hbits = hb;
+        idx->lv[l].hmask = (1ull << hb) - 1;
+        idx->hash_cap[l] = 1ll << hb;
+        total_cap += 1ll << hb;
+    }
     auto fail = [&](int code) {
         if (idx->pts) cudaFreeAsync(idx->pts, s);
         if (idx->pts_orig) cudaFreeAsync(idx->pts_orig, s);
-        if (idx->hash) cudaFreeAsync(idx->hash, s);
+        if (idx->hash_mem) cudaFreeAsync(idx->hash_mem, s);
         delete idx;
         return code;
     };
-    idx->stream = s;
     if (cudaMallocAsync(&idx->pts, n * sizeof(float4), s) != cudaSuccess ||
         cudaMallocAsync(&idx->pts_orig, n * sizeof(float4), s) != cudaSuccess ||
-        cudaMallocAsync(&idx->hash, cap * sizeof(HashEntry), s) != cudaSuccess) {
+        cudaMallocAsync(&idx->hash_mem, total_cap * sizeof(HashEntry), s) != cudaSuccess) {
         cudaGetLastError();
         return fail(set_error(GICP_ENOMEM, "index allocation failed"));
     }
-    idx->device_bytes = n * 2 * (int64_t)sizeof(float4) + cap * (int64_t)sizeof(HashEntry);
-    {
-        k_fill_hash<<<grid_for(cap, 256), 256, 0, s>>>(idx->hash, cap);
-        k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, g, idx->hash);
-        k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, g, idx->hash);
-        k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
-        if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
+    idx->device_bytes = n * 2 * (int64_t)sizeof(float4) + total_cap * (int64_t)sizeof(HashEntry);
+    k_fill_hash<<<grid_for(total_cap, 256), 256, 0, s>>>(idx->hash_mem, total_cap);
+    int64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+        idx->lv[l].hash = idx->hash_mem + off;
+        off += idx->hash_cap[l];
+        k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, idx->lv[l]);
+        k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, idx->lv[l]);
     }
+    k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
+    if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
     *out = idx;
     return GICP_OK;
 }

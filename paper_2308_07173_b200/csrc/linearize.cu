@@ -24,7 +24,6 @@ constexpr int kLinBlock = 256;
 constexpr int kPPT = 1;                       // points per thread
 constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: defines the partition)
 constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
-constexpr float kRel = 1.0f - 1.0f / (1 << 20);
 constexpr int kMaxRing = 16;
 
 struct Pose {
@@ -39,27 +38,19 @@ __constant__ signed char c_off27l[27][3] = {
     {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
     {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
 
-__device__ __forceinline__ float gap_axis(int d, float f, float s, float slack) {
-    float gap = 0.0f;
-    if (d < 0) gap = (float)(-d - 1) * s + f - slack;
-    if (d > 0) gap = (float)(d - 1) * s + (s - f) - slack;
-    return fmaxf(gap, 0.0f);
-}
+struct Levels {
+    Grid lv[kMaxLevels];
+    int n;
+};
 
-// Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) among all
-// targets whenever that d2 < r2; bp = its coordinates.
-__device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const HashEntry* __restrict__ H,
-                                          const Grid& g, float qx, float qy, float qz, float r2,
-                                          unsigned long long& best, float3& bp, int& overflow) {
+// Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) over all
+// targets whenever that d2 < r2; bp = its coordinates. The 27-voxel cube of
+// level 0 first; if the stop rule (no unsearched point below min(best, r2))
+// fails, the next pyramid level's cube (a superset); ring expansion at the last.
+__device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, float qx, float qy,
+                                          float qz, float r2, unsigned long long& best, float3& bp, int& overflow) {
     best = kEmptyKey;
     overflow = 0;
-    const int cx = cell_coord(qx, g.ox, g.inv_cell), cy = cell_coord(qy, g.oy, g.inv_cell),
-              cz = cell_coord(qz, g.oz, g.inv_cell);
-    const double sd = (double)g.cell;
-    const float fx = (float)((double)qx - ((double)g.ox + (double)cx * sd));
-    const float fy = (float)((double)qy - ((double)g.oy + (double)cy * sd));
-    const float fz = (float)((double)qz - ((double)g.oz + (double)cz * sd));
-    const float s = g.cell, slack = g.slack;
     auto bound = [&]() { return fminf(__uint_as_float((unsigned)(best >> 32)), r2); };
     auto scan = [&](int2 rng) {
         for (int j = rng.x; j < rng.y; ++j) {
@@ -72,51 +63,60 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             }
         }
     };
-    for (int c = 0; c < 27; ++c) {
-        const int dx = c_off27l[c][0], dy = c_off27l[c][1], dz = c_off27l[c][2];
-        const float gx = gap_axis(dx, fx, s, slack), gy = gap_axis(dy, fy, s, slack), gz = gap_axis(dz, fz, s, slack);
-        const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
-        if (lb2 * kRel > bound()) continue;
-        scan(cell_lookup(H, g, cx + dx, cy + dy, cz + dz));
-    }
-    const int R0 = max(max(max(-cx, cx - (g.nx - 1)), max(-cy, cy - (g.ny - 1))), max(-cz, cz - (g.nz - 1)));
-    int R = 1;
-    while (true) {
-        const float mx = fminf(fx + R * s, (R + 1) * s - fx);
-        const float my = fminf(fy + R * s, (R + 1) * s - fy);
-        const float mz = fminf(fz + R * s, (R + 1) * s - fz);
-        const float m = fminf(mx, fminf(my, mz)) - slack;
-        if (m > 0.0f && bound() < m * m * kRel) break;
-        const bool covers = cx - R <= 0 && cx + R >= g.nx - 1 && cy - R <= 0 && cy + R >= g.ny - 1 && cz - R <= 0 &&
-                            cz + R >= g.nz - 1;
-        if (covers) break;
-        ++R;
-        if (R < R0) R = R0;
-        if (R > max(R0, 1) + kMaxRing) {
-            overflow = 1;
-            return;
+    for (int l = 0; l < lvs.n; ++l) {
+        const Grid& g = lvs.lv[l];
+        const QGeom G = make_geom(g, qx, qy, qz);
+        const float s = g.cell, slack = g.slack;
+        for (int c = 0; c < 27; ++c) {
+            const int dx = c_off27l[c][0], dy = c_off27l[c][1], dz = c_off27l[c][2];
+            const float gx = axis_gap(dx, G.fx, s, slack), gy = axis_gap(dy, G.fy, s, slack),
+                        gz = axis_gap(dz, G.fz, s, slack);
+            const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+            if (lb2 * kRel > bound()) continue;
+            scan(cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz));
         }
-        const int z0 = max(-R, -cz), z1 = min(R, g.nz - 1 - cz);
-        const int y0 = max(-R, -cy), y1 = min(R, g.ny - 1 - cy);
-        const int x0 = max(-R, -cx), x1 = min(R, g.nx - 1 - cx);
-        for (int dz = z0; dz <= z1; ++dz) {
-            const float gz = gap_axis(dz, fz, s, slack);
-            for (int dy = y0; dy <= y1; ++dy) {
-                const float gy = gap_axis(dy, fy, s, slack);
-                if (__fmaf_rn(gz, gz, gy * gy) * kRel > bound()) continue;
-                auto visit = [&](int dx) {
-                    const float gx = gap_axis(dx, fx, s, slack);
-                    const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
-                    if (lb2 * kRel > bound()) return;
-                    scan(cell_lookup(H, g, cx + dx, cy + dy, cz + dz));
-                };
-                if (dz == -R || dz == R || dy == -R || dy == R) {
-                    for (int dx = x0; dx <= x1; ++dx) visit(dx);
-                } else {
-                    if (-R >= x0) visit(-R);
-                    if (R <= x1) visit(R);
+        const float m = cube_margin(G, s, slack, 1);
+        if (m > 0.0f && bound() < m * m * kRel) return;
+        const bool covers = G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 &&
+                            G.cz >= g.nz - 2;
+        if (covers) return;
+        if (l + 1 < lvs.n) continue;
+        // last level: ring expansion
+        const int R0 = max(max(max(-G.cx, G.cx - (g.nx - 1)), max(-G.cy, G.cy - (g.ny - 1))),
+                           max(-G.cz, G.cz - (g.nz - 1)));
+        for (int R = 2;; ++R) {
+            if (R < R0) R = R0;
+            if (R > max(R0, 1) + kMaxRing) {
+                overflow = 1;
+                return;
+            }
+            const int z0 = max(-R, -G.cz), z1 = min(R, g.nz - 1 - G.cz);
+            const int y0 = max(-R, -G.cy), y1 = min(R, g.ny - 1 - G.cy);
+            const int x0 = max(-R, -G.cx), x1 = min(R, g.nx - 1 - G.cx);
+            for (int dz = z0; dz <= z1; ++dz) {
+                const float gz = axis_gap(dz, G.fz, s, slack);
+                for (int dy = y0; dy <= y1; ++dy) {
+                    const float gy = axis_gap(dy, G.fy, s, slack);
+                    if (__fmaf_rn(gz, gz, gy * gy) * kRel > bound()) continue;
+                    auto visit = [&](int dx) {
+                        const float gx = axis_gap(dx, G.fx, s, slack);
+                        const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                        if (lb2 * kRel > bound()) return;
+                        scan(cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz));
+                    };
+                    if (dz == -R || dz == R || dy == -R || dy == R) {
+                        for (int dx = x0; dx <= x1; ++dx) visit(dx);
+                    } else {
+                        if (-R >= x0) visit(-R);
+                        if (R <= x1) visit(R);
+                    }
                 }
             }
+            const float mR = cube_margin(G, s, slack, R);
+            if (mR > 0.0f && bound() < mR * mR * kRel) return;
+            if (G.cx - R <= 0 && G.cx + R >= g.nx - 1 && G.cy - R <= 0 && G.cy + R >= g.ny - 1 && G.cz - R <= 0 &&
+                G.cz + R >= g.nz - 1)
+                return;
         }
     }
 }
@@ -220,8 +220,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <bool REUSE, bool ERROR_ONLY>
 __global__ void __launch_bounds__(kLinBlock) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
-                                                         const float4* __restrict__ pts_orig,
-                                                         const HashEntry* __restrict__ H, Grid g, int64_t nt,
+                                                         const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
                                                          const float* __restrict__ tgt_cov, Pose P, float r2,
                                                          int32_t* __restrict__ corr, double* __restrict__ partials,
                                                          unsigned* __restrict__ done, double* __restrict__ out29) {
@@ -253,7 +252,7 @@ __global__ void __launch_bounds__(kLinBlock) k_linearize(const float* __restrict
             unsigned long long best;
             float3 bp = make_float3(0.f, 0.f, 0.f);
             int ovf;
-            nn_search(pts, H, g, sx, sy, sz, r2, best, bp, ovf);
+            nn_search(pts, lvs, sx, sy, sz, r2, best, bp, ovf);
             if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp);
             const float bd2 = __uint_as_float((unsigned)(best >> 32));
             orig = (best != kEmptyKey && bd2 < r2) ? (int)(best & 0xffffffffu) : -1;
@@ -348,6 +347,9 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     volatile float r2v = max_corr_dist * max_corr_dist;  // fp32 product
     const float r2 = r2v;
     const int64_t nb = (ns + kPPB - 1) / kPPB;
+    Levels lvs;
+    lvs.n = tgt->n_levels;
+    for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
     void* scratch = nullptr;
     const size_t bytes = (size_t)nb * (kNumAcc + 1) * sizeof(double) + 256;
     if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
@@ -359,9 +361,8 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset");
     if (rc == GICP_OK) {
         const bool reuse = flags & GICP_LIN_REUSE_CORR, eonly = flags & GICP_LIN_ERROR_ONLY;
-#define GICP_LIN_ARGS                                                                                      \
-    src, src_cov, ns, tgt->pts, tgt->pts_orig, tgt->hash, tgt->g, tgt->n, tgt_cov, P, r2, corr, partials, done, \
-        out29
+#define GICP_LIN_ARGS \
+    src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, P, r2, corr, partials, done, out29
         if (reuse && eonly)
             k_linearize<true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
         else if (reuse)
