@@ -197,7 +197,64 @@ def _sample_posts(rng, n, post_u):
     return p, nv
 
 
-def _areas(u_lo=0.0, u_hi=TRACK_LEN, n_posts=None):
+BOX_SPACING = 30.0
+
+
+@functools.lru_cache(maxsize=4)
+def box_specs(seed: int = 0):
+    """Infield marker boxes every 30 m +- U(-8, 8) m beyond the inner wall (seeded):
+    arc position u, lateral offset w, size (a, b, h), yaw. They give scan-to-scan
+    registration a second family of vertical structure ('add a
+    few seeded infield boxes')."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 8888]))
+    base = np.arange(0.0, TRACK_LEN - 1e-9, BOX_SPACING)
+    u = np.mod(base + rng.uniform(-8.0, 8.0, len(base)), TRACK_LEN)
+    w = -HALF_WIDTH - APRON - rng.uniform(2.0, 6.0, len(base))
+    size = np.stack([rng.uniform(1.5, 4.0, len(base)), rng.uniform(0.8, 2.0, len(base)),
+                     rng.uniform(0.8, 2.5, len(base))], -1)
+    yaw = rng.uniform(0, np.pi, len(base))
+    order = np.argsort(u)
+    return u[order], w[order], size[order], yaw[order]
+
+
+def _box_area(size):
+    a, b, h = size[..., 0], size[..., 1], size[..., 2]
+    return a * b + 2 * (a + b) * h  # top + 4 sides
+
+
+def _sample_boxes(rng, n, sel):
+    u, w, size, yaw = sel
+    if n == 0 or len(u) == 0:
+        return np.zeros((0, 3)), np.zeros((0, 3))
+    area = _box_area(size)
+    which = rng.choice(len(u), n, p=area / area.sum())
+    x, y, h, k, out = _frame(u[which])
+    cx = x + w[which] * out[:, 0]
+    cy = y + w[which] * out[:, 1]
+    a, b, hh = size[which, 0], size[which, 1], size[which, 2]
+    # face choice by area: 0 top, 1/2 +-a faces (b x h), 3/4 +-b faces (a x h)
+    fa = np.stack([a * b, b * hh, b * hh, a * hh, a * hh], -1)
+    cum = np.cumsum(fa, 1) / fa.sum(1, keepdims=True)
+    r = rng.uniform(size=n)
+    face = (r[:, None] > cum).sum(1)
+    s1 = rng.uniform(-0.5, 0.5, n)
+    s2 = rng.uniform(0.0, 1.0, n)
+    lx = np.where(face == 0, s1 * a, np.where(face == 1, 0.5 * a, np.where(face == 2, -0.5 * a, s1 * a)))
+    ly = np.where(face == 0, rng.uniform(-0.5, 0.5, n) * b,
+                  np.where(face <= 2, s1 * b, np.where(face == 3, 0.5 * b, -0.5 * b)))
+    lz = np.where(face == 0, hh, s2 * hh)
+    nl = np.stack([np.where(face == 1, 1.0, np.where(face == 2, -1.0, 0.0)),
+                   np.where(face == 3, 1.0, np.where(face == 4, -1.0, 0.0)),
+                   np.where(face == 0, 1.0, 0.0)], -1)
+    cyaw, syaw = np.cos(yaw[which]), np.sin(yaw[which])
+    px = cx + cyaw * lx - syaw * ly
+    py = cy + syaw * lx + cyaw * ly
+    nx = cyaw * nl[:, 0] - syaw * nl[:, 1]
+    ny = syaw * nl[:, 0] + cyaw * nl[:, 1]
+    return np.stack([px, py, lz], -1), np.stack([nx, ny, nl[:, 2]], -1)
+
+
+def _areas(u_lo=0.0, u_hi=TRACK_LEN, n_posts=None, box_sel=None):
     """Surface areas (m^2) of the four surface kinds over an arc-length window,
     by midpoint integration of the area elements."""
     uu = np.linspace(u_lo, u_hi, 20001)
@@ -213,13 +270,17 @@ def _areas(u_lo=0.0, u_hi=TRACK_LEN, n_posts=None):
     outer = np.sum(du * (1 + HALF_WIDTH * k)) * OUTER_WALL_H
     inner = np.sum(du * (1 + (-HALF_WIDTH - APRON) * k)) * INNER_WALL_H
     posts = (n_posts if n_posts is not None else len(post_positions())) * 2 * math.pi * POST_R * POST_H
-    return np.array([ribbon, apron, outer, inner, posts])
+    boxes = float(_box_area((box_sel if box_sel is not None else box_specs())[2]).sum())
+    return np.array([ribbon, apron, outer, inner, posts, boxes])
 
 
 def _sample_surfaces(rng, n, u_lo, u_hi, post_u):
     """n points uniform by area on all track surfaces with u in [u_lo, u_hi)."""
     sel_posts = post_u[(post_u >= u_lo) & (post_u < u_hi)] if u_hi - u_lo < TRACK_LEN else post_u
-    areas = _areas(u_lo, u_hi, len(sel_posts))
+    bu, bw, bs, by = box_specs()
+    bm = (bu >= u_lo) & (bu < u_hi) if u_hi - u_lo < TRACK_LEN else np.ones(len(bu), bool)
+    box_sel = (bu[bm], bw[bm], bs[bm], by[bm])
+    areas = _areas(u_lo, u_hi, len(sel_posts), box_sel)
     counts = rng.multinomial(n, areas / areas.sum())
     parts = []
     p, nv = _sample_strip(rng, counts[0], u_lo, u_hi, -HALF_WIDTH, HALF_WIDTH, "ribbon")
@@ -233,6 +294,8 @@ def _sample_surfaces(rng, n, u_lo, u_hi, post_u):
                          lambda u: np.zeros_like(u), INNER_WALL_H)
     parts.append((p, nv))
     p, nv = _sample_posts(rng, counts[4], sel_posts)
+    parts.append((p, nv))
+    p, nv = _sample_boxes(rng, counts[5], box_sel)
     parts.append((p, nv))
     pts = np.concatenate([a for a, _ in parts])
     nrm = np.concatenate([b for _, b in parts])

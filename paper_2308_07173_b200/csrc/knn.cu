@@ -158,91 +158,160 @@ __device__ __forceinline__ void knn_exact(const float4* __restrict__ pts, const 
 // Fast path at one level (warp-synchronous: every lane of the warp must call it;
 // `active` = the lane has a query). Status: 0 done (L[0..K-1] ascending, payload =
 // sorted position), 1 try the next level, 2 exact path (tie / too few points).
+//
+// Per lane: (A) the non-empty voxels of the 27-voxel cube, nearest-first, are
+// gathered into a shared-memory range list (27 hash probes, fully unrolled so the
+// probes overlap; neighbour Morton keys by dilated-integer arithmetic); (B) one
+// flattened candidate stream over those ranges (the warp iterates max over lanes
+// of the lane's candidate count, not the sum over voxels of per-voxel maxima);
+// (C) a max-heap of K keys in shared memory, padded to a full binary tree of
+// depth D with 0-keys so sift-down needs no bound checks; fill (sift-up) and
+// replace-root (sift-down) are predicated and issued once per step for the warp.
 // ---------------------------------------------------------------------------
+constexpr unsigned long long kMortonX = 0x1249249249249249ull;  // dilated bits of x
+
+__device__ __forceinline__ unsigned long long dil_inc(unsigned long long a, unsigned long long M) {
+    return ((a | ~M) + 1ull) & M;
+}
+__device__ __forceinline__ unsigned long long dil_dec(unsigned long long a, unsigned long long M) {
+    return (a - 1ull) & M;
+}
+
+template <int KCAP>
+struct FastShape {
+    static constexpr int D = floor_log2(KCAP);   // heap depth bound for K <= KCAP
+    static constexpr int NH = (2 << D) - 1;      // full binary tree slots (>= KCAP)
+};
+
 template <int KCAP>
 __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Grid& g, const QGeom& G, int K,
-                                        bool active, unsigned long long* __restrict__ Hl,
-                                        unsigned long long (&L)[KCAP]) {
-    constexpr int D = floor_log2(KCAP);  // heap depth bound for K <= KCAP
-    int cnt = 0;
-    unsigned long long top = 0ull;  // root (max) once cnt == K
-    unsigned tie = 0xffffffffu;
+                                        bool active, unsigned long long* __restrict__ Hl, int2* __restrict__ Rl,
+                                        unsigned char* __restrict__ Cl, unsigned long long (&L)[KCAP]) {
+    constexpr int D = FastShape<KCAP>::D;
     const float s = g.cell, slack = g.slack;
+#define HSLOT(i) Hl[(i) * kBlock]
+#define RSLOT(i) Rl[(i) * kBlock]
+#define CSLOT(i) Cl[(i) * kBlock]
+    // (A) gather the voxel ranges
+    int nr = 0;
+    if (active) {
+        const unsigned long long MX = kMortonX, MY = kMortonX << 1, MZ = kMortonX << 2;
+        const unsigned long long kx = spread3((unsigned)G.cx), ky = spread3((unsigned)G.cy) << 1,
+                                 kz = spread3((unsigned)G.cz) << 2;
+        const unsigned long long kxs[3] = {dil_dec(kx, MX), kx, dil_inc(kx, MX)};
+        const unsigned long long kys[3] = {dil_dec(ky, MY), ky, dil_inc(ky, MY)};
+        const unsigned long long kzs[3] = {dil_dec(kz, MZ), kz, dil_inc(kz, MZ)};
+        const bool okx[3] = {G.cx - 1 >= 0 && G.cx - 1 < g.nx, G.cx >= 0 && G.cx < g.nx, G.cx + 1 >= 0 && G.cx + 1 < g.nx};
+        const bool oky[3] = {G.cy - 1 >= 0 && G.cy - 1 < g.ny, G.cy >= 0 && G.cy < g.ny, G.cy + 1 >= 0 && G.cy + 1 < g.ny};
+        const bool okz[3] = {G.cz - 1 >= 0 && G.cz - 1 < g.nz, G.cz >= 0 && G.cz < g.nz, G.cz + 1 >= 0 && G.cz + 1 < g.nz};
+        const int4* __restrict__ Hh = reinterpret_cast<const int4*>(g.hash);
+#pragma unroll
+        for (int c = 0; c < 27; ++c) {
+            // nearest-first order: own, faces, edges, corners (same table as c_off27)
+            constexpr signed char off[27][3] = {
+                {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
+                {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
+                {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
+                {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+            const int ix = off[c][0] + 1, iy = off[c][1] + 1, iz = off[c][2] + 1;
+            if (!(okx[ix] && oky[iy] && okz[iz])) continue;
+            const unsigned long long key = kxs[ix] | kys[iy] | kzs[iz];
+            unsigned long long h = hash_slot(g, key);
+            int4 e = __ldg(Hh + h);
+            while (((unsigned long long)(unsigned)e.x | ((unsigned long long)(unsigned)e.y << 32)) != key &&
+                   !(e.x == -1 && e.y == -1)) {
+                h = (h + 1) & g.hmask;
+                e = __ldg(Hh + h);
+            }
+            if (e.x == -1 && e.y == -1) continue;  // empty slot: voxel not occupied
+            RSLOT(nr) = make_int2(e.z, e.w);
+            CSLOT(nr) = (unsigned char)c;
+            ++nr;
+        }
+    }
     const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
     const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
     const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
-#define HSLOT(i) Hl[(i) * kBlock]
-    for (int c = 0; c < 27; ++c) {
-        const int dx = c_off27[c][0], dy = c_off27[c][1], dz = c_off27[c][2];
-        bool skip = !active;
-        if (cnt == K) {
-            const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
-            const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
-            const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
-            const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
-            skip |= lb2 * kRel > __uint_as_float(hi32(top));
+    // (B)+(C) flattened stream into the heap
+    int cnt = 0;
+    unsigned long long top = 0ull;  // root (max) once cnt == K
+    unsigned tie = 0xffffffffu;
+    int ri = 0, pos = 0, end = 0;
+    while (true) {
+        // advance exhausted lanes to their next non-pruned range
+        while (pos == end && ri < nr) {
+            const int2 r = RSLOT(ri);
+            const int c = CSLOT(ri);
+            ++ri;
+            if (cnt == K) {
+                const int dx = c_off27[c][0], dy = c_off27[c][1], dz = c_off27[c][2];
+                const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
+                const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
+                const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
+                const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                if (lb2 * kRel > __uint_as_float(hi32(top))) continue;
+            }
+            pos = r.x;
+            end = r.y;
         }
-        int2 rng = make_int2(0, 0);
-        if (!skip) rng = cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz);
-        const int nc = rng.y - rng.x;
-        const int nmax = __reduce_max_sync(0xffffffffu, nc);
-        for (int jj = 0; jj < nmax; ++jj) {
-            const bool has = jj < nc;
-            const int j = rng.x + (has ? jj : 0);
-            unsigned hi = 0xffffffffu;
-            if (has) {
-                const float4 p = __ldg(pts + j);
-                hi = __float_as_uint(dist2(G.qx, G.qy, G.qz, p.x, p.y, p.z));
-            }
-            const unsigned long long key = ((unsigned long long)hi << 32) | (unsigned)j;
-            const bool fill = has && cnt < K;
-            const unsigned th = hi32(top);
-            const bool repl = has && cnt == K && hi < th;
-            if (has && cnt == K && hi == th) tie = min(tie, hi);  // rejected key tied with the K-th
-            if (__any_sync(0xffffffffu, fill)) {
-                // predicated sift-up from slot cnt
-                int i = cnt;
-                bool moving = fill;
+        const bool has = pos < end;
+        if (!__any_sync(0xffffffffu, has)) break;
+        unsigned hi = 0xffffffffu;
+        const int j = pos;
+        if (has) {
+            const float4 p = __ldg(pts + j);
+            hi = __float_as_uint(dist2(G.qx, G.qy, G.qz, p.x, p.y, p.z));
+            ++pos;
+        }
+        const unsigned long long key = ((unsigned long long)hi << 32) | (unsigned)j;
+        const bool fill = has && cnt < K;
+        const unsigned th = hi32(top);
+        const bool repl = has && cnt == K && hi < th;
+        if (has && cnt == K && hi == th) tie = min(tie, hi);  // rejected key tied with the K-th
+        if (__any_sync(0xffffffffu, fill)) {
+            // predicated sift-up from slot cnt
+            int i = cnt;
+            bool moving = fill;
 #pragma unroll
-                for (int lev = 0; lev < D; ++lev) {
-                    const int par = (i - 1) >> 1;
-                    unsigned long long pv = 0ull;
-                    const bool can = moving && i > 0;
-                    if (can) pv = HSLOT(par);
-                    const bool mv = can && hi32(pv) < hi;
-                    if (mv) HSLOT(i) = pv;
-                    i = mv ? par : i;
-                    moving = mv;
-                }
-                if (fill) {
-                    HSLOT(i) = key;
-                    ++cnt;
-                    if (cnt == K) top = HSLOT(0);
-                }
+            for (int lev = 0; lev < D; ++lev) {
+                const int par = (i - 1) >> 1;
+                const bool can = moving && i > 0;
+                unsigned long long pv = 0ull;
+                if (can) pv = HSLOT(par);
+                const bool mv = can && hi32(pv) < hi;
+                if (mv) HSLOT(i) = pv;
+                i = mv ? par : i;
+                moving = mv;
             }
-            if (__any_sync(0xffffffffu, repl)) {
-                // predicated replace-root + sift-down
-                int i = 0;
-                bool moving = repl;
+            if (fill) {
+                HSLOT(i) = key;
+                ++cnt;
+                if (cnt == K) top = HSLOT(0);
+            }
+        }
+        if (__any_sync(0xffffffffu, repl)) {
+            // predicated replace-root + sift-down (padding slots hold 0-keys)
+            int i = 0;
+            bool moving = repl;
 #pragma unroll
-                for (int lev = 0; lev < D; ++lev) {
-                    const int l = 2 * i + 1;
-                    const bool hl = moving && l < K, hr = moving && l + 1 < K;
-                    unsigned long long cv = 0ull, rv = 0ull;
-                    if (hl) cv = HSLOT(l);
-                    if (hr) rv = HSLOT(l + 1);
-                    const bool pr = hr && hi32(rv) > hi32(cv);
-                    const unsigned long long ch = pr ? rv : cv;
-                    const bool mv = hl && hi32(ch) > hi;
-                    if (mv) HSLOT(i) = ch;
-                    i = mv ? (pr ? l + 1 : l) : i;
-                    moving = mv;
+            for (int lev = 0; lev < D; ++lev) {
+                const int l = 2 * i + 1;
+                unsigned long long cv = 0ull, rv = 0ull;
+                if (moving) {
+                    cv = HSLOT(l);
+                    rv = HSLOT(l + 1);
                 }
-                if (repl) {
-                    HSLOT(i) = key;
-                    top = HSLOT(0);
-                    if (hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
-                }
+                const bool pr = hi32(rv) > hi32(cv);
+                const unsigned long long ch = pr ? rv : cv;
+                const bool mv = moving && hi32(ch) > hi;
+                if (mv) HSLOT(i) = ch;
+                i = mv ? l + (int)pr : i;
+                moving = mv;
+            }
+            if (repl) {
+                HSLOT(i) = key;
+                top = HSLOT(0);
+                if (hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
             }
         }
     }
@@ -254,6 +323,8 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
 #pragma unroll
     for (int r = 0; r < KCAP; ++r) L[r] = (r < K) ? HSLOT(r) : kEmptyKey;
 #undef HSLOT
+#undef RSLOT
+#undef CSLOT
     sort_network<KCAP>(L);
     bool dup = false;
 #pragma unroll
@@ -377,7 +448,12 @@ __global__ void __launch_bounds__(kBlock) k_knn_level(QuerySrc src, Grid g, cons
                                                       int* __restrict__ next_count, int* __restrict__ next_list,
                                                       int* __restrict__ exact_count, int2* __restrict__ exact_list,
                                                       int last_level) {
-    extern __shared__ unsigned long long heap[];
+    extern __shared__ unsigned long long smem[];
+    constexpr int NH = FastShape<KCAP>::NH;
+    unsigned long long* heap = smem;                                   // [NH][kBlock]
+    int2* ranges = reinterpret_cast<int2*>(smem + NH * kBlock);        // [27][kBlock]
+    unsigned char* cidx = reinterpret_cast<unsigned char*>(ranges + 27 * kBlock);  // [27][kBlock]
+    for (int i = K; i < NH; ++i) heap[i * kBlock + threadIdx.x] = 0ull;  // 0-key padding of the full tree
     const int64_t total = in_list ? (int64_t)*in_count : m;
     const int lane = threadIdx.x & 31;
     const int64_t warp0 = ((int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31));
@@ -403,7 +479,8 @@ __global__ void __launch_bounds__(kBlock) k_knn_level(QuerySrc src, Grid g, cons
         const bool run = active && finite;
         const QGeom G = make_geom(g, qx, qy, qz);
         unsigned long long L[KCAP];
-        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x, L);
+        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x, ranges + threadIdx.x,
+                                      cidx + threadIdx.x, L);
         if (run && st == 0) emit_row<KCAP>(src.pts, L, K, 0, true, nullptr, row, eps, nbr, d2, cov);
         const bool to_next = run && st == 1 && !last_level;
         const bool to_exact = run && (st == 2 || (st == 1 && last_level));
@@ -542,7 +619,13 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     int2* exact = reinterpret_cast<int2*>(ovf + m + (m & 1));
     if ((rc = check_cuda(cudaMemsetAsync(counts, 0, 16 * sizeof(int), s), "memset"))) return rc;
     const QuerySrc src{idx->pts, qext};
-    const size_t shmem = (size_t)KCAP * kBlock * sizeof(unsigned long long);
+    const size_t shmem = (size_t)FastShape<KCAP>::NH * kBlock * sizeof(unsigned long long) +
+                         (size_t)27 * kBlock * (sizeof(int2) + 1);
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        cudaFuncSetAttribute(k_knn_level<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+        attr_done = true;
+    }
     const int L = idx->n_levels;
     const unsigned full_blocks = (unsigned)((m + kBlock - 1) / kBlock);
     const unsigned some_blocks = (unsigned)std::min<int64_t>(full_blocks, 148 * 8);
