@@ -166,8 +166,9 @@ int gicp_linearize(const float* src, const float* src_cov, int64_t ns, gicp_inde
  *   10 inner trials solving (H + lambda I) delta = -b (LDL^T), T' = Exp(delta) T,
  *   e' = linearize(T', REUSE_CORR, ERROR_ONLY), gain rho = (e - e')/(delta^T
  *   (lambda delta - b)); accept iff rho > 0 (lambda *= max(1/3, 1 - (2 rho - 1)^3))
- *   else lambda *= nu, nu *= 2; converged when max|delta_omega| < rot_eps and
- *   max|delta_v| < trans_eps. lm = 0 gives plain Gauss-Newton.
+ *   else lambda *= nu, nu *= 2; converged when the ACCEPTED step has
+ *   max|delta_omega| < rot_eps and max|delta_v| < trans_eps, or when no trial
+ *   decreases the cost (a numerical minimum). lm = 0 gives plain Gauss-Newton.
  * Synchronous. Errors: EINVAL, EDEGENERATE (< 6 inliers), ENOMEM, ECUDA.
  * Non-convergence is not an error (result->converged = 0).
  * ------------------------------------------------------------------------- */

@@ -648,6 +648,7 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
                     if (H[7 * a] > mx) mx = H[7 * a];
                 lambda = 1e-9 * mx;
             }
+            int accepted = 0;
             for (int inner = 0; inner < 10; ++inner) {
                 double Hl[36], nb[6];
                 memcpy(Hl, H, sizeof(Hl));
@@ -677,12 +678,18 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
                     lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
                     nu = 2.0;
                     err = en;
+                    accepted = 1;
                     break;
                 }
                 lambda *= nu;
                 nu *= 2.0;
             }
             if (rc != ORACLE_OK) break;
+            if (!accepted) {
+                /* no step decreases the cost: a (numerical) minimum */
+                converged = 1;
+                break;
+            }
         }
         double mw = fmax(fabs(delta[0]), fmax(fabs(delta[1]), fabs(delta[2])));
         double mv = fmax(fabs(delta[3]), fmax(fabs(delta[4]), fabs(delta[5])));

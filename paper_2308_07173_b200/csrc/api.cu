@@ -305,6 +305,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 for (int a = 0; a < 6; ++a) mx = std::fmax(mx, Hm[7 * a]);
                 lambda = 1e-9 * mx;
             }
+            bool accepted = false;
             for (int inner = 0; inner < 10; ++inner) {
                 double Hl[36], nb[6];
                 std::memcpy(Hl, Hm, sizeof(Hl));
@@ -331,12 +332,17 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                     lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
                     nu = 2.0;
                     err = en;
+                    accepted = true;
                     break;
                 }
                 lambda *= nu;
                 nu *= 2.0;
             }
             if (rc) break;
+            if (!accepted) {  // no step decreases the cost: a (numerical) minimum
+                converged = 1;
+                break;
+            }
         }
         const double mw = std::fmax(std::fabs(delta[0]), std::fmax(std::fabs(delta[1]), std::fabs(delta[2])));
         const double mv = std::fmax(std::fabs(delta[3]), std::fmax(std::fabs(delta[4]), std::fabs(delta[5])));

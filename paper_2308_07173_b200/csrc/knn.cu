@@ -32,13 +32,6 @@ namespace {
 constexpr int kBlock = 128;
 constexpr int kMaxRing = 24;
 
-// first ring, nearest-first: own voxel, 6 faces, 12 edges, 8 corners
-__constant__ signed char c_off27[27][3] = {
-    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
-    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
-    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
-    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
-
 __device__ __forceinline__ unsigned hi32(unsigned long long k) { return (unsigned)(k >> 32); }
 
 // sorted register list insertion (exact path)
@@ -185,16 +178,19 @@ struct FastShape {
 
 template <int KCAP>
 __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Grid& g, const QGeom& G, int K,
-                                        bool active, unsigned long long* __restrict__ Hl, int2* __restrict__ Rl,
-                                        unsigned char* __restrict__ Cl, unsigned long long (&L)[KCAP]) {
+                                        bool active, unsigned long long* __restrict__ Hl,
+                                        unsigned long long (&L)[KCAP]) {
     constexpr int D = FastShape<KCAP>::D;
     const float s = g.cell, slack = g.slack;
 #define HSLOT(i) Hl[(i) * kBlock]
-#define RSLOT(i) Rl[(i) * kBlock]
-#define CSLOT(i) Cl[(i) * kBlock]
-    // (A) gather the voxel ranges
+    // (A) gather the voxel ranges (thread-local array: L1-resident local memory)
+    int2 rl[27];
+    float lbl[27];
     int nr = 0;
     if (active) {
+        const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
+        const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
+        const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
         const unsigned long long MX = kMortonX, MY = kMortonX << 1, MZ = kMortonX << 2;
         const unsigned long long kx = spread3((unsigned)G.cx), ky = spread3((unsigned)G.cy) << 1,
                                  kz = spread3((unsigned)G.cz) << 2;
@@ -224,14 +220,11 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
                 e = __ldg(Hh + h);
             }
             if (e.x == -1 && e.y == -1) continue;  // empty slot: voxel not occupied
-            RSLOT(nr) = make_int2(e.z, e.w);
-            CSLOT(nr) = (unsigned char)c;
+            rl[nr] = make_int2(e.z, e.w);
+            lbl[nr] = __fmaf_rn(gzs[iz], gzs[iz], __fmaf_rn(gys[iy], gys[iy], gxs[ix] * gxs[ix]));
             ++nr;
         }
     }
-    const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
-    const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
-    const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
     // (B)+(C) flattened stream into the heap
     int cnt = 0;
     unsigned long long top = 0ull;  // root (max) once cnt == K
@@ -240,17 +233,10 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     while (true) {
         // advance exhausted lanes to their next non-pruned range
         while (pos == end && ri < nr) {
-            const int2 r = RSLOT(ri);
-            const int c = CSLOT(ri);
+            const int2 r = rl[ri];
+            const float lb2 = lbl[ri];
             ++ri;
-            if (cnt == K) {
-                const int dx = c_off27[c][0], dy = c_off27[c][1], dz = c_off27[c][2];
-                const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
-                const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
-                const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
-                const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
-                if (lb2 * kRel > __uint_as_float(hi32(top))) continue;
-            }
+            if (cnt == K && lb2 * kRel > __uint_as_float(hi32(top))) continue;
             pos = r.x;
             end = r.y;
         }
@@ -296,7 +282,7 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
 #pragma unroll
             for (int lev = 0; lev < D; ++lev) {
                 const int l = 2 * i + 1;
-                unsigned long long cv = 0ull, rv = 0ull;
+                unsigned long long cv, rv;
                 if (moving) {
                     cv = HSLOT(l);
                     rv = HSLOT(l + 1);
@@ -323,8 +309,6 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
 #pragma unroll
     for (int r = 0; r < KCAP; ++r) L[r] = (r < K) ? HSLOT(r) : kEmptyKey;
 #undef HSLOT
-#undef RSLOT
-#undef CSLOT
     sort_network<KCAP>(L);
     bool dup = false;
 #pragma unroll
@@ -451,8 +435,6 @@ __global__ void __launch_bounds__(kBlock) k_knn_level(QuerySrc src, Grid g, cons
     extern __shared__ unsigned long long smem[];
     constexpr int NH = FastShape<KCAP>::NH;
     unsigned long long* heap = smem;                                   // [NH][kBlock]
-    int2* ranges = reinterpret_cast<int2*>(smem + NH * kBlock);        // [27][kBlock]
-    unsigned char* cidx = reinterpret_cast<unsigned char*>(ranges + 27 * kBlock);  // [27][kBlock]
     for (int i = K; i < NH; ++i) heap[i * kBlock + threadIdx.x] = 0ull;  // 0-key padding of the full tree
     const int64_t total = in_list ? (int64_t)*in_count : m;
     const int lane = threadIdx.x & 31;
@@ -479,8 +461,7 @@ __global__ void __launch_bounds__(kBlock) k_knn_level(QuerySrc src, Grid g, cons
         const bool run = active && finite;
         const QGeom G = make_geom(g, qx, qy, qz);
         unsigned long long L[KCAP];
-        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x, ranges + threadIdx.x,
-                                      cidx + threadIdx.x, L);
+        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x, L);
         if (run && st == 0) emit_row<KCAP>(src.pts, L, K, 0, true, nullptr, row, eps, nbr, d2, cov);
         const bool to_next = run && st == 1 && !last_level;
         const bool to_exact = run && (st == 2 || (st == 1 && last_level));
@@ -619,8 +600,7 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     int2* exact = reinterpret_cast<int2*>(ovf + m + (m & 1));
     if ((rc = check_cuda(cudaMemsetAsync(counts, 0, 16 * sizeof(int), s), "memset"))) return rc;
     const QuerySrc src{idx->pts, qext};
-    const size_t shmem = (size_t)FastShape<KCAP>::NH * kBlock * sizeof(unsigned long long) +
-                         (size_t)27 * kBlock * (sizeof(int2) + 1);
+    const size_t shmem = (size_t)FastShape<KCAP>::NH * kBlock * sizeof(unsigned long long);
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         cudaFuncSetAttribute(k_knn_level<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
