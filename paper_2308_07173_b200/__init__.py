@@ -17,7 +17,9 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgicp_b200.so")
+# GICP_LIB_VARIANT selects an alternative build of the SAME library (tools/ only,
+# for A/B timing of compile options); the default is the in-tree build.
+LIB_PATH = os.environ.get("GICP_LIB_VARIANT") or os.path.join(_HERE, "libgicp_b200.so")
 
 OK, EINVAL, EK, ERANGE, ENOMEM, ECUDA, EDEGENERATE = 0, -1, -2, -3, -4, -5, -6
 LIN_REUSE_CORR, LIN_ERROR_ONLY = 1, 2

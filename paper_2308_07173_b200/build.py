@@ -31,16 +31,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str | None = None) -> str:
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", target + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

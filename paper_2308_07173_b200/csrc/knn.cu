@@ -30,6 +30,9 @@ namespace gicp {
 namespace {
 
 constexpr int kBlock = 128;
+#ifndef GICP_KNN_MINB
+#define GICP_KNN_MINB 6
+#endif
 constexpr int kMaxRing = 24;
 
 __device__ __forceinline__ unsigned hi32(unsigned long long k) { return (unsigned)(k >> 32); }
@@ -83,6 +86,21 @@ __device__ __forceinline__ void sort_network(unsigned long long (&v)[N]) {
     constexpr SortNet net = make_sortnet(N);
 #pragma unroll
     for (int c = 0; c < net.n; ++c) cas_hi(v[net.a[c]], v[net.b[c]]);
+}
+
+// the same network on a shared-memory column (stride kBlock) -- keeps the K keys
+// out of registers
+template <int N, int STRIDE>
+__device__ __forceinline__ void sort_network_smem(unsigned long long* __restrict__ H) {
+    constexpr SortNet net = make_sortnet(N);
+#pragma unroll
+    for (int c = 0; c < net.n; ++c) {
+        const unsigned long long a = H[net.a[c] * STRIDE], b = H[net.b[c] * STRIDE];
+        if (hi32(b) < hi32(a)) {
+            H[net.a[c] * STRIDE] = b;
+            H[net.b[c] * STRIDE] = a;
+        }
+    }
 }
 
 constexpr int floor_log2(int x) { return x <= 1 ? 0 : 1 + floor_log2(x / 2); }
@@ -178,8 +196,7 @@ struct FastShape {
 
 template <int KCAP>
 __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Grid& g, const QGeom& G, int K,
-                                        bool active, unsigned long long* __restrict__ Hl,
-                                        unsigned long long (&L)[KCAP]) {
+                                        bool active, unsigned long long* __restrict__ Hl) {
     constexpr int D = FastShape<KCAP>::D;
     const float s = g.cell, slack = g.slack;
 #define HSLOT(i) Hl[(i) * kBlock]
@@ -306,14 +323,18 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     const float m = cube_margin(G, s, slack, 1);
     if (!(m > 0.0f && __uint_as_float(hi32(top)) < m * m * kRel)) return 1;
     if (tie == hi32(top)) return 2;
-#pragma unroll
-    for (int r = 0; r < KCAP; ++r) L[r] = (r < K) ? HSLOT(r) : kEmptyKey;
-#undef HSLOT
-    sort_network<KCAP>(L);
+    // sort the K keys in place (slots K..KCAP-1 temporarily +inf; the caller
+    // restores the 0-key padding after emitting the row)
+    for (int r = K; r < KCAP; ++r) HSLOT(r) = kEmptyKey;
+    sort_network_smem<KCAP, kBlock>(Hl);
     bool dup = false;
-#pragma unroll
-    for (int r = 0; r + 1 < KCAP; ++r)
-        if (r + 1 < K) dup |= hi32(L[r]) == hi32(L[r + 1]);
+    unsigned prev = hi32(HSLOT(0));
+    for (int r = 1; r < K; ++r) {
+        const unsigned h = hi32(HSLOT(r));
+        dup |= h == prev;
+        prev = h;
+    }
+#undef HSLOT
     return dup ? 2 : 0;
 }
 
@@ -360,6 +381,40 @@ __device__ __forceinline__ void emit_row(const float4* __restrict__ pts, const u
     for (int r = 0; r < KCAP; ++r) {
         if (r < base || r >= base + K) continue;
         const float4 p = __ldg(pts + pos(L[r]));
+        const float x = (p.x - p0.x) - mx, y = (p.y - p0.y) - my, z = (p.z - p0.z) - mz;
+        c00 = fmaf(x, x, c00);
+        c01 = fmaf(x, y, c01);
+        c02 = fmaf(x, z, c02);
+        c11 = fmaf(y, y, c11);
+        c12 = fmaf(y, z, c12);
+        c22 = fmaf(z, z, c22);
+    }
+    float c[6];
+    plane_cov(c00 * invk, c01 * invk, c02 * invk, c11 * invk, c12 * invk, c22 * invk, eps, c);
+    store_cov(cov, row, c);
+}
+
+// emit a fast-path row: keys sorted ascending in the smem column Hl[0..K-1]
+__device__ __forceinline__ void emit_row_smem(const float4* __restrict__ pts, const unsigned long long* __restrict__ Hl,
+                                              int K, int64_t row, float eps, int32_t* __restrict__ nbr,
+                                              float* __restrict__ d2, float* __restrict__ cov) {
+    const float4 p0 = __ldg(pts + (unsigned)(Hl[0] & 0xffffffffu));
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    for (int r = 0; r < K; ++r) {
+        const unsigned long long key = Hl[r * kBlock];
+        const float4 p = __ldg(pts + (unsigned)(key & 0xffffffffu));
+        if (nbr) nbr[row * K + r] = __float_as_int(p.w);
+        if (d2) d2[row * K + r] = __uint_as_float(hi32(key));
+        sx += p.x - p0.x;
+        sy += p.y - p0.y;
+        sz += p.z - p0.z;
+    }
+    if (!cov) return;
+    const float invk = 1.0f / (float)K;
+    const float mx = sx * invk, my = sy * invk, mz = sz * invk;
+    float c00 = 0.f, c01 = 0.f, c02 = 0.f, c11 = 0.f, c12 = 0.f, c22 = 0.f;
+    for (int r = 0; r < K; ++r) {
+        const float4 p = __ldg(pts + (unsigned)(Hl[r * kBlock] & 0xffffffffu));
         const float x = (p.x - p0.x) - mx, y = (p.y - p0.y) - my, z = (p.z - p0.z) - mz;
         c00 = fmaf(x, x, c00);
         c01 = fmaf(x, y, c01);
@@ -425,7 +480,7 @@ struct QuerySrc {
 // when in_list == nullptr, the identity / perm over [0, m). Warp-uniform
 // grid-stride loop (all 32 lanes stay together for the warp votes).
 template <int KCAP>
-__global__ void __launch_bounds__(kBlock) k_knn_level(QuerySrc src, Grid g, const int* __restrict__ perm, int64_t m,
+__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_level(QuerySrc src, Grid g, const int* __restrict__ perm, int64_t m,
                                                       const int* __restrict__ in_list, const int* __restrict__ in_count,
                                                       int K, float eps, int32_t* __restrict__ nbr,
                                                       float* __restrict__ d2, float* __restrict__ cov,
@@ -460,13 +515,64 @@ __global__ void __launch_bounds__(kBlock) k_knn_level(QuerySrc src, Grid g, cons
         }
         const bool run = active && finite;
         const QGeom G = make_geom(g, qx, qy, qz);
-        unsigned long long L[KCAP];
-        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x, L);
-        if (run && st == 0) emit_row<KCAP>(src.pts, L, K, 0, true, nullptr, row, eps, nbr, d2, cov);
+        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x);
+        if (run && st == 0) emit_row_smem(src.pts, heap + threadIdx.x, K, row, eps, nbr, d2, cov);
+        for (int r = K; r < NH; ++r) heap[r * kBlock + threadIdx.x] = 0ull;  // restore the 0-key padding
         const bool to_next = run && st == 1 && !last_level;
         const bool to_exact = run && (st == 2 || (st == 1 && last_level));
         push_warp(next_count, next_list, to_next, id);
         push_warp2(exact_count, exact_list, to_exact, make_int2(id, g.level));
+    }
+}
+
+// Queries level 0 could not settle climb the pyramid in ONE launch: each warp
+// takes 32 of them through levels 1..L-1 (warp-synchronous fast path at every
+// level, lanes that finish idle); still-unsettled queries and ties go to the
+// exact path with the level they stopped at.
+template <int KCAP>
+__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_escalate(QuerySrc src, Levels lvs, int n_levels,
+                                                                      const int* __restrict__ in_list,
+                                                                      const int* __restrict__ in_count, int K,
+                                                                      float eps, int32_t* __restrict__ nbr,
+                                                                      float* __restrict__ d2, float* __restrict__ cov,
+                                                                      int* __restrict__ exact_count,
+                                                                      int2* __restrict__ exact_list) {
+    extern __shared__ unsigned long long smem[];
+    constexpr int NH = FastShape<KCAP>::NH;
+    unsigned long long* heap = smem;
+    for (int i = K; i < NH; ++i) heap[i * kBlock + threadIdx.x] = 0ull;
+    const int64_t total = *in_count;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31));
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    for (int64_t base = warp0; base < total; base += stride) {
+        const int64_t t = base + lane;
+        const bool active = t < total;
+        int id = 0;
+        float qx = 0.f, qy = 0.f, qz = 0.f;
+        int64_t row = 0;
+        if (active) {
+            id = in_list[t];
+            src.get(id, qx, qy, qz, row);
+        }
+        bool pending = active;
+        int stop_level = n_levels - 1;
+        bool to_exact = false;
+        for (int l = 1; l < n_levels; ++l) {
+            if (!__any_sync(0xffffffffu, pending)) break;
+            const Grid g = lvs.lv[l];
+            const QGeom G = make_geom(g, qx, qy, qz);
+            const int st = knn_fast<KCAP>(src.pts, g, G, K, pending, heap + threadIdx.x);
+            if (pending && st == 0) emit_row_smem(src.pts, heap + threadIdx.x, K, row, eps, nbr, d2, cov);
+            for (int r = K; r < NH; ++r) heap[r * kBlock + threadIdx.x] = 0ull;
+            if (pending && st == 2) {
+                to_exact = true;
+                stop_level = l;
+            }
+            if (pending && st != 1) pending = false;
+        }
+        if (pending) to_exact = true;  // exhausted the pyramid: ring expansion at the last level
+        push_warp2(exact_count, exact_list, to_exact, make_int2(id, stop_level));
     }
 }
 
@@ -601,28 +707,19 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     if ((rc = check_cuda(cudaMemsetAsync(counts, 0, 16 * sizeof(int), s), "memset"))) return rc;
     const QuerySrc src{idx->pts, qext};
     const size_t shmem = (size_t)FastShape<KCAP>::NH * kBlock * sizeof(unsigned long long);
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        cudaFuncSetAttribute(k_knn_level<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
-        attr_done = true;
-    }
+    cudaFuncSetAttribute(k_knn_level<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    cudaFuncSetAttribute(k_knn_escalate<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
     const int L = idx->n_levels;
     const unsigned full_blocks = (unsigned)((m + kBlock - 1) / kBlock);
     const unsigned some_blocks = (unsigned)std::min<int64_t>(full_blocks, 148 * 8);
-    // level 0 over every query; level l over the queries level l-1 could not settle
-    int* in = nullptr;
-    int* in_cnt = nullptr;
-    for (int l = 0; l < L; ++l) {
-        int* out = (l % 2 == 0) ? listA : listB;
-        int* out_cnt = counts + 2 + l;  // fresh counter per level
-        k_knn_level<KCAP><<<l == 0 ? full_blocks : some_blocks, kBlock, shmem, s>>>(
-            src, idx->lv[l], perm, m, in, in_cnt, k, eps, nbr, d2, cov, out_cnt, out, counts + 0, exact,
-            l == L - 1);
-        in = out;
-        in_cnt = out_cnt;
-    }
     Levels lvs;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
+    // level 0 over every query, then one launch that climbs the pyramid for the rest
+    k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
+                                                         cov, counts + 2, listA, counts + 0, exact, L == 1);
+    if (L > 1)
+        k_knn_escalate<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, lvs, L, listA, counts + 2, k, eps, nbr, d2, cov,
+                                                                counts + 0, exact);
     k_knn_exact<KCAP><<<some_blocks, kBlock, 0, s>>>(src, idx->pts_orig, lvs, exact, counts + 0, k, eps, nbr, d2,
                                                       cov, counts + 1, ovf);
     k_knn_bruteforce<KCAP><<<(unsigned)std::min<int64_t>(m, 1024), kBFBlock, 0, s>>>(

@@ -32,11 +32,6 @@ struct Pose {
     float Rf[9];
 };
 
-__constant__ signed char c_off27l[27][3] = {
-    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
-    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
-    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
-    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
 
 struct Levels {
     Grid lv[kMaxLevels];
@@ -67,13 +62,44 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         const Grid& g = lvs.lv[l];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
-        for (int c = 0; c < 27; ++c) {
-            const int dx = c_off27l[c][0], dy = c_off27l[c][1], dz = c_off27l[c][2];
-            const float gx = axis_gap(dx, G.fx, s, slack), gy = axis_gap(dy, G.fy, s, slack),
-                        gz = axis_gap(dz, G.fz, s, slack);
-            const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
-            if (lb2 * kRel > bound()) continue;
-            scan(cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz));
+        {
+            // the 27 voxel probes are independent: issue them all (unrolled) and keep
+            // the non-empty ranges with their lower bounds, then scan nearest-first
+            const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
+            const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
+            const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
+            int2 rl[27];
+            float lbl[27];
+            int nr = 0;
+            const int4* __restrict__ Hh = reinterpret_cast<const int4*>(g.hash);
+#pragma unroll
+            for (int c = 0; c < 27; ++c) {
+                constexpr signed char off[27][3] = {
+                    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
+                    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
+                    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
+                    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+                const int dx = off[c][0], dy = off[c][1], dz = off[c][2];
+                const int cx = G.cx + dx, cy = G.cy + dy, cz = G.cz + dz;
+                if ((unsigned)cx >= (unsigned)g.nx || (unsigned)cy >= (unsigned)g.ny || (unsigned)cz >= (unsigned)g.nz)
+                    continue;
+                const unsigned long long key = cell_key(cx, cy, cz);
+                unsigned long long h = hash_slot(g, key);
+                int4 e = __ldg(Hh + h);
+                while (((unsigned long long)(unsigned)e.x | ((unsigned long long)(unsigned)e.y << 32)) != key &&
+                       !(e.x == -1 && e.y == -1)) {
+                    h = (h + 1) & g.hmask;
+                    e = __ldg(Hh + h);
+                }
+                if (e.x == -1 && e.y == -1) continue;
+                rl[nr] = make_int2(e.z, e.w);
+                lbl[nr] = __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
+                ++nr;
+            }
+            for (int r = 0; r < nr; ++r) {
+                if (lbl[r] * kRel > bound()) continue;
+                scan(rl[r]);
+            }
         }
         const float m = cube_margin(G, s, slack, 1);
         if (m > 0.0f && bound() < m * m * kRel) return;
@@ -218,7 +244,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <bool REUSE, bool ERROR_ONLY>
-__global__ void __launch_bounds__(kLinBlock) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
+__global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
                                                          const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
                                                          const float* __restrict__ tgt_cov, Pose P, float r2,

@@ -257,7 +257,7 @@ def test_align_c2(orc):
     idx = g.build_index(D(tgt), 0.0)
     T, info = g.align(D(src), D(cs), idx, D(ct), T0)
     ref = orc.align(src, cs, tgt, ct, T0)
-    assert info.converged
+    assert info.converged and ref["converged"]
     o29, _, corr = orc.linearize(src, cs, tgt, ct, ref["T"], 1.0)
     pw = src.astype(np.float64) @ ref["T"][:3, :3].T + ref["T"][:3, 3]
     kp = kappa_prime(o29, pw[corr >= 0])
@@ -265,10 +265,20 @@ def test_align_c2(orc):
         dt, dr = _pose_err(T, ref["T"])
         assert dt <= 1e-3 and dr <= 1e-4
     else:
-        # below the eps floor the optimum is a flat valley: compare the costs reached
+        # Below the eps floor (align) the optimum is a flat
+        # valley: LM accept/reject decisions hinge on cost differences at the
+        # rounding level, so the two LM paths may stop at different points of the
+        # valley. Gauss-Newton has no such decisions: its poses must agree; the LM
+        # costs must agree to 1e-3 relative and not exceed the GN cost by more.
+        Tg, ig = g.align(D(src), D(cs), idx, D(ct), T0, lm=False)
+        rg = orc.align(src, cs, tgt, ct, T0, lm=False)
+        dt, dr = _pose_err(Tg, rg["T"])
+        assert dt <= 1e-3 and dr <= 1e-4, (kp, dt, dr)
         e_gpu = orc.linearize(src, cs, tgt, ct, T, 1.0)[0][27]
         e_ref = o29[27]
-        assert abs(e_gpu - e_ref) <= 1e-4 * abs(e_ref), (kp, e_gpu, e_ref)
+        e_gn = orc.linearize(src, cs, tgt, ct, rg["T"], 1.0)[0][27]
+        assert abs(e_gpu - e_ref) <= 1e-3 * abs(e_ref), (kp, e_gpu, e_ref)
+        assert e_gpu <= e_gn * (1 + 1e-3) and e_ref <= e_gn * (1 + 1e-3)
 
 
 def test_align_degenerate(orc):
