@@ -23,6 +23,9 @@
 //    (d2, original index) keys; pathological ones to a block brute force.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "cov_device.cuh"
 #include "gicp_internal.cuh"
 
@@ -90,13 +93,13 @@ __device__ __forceinline__ void sort_network(unsigned long long (&v)[N]) {
 
 // the same network on a shared-memory column (stride kBlock) -- keeps the K keys
 // out of registers
-template <int N, int STRIDE>
+template <int N, int STRIDE, bool FULL = false>
 __device__ __forceinline__ void sort_network_smem(unsigned long long* __restrict__ H) {
     constexpr SortNet net = make_sortnet(N);
 #pragma unroll
     for (int c = 0; c < net.n; ++c) {
         const unsigned long long a = H[net.a[c] * STRIDE], b = H[net.b[c] * STRIDE];
-        if (hi32(b) < hi32(a)) {
+        if (FULL ? b < a : hi32(b) < hi32(a)) {
             H[net.a[c] * STRIDE] = b;
             H[net.b[c] * STRIDE] = a;
         }
@@ -194,7 +197,7 @@ struct FastShape {
     static constexpr int NH = (2 << D) - 1;      // full binary tree slots (>= KCAP)
 };
 
-template <int KCAP>
+template <int KCAP, bool EXACT = false>
 __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Grid& g, const QGeom& G, int K,
                                         bool active, unsigned long long* __restrict__ Hl) {
     constexpr int D = FastShape<KCAP>::D;
@@ -259,18 +262,19 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
         }
         const bool has = pos < end;
         if (!__any_sync(0xffffffffu, has)) break;
-        unsigned hi = 0xffffffffu;
+        unsigned hi = 0xffffffffu, pay = 0u;
         const int j = pos;
         if (has) {
             const float4 p = __ldg(pts + j);
             hi = __float_as_uint(dist2(G.qx, G.qy, G.qz, p.x, p.y, p.z));
+            pay = EXACT ? __float_as_uint(p.w) : (unsigned)j;
             ++pos;
         }
-        const unsigned long long key = ((unsigned long long)hi << 32) | (unsigned)j;
+        const unsigned long long key = ((unsigned long long)hi << 32) | pay;
         const bool fill = has && cnt < K;
         const unsigned th = hi32(top);
-        const bool repl = has && cnt == K && hi < th;
-        if (has && cnt == K && hi == th) tie = min(tie, hi);  // rejected key tied with the K-th
+        const bool repl = has && cnt == K && (EXACT ? key < top : hi < th);
+        if (!EXACT && has && cnt == K && hi == th) tie = min(tie, hi);  // rejected key tied with the K-th
         if (__any_sync(0xffffffffu, fill)) {
             // predicated sift-up from slot cnt
             int i = cnt;
@@ -281,7 +285,7 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
                 const bool can = moving && i > 0;
                 unsigned long long pv = 0ull;
                 if (can) pv = HSLOT(par);
-                const bool mv = can && hi32(pv) < hi;
+                const bool mv = can && (EXACT ? pv < key : hi32(pv) < hi);
                 if (mv) HSLOT(i) = pv;
                 i = mv ? par : i;
                 moving = mv;
@@ -304,9 +308,9 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
                     cv = HSLOT(l);
                     rv = HSLOT(l + 1);
                 }
-                const bool pr = hi32(rv) > hi32(cv);
+                const bool pr = EXACT ? rv > cv : hi32(rv) > hi32(cv);
                 const unsigned long long ch = pr ? rv : cv;
-                const bool mv = moving && hi32(ch) > hi;
+                const bool mv = moving && (EXACT ? ch > key : hi32(ch) > hi);
                 if (mv) HSLOT(i) = ch;
                 i = mv ? l + (int)pr : i;
                 moving = mv;
@@ -314,7 +318,7 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
             if (repl) {
                 HSLOT(i) = key;
                 top = HSLOT(0);
-                if (hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
+                if (!EXACT && hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
             }
         }
     }
@@ -322,11 +326,12 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     if (cnt < K) return 1;
     const float m = cube_margin(G, s, slack, 1);
     if (!(m > 0.0f && __uint_as_float(hi32(top)) < m * m * kRel)) return 1;
-    if (tie == hi32(top)) return 2;
+    if (!EXACT && tie == hi32(top)) return 2;
     // sort the K keys in place (slots K..KCAP-1 temporarily +inf; the caller
     // restores the 0-key padding after emitting the row)
     for (int r = K; r < KCAP; ++r) HSLOT(r) = kEmptyKey;
-    sort_network_smem<KCAP, kBlock>(Hl);
+    sort_network_smem<KCAP, kBlock, EXACT>(Hl);
+    if (EXACT) return 0;
     bool dup = false;
     unsigned prev = hi32(HSLOT(0));
     for (int r = 1; r < K; ++r) {
@@ -395,14 +400,21 @@ __device__ __forceinline__ void emit_row(const float4* __restrict__ pts, const u
 }
 
 // emit a fast-path row: keys sorted ascending in the smem column Hl[0..K-1]
+template <bool EXACT = false>
 __device__ __forceinline__ void emit_row_smem(const float4* __restrict__ pts, const unsigned long long* __restrict__ Hl,
                                               int K, int64_t row, float eps, int32_t* __restrict__ nbr,
-                                              float* __restrict__ d2, float* __restrict__ cov) {
-    const float4 p0 = __ldg(pts + (unsigned)(Hl[0] & 0xffffffffu));
+                                              float* __restrict__ d2, float* __restrict__ cov,
+                                              const float4* __restrict__ pts_orig = nullptr) {
+    // payload: sorted position (fast path) or original index (EXACT: map back)
+    auto sp = [&](unsigned long long key) -> unsigned {
+        const unsigned pay = (unsigned)(key & 0xffffffffu);
+        return EXACT ? (unsigned)__float_as_int(__ldg(pts_orig + pay).w) : pay;
+    };
+    const float4 p0 = __ldg(pts + sp(Hl[0]));
     float sx = 0.f, sy = 0.f, sz = 0.f;
     for (int r = 0; r < K; ++r) {
         const unsigned long long key = Hl[r * kBlock];
-        const float4 p = __ldg(pts + (unsigned)(key & 0xffffffffu));
+        const float4 p = __ldg(pts + sp(key));
         if (nbr) nbr[row * K + r] = __float_as_int(p.w);
         if (d2) d2[row * K + r] = __uint_as_float(hi32(key));
         sx += p.x - p0.x;
@@ -414,7 +426,7 @@ __device__ __forceinline__ void emit_row_smem(const float4* __restrict__ pts, co
     const float mx = sx * invk, my = sy * invk, mz = sz * invk;
     float c00 = 0.f, c01 = 0.f, c02 = 0.f, c11 = 0.f, c12 = 0.f, c22 = 0.f;
     for (int r = 0; r < K; ++r) {
-        const float4 p = __ldg(pts + (unsigned)(Hl[r * kBlock] & 0xffffffffu));
+        const float4 p = __ldg(pts + sp(Hl[r * kBlock]));
         const float x = (p.x - p0.x) - mx, y = (p.y - p0.y) - my, z = (p.z - p0.z) - mz;
         c00 = fmaf(x, x, c00);
         c01 = fmaf(x, y, c01);
@@ -576,32 +588,61 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_escalate(QuerySrc
     }
 }
 
-// Exact path for the rare queries the fast path could not settle (d2 ties, or the
-// coarsest level's cube did not suffice): ring expansion at the level where the
-// query stopped, with (d2, original index) keys.
+// Exact path for the rare queries the fast path could not settle (a d2 tie
+// touching the result, or the pyramid exhausted): the same warp-synchronous heap
+// search with (d2, ORIGINAL index) keys -- the definition's key, so ties need no
+// special care -- from the level the query stopped at, climbing the pyramid; a
+// query that exhausts it gets the ring-expanding search (register list).
 template <int KCAP>
-__global__ void __launch_bounds__(kBlock) k_knn_exact(QuerySrc src, const float4* __restrict__ pts_orig, Levels lvs,
-                                                      const int2* __restrict__ list, const int* __restrict__ count,
-                                                      int K, float eps, int32_t* __restrict__ nbr,
-                                                      float* __restrict__ d2, float* __restrict__ cov,
-                                                      int* __restrict__ ovf_count, int* __restrict__ ovf_list) {
-    const int total = *count;
-    for (int t = blockIdx.x * kBlock + threadIdx.x; t < total; t += gridDim.x * kBlock) {
-        const int2 e = list[t];
-        const int id = e.x;
-        const Grid& g = lvs.lv[e.y];
-        float qx, qy, qz;
-        int64_t row;
-        src.get(id, qx, qy, qz, row);
-        const QGeom G = make_geom(g, qx, qy, qz);
-        unsigned long long L[KCAP];
-        int ovf;
-        knn_exact<KCAP>(src.pts, g, G, L, K, ovf);
-        if (ovf) {
-            ovf_list[atomicAdd(ovf_count, 1)] = id;
-            continue;
+__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_exact(QuerySrc src, const float4* __restrict__ pts_orig,
+                                                                   Levels lvs, int n_levels,
+                                                                   const int2* __restrict__ list,
+                                                                   const int* __restrict__ count, int K, float eps,
+                                                                   int32_t* __restrict__ nbr, float* __restrict__ d2,
+                                                                   float* __restrict__ cov, int* __restrict__ ovf_count,
+                                                                   int* __restrict__ ovf_list) {
+    extern __shared__ unsigned long long smem[];
+    constexpr int NH = FastShape<KCAP>::NH;
+    unsigned long long* heap = smem;
+    for (int i = K; i < NH; ++i) heap[i * kBlock + threadIdx.x] = 0ull;
+    const int64_t total = *count;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31));
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    for (int64_t base = warp0; base < total; base += stride) {
+        const int64_t t = base + lane;
+        const bool active = t < total;
+        int2 e = make_int2(0, 0);
+        float qx = 0.f, qy = 0.f, qz = 0.f;
+        int64_t row = 0;
+        if (active) {
+            e = list[t];
+            src.get(e.x, qx, qy, qz, row);
         }
-        emit_row<KCAP>(src.pts, L, K, KCAP - K, false, pts_orig, row, eps, nbr, d2, cov);
+        bool pending = active;
+        for (int l = 0; l < n_levels; ++l) {
+            const bool part = pending && l >= e.y;
+            if (!__any_sync(0xffffffffu, part)) continue;
+            const Grid g = lvs.lv[l];
+            const QGeom G = make_geom(g, qx, qy, qz);
+            const int st = knn_fast<KCAP, true>(src.pts, g, G, K, part, heap + threadIdx.x);
+            if (part && st == 0) {
+                emit_row_smem<true>(src.pts, heap + threadIdx.x, K, row, eps, nbr, d2, cov, pts_orig);
+                pending = false;
+            }
+            for (int r = K; r < NH; ++r) heap[r * kBlock + threadIdx.x] = 0ull;
+        }
+        if (pending) {  // pyramid exhausted: ring expansion at the last level (per lane)
+            const Grid& g = lvs.lv[n_levels - 1];
+            const QGeom G = make_geom(g, qx, qy, qz);
+            unsigned long long L[KCAP];
+            int ovf;
+            knn_exact<KCAP>(src.pts, g, G, L, K, ovf);
+            if (ovf)
+                ovf_list[atomicAdd(ovf_count, 1)] = e.x;
+            else
+                emit_row<KCAP>(src.pts, L, K, KCAP - K, false, pts_orig, row, eps, nbr, d2, cov);
+        }
     }
 }
 
@@ -709,6 +750,7 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     const size_t shmem = (size_t)FastShape<KCAP>::NH * kBlock * sizeof(unsigned long long);
     cudaFuncSetAttribute(k_knn_level<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
     cudaFuncSetAttribute(k_knn_escalate<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    cudaFuncSetAttribute(k_knn_exact<KCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
     const int L = idx->n_levels;
     const unsigned full_blocks = (unsigned)((m + kBlock - 1) / kBlock);
     const unsigned some_blocks = (unsigned)std::min<int64_t>(full_blocks, 148 * 8);
@@ -720,10 +762,17 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     if (L > 1)
         k_knn_escalate<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, lvs, L, listA, counts + 2, k, eps, nbr, d2, cov,
                                                                 counts + 0, exact);
-    k_knn_exact<KCAP><<<some_blocks, kBlock, 0, s>>>(src, idx->pts_orig, lvs, exact, counts + 0, k, eps, nbr, d2,
-                                                      cov, counts + 1, ovf);
+    k_knn_exact<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, idx->pts_orig, lvs, L, exact, counts + 0, k, eps, nbr,
+                                                          d2, cov, counts + 1, ovf);
     k_knn_bruteforce<KCAP><<<(unsigned)std::min<int64_t>(m, 1024), kBFBlock, 0, s>>>(
         src, idx->pts_orig, idx->n, ovf, counts + 1, k, eps, nbr, d2, cov);
+    if (getenv("GICP_DEBUG_STATS")) {  // diagnostics only: path counts of this call
+        int h[4] = {0, 0, 0, 0};
+        cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[gicp knn] m=%lld levels=%d escalated=%d exact=%d bruteforce=%d\n", (long long)m, L, h[2],
+                h[0], h[1]);
+    }
     return check_cuda(cudaGetLastError(), "knn launch");
 }
 
