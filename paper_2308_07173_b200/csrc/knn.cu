@@ -607,11 +607,16 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_exact(QuerySrc sr
     for (int i = K; i < NH; ++i) heap[i * kBlock + threadIdx.x] = 0ull;
     const int64_t total = *count;
     const int lane = threadIdx.x & 31;
-    const int64_t warp0 = ((int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31));
-    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    // few entries (the usual case): one query per warp (lane 0) so they run in
+    // parallel rather than as one warp's 32 lanes back to back
+    const int64_t nwarps = (int64_t)gridDim.x * (kBlock / 32);
+    const bool sparse = total <= nwarps;
+    const int64_t wid = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    const int64_t warp0 = sparse ? wid : ((int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31));
+    const int64_t stride = sparse ? nwarps : (int64_t)gridDim.x * kBlock;
     for (int64_t base = warp0; base < total; base += stride) {
-        const int64_t t = base + lane;
-        const bool active = t < total;
+        const int64_t t = sparse ? base : base + lane;
+        const bool active = sparse ? (lane == 0) : (t < total);
         int2 e = make_int2(0, 0);
         float qx = 0.f, qy = 0.f, qz = 0.f;
         int64_t row = 0;
@@ -772,6 +777,13 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
         cudaStreamSynchronize(s);
         fprintf(stderr, "[gicp knn] m=%lld levels=%d escalated=%d exact=%d bruteforce=%d\n", (long long)m, L, h[2],
                 h[0], h[1]);
+        if (h[0] > 0) {
+            int2 ex[16];
+            const int ne = h[0] < 16 ? h[0] : 16;
+            cudaMemcpyAsync(ex, exact, ne * sizeof(int2), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            for (int i = 0; i < ne; ++i) fprintf(stderr, "   exact id=%d level=%d\n", ex[i].x, ex[i].y);
+        }
     }
     return check_cuda(cudaGetLastError(), "knn launch");
 }

@@ -36,41 +36,47 @@ struct Pose {
 struct Levels {
     Grid lv[kMaxLevels];
     int n;
+    int ring_level;  // finest level with cell >= r/2: rings there reach the gate in <= 3 steps
 };
 
 // Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) over all
-// targets whenever that d2 < r2; bp = its coordinates. The 27-voxel cube of
-// level 0 first; if the stop rule (no unsearched point below min(best, r2))
-// fails, the next pyramid level's cube (a superset); ring expansion at the last.
-__device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, float qx, float qy,
-                                          float qz, float r2, unsigned long long& best, float3& bp, int& overflow) {
+// targets whenever that d2 < r2; bp = its coordinates. WARP-SYNCHRONOUS: all 32
+// lanes call it (`active` = the lane has a point). Level 0's 27-voxel cube is
+// gathered (27 independent probes) and scanned as one flattened stream per lane
+// in lockstep (no divergent per-voxel loops); the few points the stop rule (no
+// unsearched point below min(best, r2)) does not settle continue per lane:
+// coarser levels up to `ring_level`, then ring expansion there.
+__device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
+                                          float qy, float qz, float r2, unsigned long long& best, float3& bp,
+                                          int& overflow) {
     best = kEmptyKey;
     overflow = 0;
+    bp = make_float3(0.f, 0.f, 0.f);
     auto bound = [&]() { return fminf(__uint_as_float((unsigned)(best >> 32)), r2); };
-    auto scan = [&](int2 rng) {
-        for (int j = rng.x; j < rng.y; ++j) {
-            const float4 p = __ldg(pts + j);
-            const float d2 = dist2(qx, qy, qz, p.x, p.y, p.z);
-            const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
-            if (key < best) {
-                best = key;
-                bp = make_float3(p.x, p.y, p.z);
-            }
+    auto consider = [&](int j) {
+        const float4 p = __ldg(pts + j);
+        const float d2 = dist2(qx, qy, qz, p.x, p.y, p.z);
+        const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
+        if (key < best) {
+            best = key;
+            bp = make_float3(p.x, p.y, p.z);
         }
     };
-    for (int l = 0; l < lvs.n; ++l) {
-        const Grid& g = lvs.lv[l];
+    auto scan = [&](int2 rng) {
+        for (int j = rng.x; j < rng.y; ++j) consider(j);
+    };
+    // (1) level 0, the 27-voxel cube, lanes in lockstep
+    {
+        const Grid& g = lvs.lv[0];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
-        {
-            // the 27 voxel probes are independent: issue them all (unrolled) and keep
-            // the non-empty ranges with their lower bounds, then scan nearest-first
+        int2 rl[27];
+        float lbl[27];
+        int nr = 0;
+        if (active) {
             const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
             const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
             const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
-            int2 rl[27];
-            float lbl[27];
-            int nr = 0;
             const int4* __restrict__ Hh = reinterpret_cast<const int4*>(g.hash);
 #pragma unroll
             for (int c = 0; c < 27; ++c) {
@@ -83,6 +89,9 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 const int cx = G.cx + dx, cy = G.cy + dy, cz = G.cz + dz;
                 if ((unsigned)cx >= (unsigned)g.nx || (unsigned)cy >= (unsigned)g.ny || (unsigned)cz >= (unsigned)g.nz)
                     continue;
+                const float lb2 =
+                    __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
+                if (lb2 * kRel > r2) continue;  // beyond the gate: cannot hold an inlier
                 const unsigned long long key = cell_key(cx, cy, cz);
                 unsigned long long h = hash_slot(g, key);
                 int4 e = __ldg(Hh + h);
@@ -93,21 +102,51 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 }
                 if (e.x == -1 && e.y == -1) continue;
                 rl[nr] = make_int2(e.z, e.w);
-                lbl[nr] = __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
+                lbl[nr] = lb2;
                 ++nr;
             }
-            for (int r = 0; r < nr; ++r) {
-                if (lbl[r] * kRel > bound()) continue;
-                scan(rl[r]);
-            }
         }
+        int ri = 0, pos = 0, end = 0;
+        while (true) {
+            while (pos == end && ri < nr) {
+                if (lbl[ri] * kRel > bound()) {
+                    ++ri;
+                    continue;
+                }
+                pos = rl[ri].x;
+                end = rl[ri].y;
+                ++ri;
+            }
+            const bool has = pos < end;
+            if (!__any_sync(0xffffffffu, has)) break;
+            if (has) consider(pos++);
+        }
+        if (!active) return;
         const float m = cube_margin(G, s, slack, 1);
         if (m > 0.0f && bound() < m * m * kRel) return;
-        const bool covers = G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 &&
-                            G.cz >= g.nz - 2;
-        if (covers) return;
-        if (l + 1 < lvs.n) continue;
-        // last level: ring expansion
+        if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) return;
+    }
+    // (2) per lane: coarser levels' cubes up to ring_level, then rings there
+    for (int l = 1; l <= lvs.ring_level; ++l) {
+        const Grid& g = lvs.lv[l];
+        const QGeom G = make_geom(g, qx, qy, qz);
+        const float s = g.cell, slack = g.slack;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const float gx = axis_gap(dx, G.fx, s, slack), gy = axis_gap(dy, G.fy, s, slack),
+                                gz = axis_gap(dz, G.fz, s, slack);
+                    if (__fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx)) * kRel > bound()) continue;
+                    scan(cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz));
+                }
+        const float m = cube_margin(G, s, slack, 1);
+        if (m > 0.0f && bound() < m * m * kRel) return;
+        if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) return;
+    }
+    {
+        const Grid& g = lvs.lv[lvs.ring_level];
+        const QGeom G = make_geom(g, qx, qy, qz);
+        const float s = g.cell, slack = g.slack;
         const int R0 = max(max(max(-G.cx, G.cx - (g.nx - 1)), max(-G.cy, G.cy - (g.ny - 1))),
                            max(-G.cz, G.cz - (g.nz - 1)));
         for (int R = 2;; ++R) {
@@ -258,36 +297,44 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
 #pragma unroll 1
     for (int k = 0; k < kPPT; ++k) {
         const int64_t i = base + (int64_t)k * kLinBlock;
-        if (i >= ns) break;
-        const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
-        double pp[3];
+        const bool active = i < ns;  // warp-uniform loop: every lane reaches the search
+        double pp[3] = {0.0, 0.0, 0.0};
+        if (active) {
+            const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-            pp[a] = __fma_rn(P.R[3 * a + 2], pz, __fma_rn(P.R[3 * a + 1], py, __fma_rn(P.R[3 * a], px, P.t[a])));
-        int orig;
-        float qx, qy, qz;
+            for (int a = 0; a < 3; ++a)
+                pp[a] = __fma_rn(P.R[3 * a + 2], pz, __fma_rn(P.R[3 * a + 1], py, __fma_rn(P.R[3 * a], px, P.t[a])));
+        }
+        int orig = -1;
+        float qx = 0.f, qy = 0.f, qz = 0.f;
         if (REUSE) {
-            orig = corr[i];
-            if (orig < 0 || orig >= nt) continue;
-            const float4 q = __ldg(pts_orig + orig);
-            qx = q.x;
-            qy = q.y;
-            qz = q.z;
+            if (active) {
+                orig = corr[i];
+                if (orig >= nt) orig = -1;
+                if (orig >= 0) {
+                    const float4 q = __ldg(pts_orig + orig);
+                    qx = q.x;
+                    qy = q.y;
+                    qz = q.z;
+                }
+            }
         } else {
             const float sx = (float)pp[0], sy = (float)pp[1], sz = (float)pp[2];
             unsigned long long best;
-            float3 bp = make_float3(0.f, 0.f, 0.f);
+            float3 bp;
             int ovf;
-            nn_search(pts, lvs, sx, sy, sz, r2, best, bp, ovf);
-            if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp);
-            const float bd2 = __uint_as_float((unsigned)(best >> 32));
-            orig = (best != kEmptyKey && bd2 < r2) ? (int)(best & 0xffffffffu) : -1;
-            if (corr) corr[i] = orig;
-            if (orig < 0) continue;
-            qx = bp.x;
-            qy = bp.y;
-            qz = bp.z;
+            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bp, ovf);
+            if (active) {
+                if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp);
+                const float bd2 = __uint_as_float((unsigned)(best >> 32));
+                orig = (best != kEmptyKey && bd2 < r2) ? (int)(best & 0xffffffffu) : -1;
+                if (corr) corr[i] = orig;
+                qx = bp.x;
+                qy = bp.y;
+                qz = bp.z;
+            }
         }
+        if (!active || orig < 0) continue;
         float cp[6], cq[6];
         load_cov6(src_cov, i, cp);
         load_cov6(tgt_cov, orig, cq);
@@ -376,6 +423,12 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
+    lvs.ring_level = lvs.n - 1;
+    for (int l = 0; l < lvs.n; ++l)
+        if (2.0f * tgt->lv[l].cell >= max_corr_dist) {
+            lvs.ring_level = l;
+            break;
+        }
     void* scratch = nullptr;
     const size_t bytes = (size_t)nb * (kNumAcc + 1) * sizeof(double) + 256;
     if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
