@@ -201,6 +201,7 @@ def main():
         imap = g.build_index(map_d, MAP_CELL)
         e[1].record(stream)
         _, _, cov_map = g.knn_cov_self(imap, K, EPS, with_nbr=True)
+        g.attach_cov(imap, cov_map)
         e[2].record(stream)
         iscan = g.build_index(scan_d, 0.0)
         _, _, cov_scan = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
@@ -289,6 +290,7 @@ def main():
             sd = scan_h.to(dev, non_blocking=True)
             imap = g.build_index(md, MAP_CELL)
             _, _, cm = g.knn_cov_self(imap, K, EPS, with_nbr=True)
+            g.attach_cov(imap, cm)
             iscan = g.build_index(sd, 0.0)
             _, _, cs = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
             T, info = g.align(sd, cs, imap, cm, T0)

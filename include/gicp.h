@@ -87,6 +87,15 @@ typedef struct {
     int32_t n_levels;     /* voxel pyramid levels (cell_l = cell_size * 2^l) */
 } gicp_index_info;
 
+/* Attach the covariances of the index's points (cov [n][6], ORIGINAL order,
+ * device; e.g. the output of gicp_knn_cov_self): the index keeps a copy permuted
+ * into its sorted order, and gicp_linearize / gicp_align use that copy whenever
+ * they are passed this same `cov` pointer as tgt_cov (the results are identical;
+ * the target covariance is then read next to the target point instead of by a
+ * random gather). Re-attach after modifying `cov`. Stream-ordered.
+ * Errors: EINVAL (null), ENOMEM, ECUDA. */
+int gicp_index_attach_cov(gicp_index idx, const float* cov, void* stream);
+
 /* Host-side description of an index. Errors: EINVAL. */
 int gicp_get_index_info(gicp_index idx, gicp_index_info* info /* host */);
 

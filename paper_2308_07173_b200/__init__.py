@@ -56,6 +56,7 @@ _lib.gicp_build_index.argtypes = [_P, _i64, _f32, _P, ctypes.POINTER(_P)]
 _lib.gicp_index_free.argtypes = [_P]
 _lib.gicp_index_free.restype = None
 _lib.gicp_get_index_info.argtypes = [_P, ctypes.POINTER(IndexInfo)]
+_lib.gicp_index_attach_cov.argtypes = [_P, _P, _P]
 _lib.gicp_knn.argtypes = [_P, _P, _i64, _i32, _P, _P, _P]
 _lib.gicp_knn_self.argtypes = [_P, _i32, _P, _P, _P]
 _lib.gicp_covariances.argtypes = [_P, _i64, _P, _i64, _i32, _f32, _P, _P]
@@ -65,6 +66,7 @@ _lib.gicp_align.argtypes = [_P, _P, _i64, _P, _P, _P, ctypes.POINTER(AlignParams
                             _P]
 
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
+           "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align"]
 
 
@@ -136,6 +138,15 @@ def build_index(xyz: torch.Tensor, cell_size: float = 0.0) -> Index:
     h = ctypes.c_void_p()
     _check(_lib.gicp_build_index(_dptr(xyz), xyz.shape[0], float(cell_size), _stream(), ctypes.byref(h)))
     return Index(h, xyz.device)
+
+
+def attach_cov(index: Index, cov: torch.Tensor) -> None:
+    """gicp_index_attach_cov: keep a sorted-order copy of `cov` ([n, 6], original
+    order) in the index; linearize/align use it when passed this same tensor."""
+    if cov.dtype != torch.float32 or cov.shape != (index.n, 6) or not cov.is_contiguous():
+        raise ValueError("cov must be a contiguous float32 [n, 6] tensor")
+    _check(_lib.gicp_index_attach_cov(index.handle, _dptr(cov), _stream()))
+    index._attached = cov  # keep the tensor alive while attached
 
 
 def knn(index: Index, q: torch.Tensor, k: int, out=None):

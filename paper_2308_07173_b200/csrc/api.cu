@@ -163,8 +163,15 @@ GICP_API void gicp_index_free(gicp_index idx) {
     }
     cudaFreeAsync(idx->pts_orig, s);
     cudaFreeAsync(idx->hash_mem, s);
+    if (idx->cov_sorted) cudaFreeAsync(idx->cov_sorted, s);
     cudaGetLastError();
     delete idx;
+}
+
+GICP_API int gicp_index_attach_cov(gicp_index idx, const float* cov, void* stream) {
+    if (!idx || !cov) return set_error(GICP_EINVAL, "gicp_index_attach_cov: null pointer");
+    init_pool_once();
+    return attach_covariances(idx, cov, (cudaStream_t)stream);
 }
 
 GICP_API int gicp_get_index_info(gicp_index idx, gicp_index_info* info) {
@@ -256,16 +263,33 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     cudaStream_t s = (cudaStream_t)stream;
     double* h = pinned29();
     if (!h) return set_error(GICP_ENOMEM, "gicp_align: pinned buffer");
-    double* d_out = nullptr;
-    int32_t* d_corr = nullptr;
-    if (cudaMallocAsync(&d_out, 64 * sizeof(double), s) != cudaSuccess ||
-        cudaMallocAsync(&d_corr, (size_t)(ns > 0 ? ns : 1) * sizeof(int32_t), s) != cudaSuccess) {
+    // one scratch block for the whole alignment: out29 | done counter | block
+    // partials | correspondences | Morton-sorted copies of the source and its
+    // covariances
+    const int64_t nsa = ns > 0 ? ns : 1;
+    const size_t lin_bytes = linearize_scratch_bytes(nsa);
+    const size_t bytes = 512 + lin_bytes + nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256;
+    char* scratch = nullptr;
+    if (cudaMallocAsync((void**)&scratch, bytes, s) != cudaSuccess) {
         cudaGetLastError();
-        if (d_out) cudaFreeAsync(d_out, s);
         return set_error(GICP_ENOMEM, "gicp_align: scratch allocation failed");
     }
+    double* d_out = (double*)scratch;
+    LinScratch ls;
+    ls.done = (unsigned*)(scratch + 256);
+    ls.partials = (double*)(scratch + 512);
+    int32_t* d_corr = (int32_t*)(scratch + 512 + lin_bytes);
+    float* src_p = (float*)(((uintptr_t)(d_corr + nsa) + 15) & ~(uintptr_t)15);
+    float* cov_p = src_p + 3 * nsa;
+    int rc0 = check_cuda(cudaMemsetAsync(ls.done, 0, sizeof(unsigned), s), "memset");
+    if (!rc0 && ns > 0) rc0 = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s);
+    if (rc0) {
+        cudaFreeAsync(scratch, s);
+        return rc0;
+    }
     auto lin = [&](const double* T, int flags) -> int {
-        int rc = launch_linearize(src, src_cov, ns, tgt, tgt_cov, T, prm->max_corr_dist, flags, d_out, d_corr, s);
+        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, prm->max_corr_dist, flags | kLinCorrSpos, d_out,
+                                  d_corr, s, &ls);
         if (rc) return rc;
         if ((rc = check_cuda(cudaMemcpyAsync(h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
             return rc;
@@ -351,8 +375,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
             break;
         }
     }
-    cudaFreeAsync(d_out, s);
-    cudaFreeAsync(d_corr, s);
+    cudaFreeAsync(scratch, s);
     std::memcpy(res->T, T, sizeof(T));
     res->iterations = it > prm->max_iter ? prm->max_iter : it;
     res->converged = converged;

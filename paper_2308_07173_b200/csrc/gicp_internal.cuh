@@ -149,6 +149,8 @@ struct gicp_index_s {
     float4* pts = nullptr;
     float4* pts_orig = nullptr;
     gicp::HashEntry* hash_mem = nullptr;  // all levels' tables, one allocation
+    float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
+    const float* cov_attached = nullptr;  // the caller's original-order array they were copied from
     int device = 0;
     cudaStream_t stream = nullptr;  // build stream: device memory is pool-allocated on it
     int64_t device_bytes = 0;
@@ -166,8 +168,18 @@ int launch_knn_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, flo
 int launch_knn(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, cudaStream_t s);
 int launch_covariances(const float* xyz, int64_t n, const int32_t* nbr, int64_t m, int k, float eps, float* cov,
                        cudaStream_t s);
+// preallocated linearize scratch (gicp_align): block partials + done counter
+struct LinScratch {
+    unsigned* done;
+    double* partials;
+};
+constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
+size_t linearize_scratch_bytes(int64_t ns);
 int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                      const float* tgt_cov, const double T[16], float max_corr_dist, int flags, double* out29,
-                     int32_t* corr, cudaStream_t s);
+                     int32_t* corr, cudaStream_t s, const LinScratch* pre = nullptr);
+int attach_covariances(gicp_index_s* idx, const float* cov, cudaStream_t s);
+int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
+                cudaStream_t s);
 
 }  // namespace gicp

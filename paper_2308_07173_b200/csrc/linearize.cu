@@ -47,10 +47,11 @@ struct Levels {
 // unsearched point below min(best, r2)) does not settle continue per lane:
 // coarser levels up to `ring_level`, then ring expansion there.
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
-                                          float qy, float qz, float r2, unsigned long long& best, float3& bp,
+                                          float qy, float qz, float r2, unsigned long long& best, float3& bp, int& bj,
                                           int& overflow) {
     best = kEmptyKey;
     overflow = 0;
+    bj = -1;
     bp = make_float3(0.f, 0.f, 0.f);
     auto bound = [&]() { return fminf(__uint_as_float((unsigned)(best >> 32)), r2); };
     auto consider = [&](int j) {
@@ -60,6 +61,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         if (key < best) {
             best = key;
             bp = make_float3(p.x, p.y, p.z);
+            bj = j;
         }
     };
     auto scan = [&](int2 rng) {
@@ -188,7 +190,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
 
 // brute-force fallback for overflowed searches (the caller handles one point)
 __device__ __forceinline__ void nn_bruteforce(const float4* __restrict__ pts, int64_t n, float qx, float qy, float qz,
-                                              unsigned long long& best, float3& bp) {
+                                              unsigned long long& best, float3& bp, int& bj) {
     best = kEmptyKey;
     for (int64_t j = 0; j < n; ++j) {
         const float4 p = __ldg(pts + j);
@@ -197,8 +199,21 @@ __device__ __forceinline__ void nn_bruteforce(const float4* __restrict__ pts, in
         if (key < best) {
             best = key;
             bp = make_float3(p.x, p.y, p.z);
+            bj = (int)j;
         }
     }
+}
+
+// target covariance of a correspondence: the index's sorted-order copy (2 x
+// float4, one 32-B sector, spatially coherent) or the caller's original order
+__device__ __forceinline__ void load_cov_sorted(const float4* __restrict__ c8, int spos, float o[6]) {
+    const float4 a = __ldg(c8 + 2 * (int64_t)spos), b = __ldg(c8 + 2 * (int64_t)spos + 1);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = a.z;
+    o[3] = a.w;
+    o[4] = b.x;
+    o[5] = b.y;
 }
 
 __device__ __forceinline__ void load_cov6(const float* __restrict__ c, int64_t row, float o[6]) {
@@ -282,11 +297,14 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <bool REUSE, bool ERROR_ONLY>
+// SORTED: target covariances from the index's sorted-order copy; SPOS: corr holds
+// sorted positions (internal to gicp_align) instead of original indices.
+template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS>
 __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
                                                          const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
-                                                         const float* __restrict__ tgt_cov, Pose P, float r2,
+                                                         const float* __restrict__ tgt_cov,
+                                                         const float4* __restrict__ tgt_cov_sorted, Pose P, float r2,
                                                          int32_t* __restrict__ corr, double* __restrict__ partials,
                                                          unsigned* __restrict__ done, double* __restrict__ out29) {
     double acc[kNumAcc];
@@ -305,30 +323,33 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             for (int a = 0; a < 3; ++a)
                 pp[a] = __fma_rn(P.R[3 * a + 2], pz, __fma_rn(P.R[3 * a + 1], py, __fma_rn(P.R[3 * a], px, P.t[a])));
         }
-        int orig = -1;
+        int orig = -1, spos = -1;
         float qx = 0.f, qy = 0.f, qz = 0.f;
         if (REUSE) {
             if (active) {
-                orig = corr[i];
-                if (orig >= nt) orig = -1;
-                if (orig >= 0) {
-                    const float4 q = __ldg(pts_orig + orig);
+                const int c = corr[i];
+                if (c >= 0 && c < nt) {
+                    const float4 q = SPOS ? __ldg(pts + c) : __ldg(pts_orig + c);
                     qx = q.x;
                     qy = q.y;
                     qz = q.z;
+                    orig = SPOS ? __float_as_int(q.w) : c;
+                    spos = SPOS ? c : __float_as_int(q.w);
                 }
             }
         } else {
             const float sx = (float)pp[0], sy = (float)pp[1], sz = (float)pp[2];
             unsigned long long best;
             float3 bp;
-            int ovf;
-            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bp, ovf);
+            int bj, ovf;
+            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bp, bj, ovf);
             if (active) {
-                if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp);
+                if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp, bj);
                 const float bd2 = __uint_as_float((unsigned)(best >> 32));
-                orig = (best != kEmptyKey && bd2 < r2) ? (int)(best & 0xffffffffu) : -1;
-                if (corr) corr[i] = orig;
+                const bool inl = best != kEmptyKey && bd2 < r2;
+                orig = inl ? (int)(best & 0xffffffffu) : -1;
+                spos = inl ? bj : -1;
+                if (corr) corr[i] = SPOS ? spos : orig;
                 qx = bp.x;
                 qy = bp.y;
                 qz = bp.z;
@@ -337,7 +358,10 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         if (!active || orig < 0) continue;
         float cp[6], cq[6];
         load_cov6(src_cov, i, cp);
-        load_cov6(tgt_cov, orig, cq);
+        if (SORTED)
+            load_cov_sorted(tgt_cov_sorted, spos, cq);
+        else
+            load_cov6(tgt_cov, orig, cq);
         accumulate_point<ERROR_ONLY>(P, pp, qx, qy, qz, cp, cq, acc);
         cnt += 1.0;
     }
@@ -404,7 +428,7 @@ __global__ void k_zero29(double* out29) {
 
 int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                      const float* tgt_cov, const double T[16], float max_corr_dist, int flags, double* out29,
-                     int32_t* corr, cudaStream_t s) {
+                     int32_t* corr, cudaStream_t s, const LinScratch* pre) {
     if (ns == 0) {
         k_zero29<<<1, 32, 0, s>>>(out29);
         return check_cuda(cudaGetLastError(), "linearize launch");
@@ -430,31 +454,60 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
             break;
         }
     void* scratch = nullptr;
-    const size_t bytes = (size_t)nb * (kNumAcc + 1) * sizeof(double) + 256;
-    if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
-        cudaGetLastError();
-        return set_error(GICP_ENOMEM, "linearize scratch allocation failed");
+    unsigned* done;
+    double* partials;
+    if (pre) {
+        done = pre->done;
+        partials = pre->partials;
+    } else {
+        const size_t bytes = linearize_scratch_bytes(ns);
+        if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(GICP_ENOMEM, "linearize scratch allocation failed");
+        }
+        done = (unsigned*)scratch;
+        partials = (double*)((char*)scratch + 256);
+        int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset");
+        if (rc) {
+            cudaFreeAsync(scratch, s);
+            return rc;
+        }
     }
-    unsigned* done = (unsigned*)scratch;
-    double* partials = (double*)((char*)scratch + 256);
-    int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset");
-    if (rc == GICP_OK) {
-        const bool reuse = flags & GICP_LIN_REUSE_CORR, eonly = flags & GICP_LIN_ERROR_ONLY;
+    // the counter is reset by the last block of every launch, so a preallocated
+    // scratch stays valid across calls on one stream
+    const bool reuse = flags & GICP_LIN_REUSE_CORR, eonly = flags & GICP_LIN_ERROR_ONLY;
+    const bool sorted = tgt->cov_sorted != nullptr && tgt_cov == tgt->cov_attached;
+    const bool spos = (flags & kLinCorrSpos) && sorted;
 #define GICP_LIN_ARGS \
-    src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, P, r2, corr, partials, done, out29
-        if (reuse && eonly)
-            k_linearize<true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
-        else if (reuse)
-            k_linearize<true, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
-        else if (eonly)
-            k_linearize<false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
-        else
-            k_linearize<false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
-#undef GICP_LIN_ARGS
-        rc = check_cuda(cudaGetLastError(), "linearize launch");
+    src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, partials, done, out29
+#define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
+#define GICP_LIN_RE(S, SP)           \
+    if (reuse && eonly)              \
+        GICP_LIN_GO(true, true, S, SP);   \
+    else if (reuse)                  \
+        GICP_LIN_GO(true, false, S, SP);  \
+    else if (eonly)                  \
+        GICP_LIN_GO(false, true, S, SP);  \
+    else                             \
+        GICP_LIN_GO(false, false, S, SP);
+    if (spos) {
+        GICP_LIN_RE(true, true)
+    } else if (sorted) {
+        GICP_LIN_RE(true, false)
+    } else {
+        GICP_LIN_RE(false, false)
     }
-    cudaFreeAsync(scratch, s);
+#undef GICP_LIN_RE
+#undef GICP_LIN_GO
+#undef GICP_LIN_ARGS
+    const int rc = check_cuda(cudaGetLastError(), "linearize launch");
+    if (scratch) cudaFreeAsync(scratch, s);
     return rc;
+}
+
+size_t linearize_scratch_bytes(int64_t ns) {
+    const int64_t nb = (ns + kPPB - 1) / kPPB;
+    return (size_t)nb * (kNumAcc + 1) * sizeof(double) + 256;
 }
 
 }  // namespace gicp

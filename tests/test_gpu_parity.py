@@ -220,6 +220,23 @@ def test_linearize_deterministic_and_empty(orc):
     assert np.all(H(e) == 0)
 
 
+def test_attached_covariances_give_identical_results(orc):
+    # gicp_index_attach_cov is a layout optimisation only: bitwise identical output
+    src, tgt, T_true, T0 = gen.config_c1(sigma=0.002)
+    cs, ct = _covs_oracle(orc, src, 10), _covs_oracle(orc, tgt, 10)
+    idx = g.build_index(D(tgt), 0.6)
+    ctd = D(ct)
+    a, ca = g.linearize(D(src), D(cs), idx, ctd, T0, 1.0)
+    a, ca = H(a).copy(), H(ca).copy()
+    g.attach_cov(idx, ctd)
+    b, cb = g.linearize(D(src), D(cs), idx, ctd, T0, 1.0)
+    assert np.array_equal(H(b), a) and np.array_equal(H(cb), ca)
+    T1, i1 = g.align(D(src), D(cs), idx, ctd, T0)
+    ref = orc.align(src, cs, tgt, ct, T0)
+    dt, dr = _pose_err(T1, ref["T"])
+    assert dt <= 1e-3 and dr <= 1e-4
+
+
 def test_linearize_c2_scan_to_scan(orc):
     src, tgt, T_rel, T0 = gen.config_c2(30_000)
     cs, ct = _covs_oracle(orc, src, 20), _covs_oracle(orc, tgt, 20)

@@ -1,0 +1,37 @@
+"""Time gicp_linearize on C3 (100k scan vs 2M map) at T_true and at T0."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import gen
+import paper_2308_07173_b200 as g
+
+sc, mp, T, T0 = gen.config_c3()
+md = torch.from_numpy(np.array(mp)).cuda()
+sd = torch.from_numpy(np.array(sc)).cuda()
+im = g.build_index(md, 0.5)
+cm = torch.from_numpy(gen.random_covariances(len(mp), 2)).cuda()
+cs = torch.from_numpy(gen.random_covariances(len(sc), 1)).cuda()
+out = torch.empty(29, dtype=torch.float64, device="cuda")
+if os.environ.get("LB_ATTACH"):
+    g.attach_cov(im, cm)
+corr = torch.empty(len(sc), dtype=torch.int32, device="cuda")
+prof = os.environ.get("LB_PROF")
+for name, TT, kw in (("T_true", T, {}), ("T0", T0, {}), ("T_true reuse+err", T, dict(reuse_corr=True, error_only=True))):
+    ts = []
+    for r in range(12):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if prof and r == 11:
+            torch.cuda.cudart().cudaProfilerStart()
+        a.record()
+        g.linearize(sd, cs, im, cm, TT, 1.0, corr=corr, out=out, **kw)
+        b.record()
+        torch.cuda.synchronize()
+        if prof and r == 11:
+            torch.cuda.cudart().cudaProfilerStop()
+        if r >= 2:
+            ts.append(a.elapsed_time(b))
+    print(f"linearize {name}: median {1e3 * np.median(ts):.1f} us  inliers {out[28].item():.0f}")
