@@ -164,6 +164,9 @@ GICP_API void gicp_index_free(gicp_index idx) {
     cudaFreeAsync(idx->pts_orig, s);
     cudaFreeAsync(idx->hash_mem, s);
     if (idx->cov_sorted) cudaFreeAsync(idx->cov_sorted, s);
+    if (idx->adj_off) cudaFreeAsync(idx->adj_off, s);
+    if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
+    if (idx->adj_code) cudaFreeAsync(idx->adj_code, s);
     cudaGetLastError();
     delete idx;
 }

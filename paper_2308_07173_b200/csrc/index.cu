@@ -136,6 +136,46 @@ __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__
     pts_orig[j] = make_float4(x, y, z, __int_as_float((int)i));
 }
 
+// Level-0 voxel adjacency lists: for every occupied voxel, its
+// non-empty voxels among the 27 around it, nearest-first, as (start, end) ranges
+// of pts plus a 5-bit offset code (dx+1)*9 + (dy+1)*3 + (dz+1). A query in an
+// occupied voxel reads this shared list instead of probing the hash 27 times.
+__device__ __constant__ signed char c_adj_order[27][3] = {
+    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
+    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
+    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
+    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+
+template <bool FILL>
+__global__ void k_adjacency(const unsigned long long* __restrict__ keys, const float* __restrict__ xyz,
+                            const int* __restrict__ perm, int64_t n, Grid g, int* __restrict__ off,
+                            int2* __restrict__ rng_out, unsigned char* __restrict__ code_out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bool head = (i == 0 || keys[i - 1] != keys[i]);
+    if (!head) {
+        if (!FILL) off[i] = 0;
+        return;
+    }
+    const int64_t j = perm[i];
+    const int cx = cell_coord(xyz[3 * j], g.ox, g.inv_cell), cy = cell_coord(xyz[3 * j + 1], g.oy, g.inv_cell),
+              cz = cell_coord(xyz[3 * j + 2], g.oz, g.inv_cell);
+    int cnt = 0;
+    int o = FILL ? off[i] : 0;
+    for (int c = 0; c < 27; ++c) {
+        const int dx = c_adj_order[c][0], dy = c_adj_order[c][1], dz = c_adj_order[c][2];
+        const int2 r = cell_lookup(g, cx + dx, cy + dy, cz + dz);
+        if (r.y <= r.x) continue;
+        if (FILL) {
+            rng_out[o] = r;
+            code_out[o] = (unsigned char)((dx + 1) * 9 + (dy + 1) * 3 + (dz + 1));
+            ++o;
+        }
+        ++cnt;
+    }
+    if (!FILL) off[i] = cnt;
+}
+
 __global__ void k_fill_hash(HashEntry* H, int64_t cap) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < cap) {
@@ -318,6 +358,9 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if (idx->pts) cudaFreeAsync(idx->pts, s);
         if (idx->pts_orig) cudaFreeAsync(idx->pts_orig, s);
         if (idx->hash_mem) cudaFreeAsync(idx->hash_mem, s);
+        if (idx->adj_off) cudaFreeAsync(idx->adj_off, s);
+        if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
+        if (idx->adj_code) cudaFreeAsync(idx->adj_code, s);
         delete idx;
         return code;
     };
@@ -338,6 +381,38 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     }
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
+    {
+        // level-0 adjacency: count, exclusive scan, fill
+        if (cudaMallocAsync(&idx->adj_off, (n + 1) * sizeof(int), s) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
+        }
+        k_adjacency<false><<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, xyz, (int*)perm.p, n,
+                                                             idx->lv[0], idx->adj_off, nullptr, nullptr);
+        DevBuf cnt1, tmp;
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, idx->adj_off, idx->adj_off, (int)(n + 1), s);
+        if ((rc = alloc_async(tmp, tb, s))) return fail(rc);
+        if ((rc = check_cuda(cudaMemsetAsync(idx->adj_off + n, 0, sizeof(int), s), "memset"))) return fail(rc);
+        if ((rc = check_cuda(cub::DeviceScan::ExclusiveSum(tmp.p, tb, idx->adj_off, idx->adj_off, (int)(n + 1), s),
+                             "adjacency scan")))
+            return fail(rc);
+        int total = 0;
+        if ((rc = check_cuda(cudaMemcpyAsync(&total, idx->adj_off + n, sizeof(int), cudaMemcpyDeviceToHost, s),
+                             "D2H")))
+            return fail(rc);
+        if ((rc = check_cuda(cudaStreamSynchronize(s), "adjacency"))) return fail(rc);
+        idx->adj_total = total;
+        if (cudaMallocAsync(&idx->adj_rng, (size_t)std::max(total, 1) * sizeof(int2), s) != cudaSuccess ||
+            cudaMallocAsync(&idx->adj_code, (size_t)std::max(total, 1), s) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
+        }
+        k_adjacency<true><<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, xyz, (int*)perm.p, n,
+                                                            idx->lv[0], idx->adj_off, idx->adj_rng, idx->adj_code);
+        idx->device_bytes += (n + 1) * 4 + (int64_t)total * 9;
+        if ((rc = check_cuda(cudaGetLastError(), "adjacency kernels"))) return fail(rc);
+    }
     if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
     *out = idx;
     return GICP_OK;

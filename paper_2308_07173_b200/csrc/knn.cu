@@ -197,17 +197,36 @@ struct FastShape {
     static constexpr int NH = (2 << D) - 1;      // full binary tree slots (>= KCAP)
 };
 
+// level-0 voxel adjacency lists of the index (index.cu)
+struct AdjView {
+    const int* off;
+    const int2* rng;
+    const unsigned char* code;
+};
+
 template <int KCAP, bool EXACT = false>
 __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Grid& g, const QGeom& G, int K,
-                                        bool active, unsigned long long* __restrict__ Hl) {
+                                        bool active, unsigned long long* __restrict__ Hl, AdjView adj) {
     constexpr int D = FastShape<KCAP>::D;
     const float s = g.cell, slack = g.slack;
 #define HSLOT(i) Hl[(i) * kBlock]
-    // (A) gather the voxel ranges (thread-local array: L1-resident local memory)
+    // (A) the voxel ranges: the index's adjacency list of the query's voxel when it
+    // is occupied at level 0 (no probes, shared by the voxel's queries), else a
+    // gather of the 27 probes into a thread-local list
     int2 rl[27];
     float lbl[27];
     int nr = 0;
-    if (active) {
+    int a0 = 0, a1 = 0;
+    bool use_adj = false;
+    if (active && g.level == 0 && adj.off != nullptr) {
+        const int2 own = cell_lookup(g, G.cx, G.cy, G.cz);
+        if (own.y > own.x) {
+            use_adj = true;
+            a0 = __ldg(adj.off + own.x);
+            a1 = __ldg(adj.off + own.x + 1);
+        }
+    }
+    if (active && !use_adj) {
         const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
         const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
         const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
@@ -245,16 +264,33 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
             ++nr;
         }
     }
+    const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
+    const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
+    const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
     // (B)+(C) flattened stream into the heap
     int cnt = 0;
     unsigned long long top = 0ull;  // root (max) once cnt == K
     unsigned tie = 0xffffffffu;
-    int ri = 0, pos = 0, end = 0;
+    int ri = use_adj ? a0 : 0;
+    const int rend = use_adj ? a1 : nr;
+    int pos = 0, end = 0;
     while (true) {
         // advance exhausted lanes to their next non-pruned range
-        while (pos == end && ri < nr) {
-            const int2 r = rl[ri];
-            const float lb2 = lbl[ri];
+        while (pos == end && ri < rend) {
+            int2 r;
+            float lb2;
+            if (use_adj) {
+                r = __ldg(adj.rng + ri);
+                const int code = __ldg(adj.code + ri);
+                const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
+                const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
+                const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
+                const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
+                lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+            } else {
+                r = rl[ri];
+                lb2 = lbl[ri];
+            }
             ++ri;
             if (cnt == K && lb2 * kRel > __uint_as_float(hi32(top))) continue;
             pos = r.x;
@@ -492,7 +528,7 @@ struct QuerySrc {
 // when in_list == nullptr, the identity / perm over [0, m). Warp-uniform
 // grid-stride loop (all 32 lanes stay together for the warp votes).
 template <int KCAP>
-__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_level(QuerySrc src, Grid g, const int* __restrict__ perm, int64_t m,
+__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_level(QuerySrc src, AdjView adj, Grid g, const int* __restrict__ perm, int64_t m,
                                                       const int* __restrict__ in_list, const int* __restrict__ in_count,
                                                       int K, float eps, int32_t* __restrict__ nbr,
                                                       float* __restrict__ d2, float* __restrict__ cov,
@@ -527,7 +563,7 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_level(QuerySrc sr
         }
         const bool run = active && finite;
         const QGeom G = make_geom(g, qx, qy, qz);
-        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x);
+        const int st = knn_fast<KCAP>(src.pts, g, G, K, run, heap + threadIdx.x, adj);
         if (run && st == 0) emit_row_smem(src.pts, heap + threadIdx.x, K, row, eps, nbr, d2, cov);
         for (int r = K; r < NH; ++r) heap[r * kBlock + threadIdx.x] = 0ull;  // restore the 0-key padding
         const bool to_next = run && st == 1 && !last_level;
@@ -542,7 +578,7 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_level(QuerySrc sr
 // level, lanes that finish idle); still-unsettled queries and ties go to the
 // exact path with the level they stopped at.
 template <int KCAP>
-__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_escalate(QuerySrc src, Levels lvs, int n_levels,
+__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_escalate(QuerySrc src, AdjView adj, Levels lvs, int n_levels,
                                                                       const int* __restrict__ in_list,
                                                                       const int* __restrict__ in_count, int K,
                                                                       float eps, int32_t* __restrict__ nbr,
@@ -574,7 +610,7 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_escalate(QuerySrc
             if (!__any_sync(0xffffffffu, pending)) break;
             const Grid g = lvs.lv[l];
             const QGeom G = make_geom(g, qx, qy, qz);
-            const int st = knn_fast<KCAP>(src.pts, g, G, K, pending, heap + threadIdx.x);
+            const int st = knn_fast<KCAP>(src.pts, g, G, K, pending, heap + threadIdx.x, adj);
             if (pending && st == 0) emit_row_smem(src.pts, heap + threadIdx.x, K, row, eps, nbr, d2, cov);
             for (int r = K; r < NH; ++r) heap[r * kBlock + threadIdx.x] = 0ull;
             if (pending && st == 2) {
@@ -594,7 +630,7 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_escalate(QuerySrc
 // special care -- from the level the query stopped at, climbing the pyramid; a
 // query that exhausts it gets the ring-expanding search (register list).
 template <int KCAP>
-__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_exact(QuerySrc src, const float4* __restrict__ pts_orig,
+__global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_exact(QuerySrc src, AdjView adj, const float4* __restrict__ pts_orig,
                                                                    Levels lvs, int n_levels,
                                                                    const int2* __restrict__ list,
                                                                    const int* __restrict__ count, int K, float eps,
@@ -630,7 +666,7 @@ __global__ void __launch_bounds__(kBlock, GICP_KNN_MINB) k_knn_exact(QuerySrc sr
             if (!__any_sync(0xffffffffu, part)) continue;
             const Grid g = lvs.lv[l];
             const QGeom G = make_geom(g, qx, qy, qz);
-            const int st = knn_fast<KCAP, true>(src.pts, g, G, K, part, heap + threadIdx.x);
+            const int st = knn_fast<KCAP, true>(src.pts, g, G, K, part, heap + threadIdx.x, adj);
             if (part && st == 0) {
                 emit_row_smem<true>(src.pts, heap + threadIdx.x, K, row, eps, nbr, d2, cov, pts_orig);
                 pending = false;
@@ -762,12 +798,13 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     Levels lvs;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
     // level 0 over every query, then one launch that climbs the pyramid for the rest
-    k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
+    const AdjView adj{idx->adj_off, idx->adj_rng, idx->adj_code};
+    k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
                                                          cov, counts + 2, listA, counts + 0, exact, L == 1);
     if (L > 1)
-        k_knn_escalate<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, lvs, L, listA, counts + 2, k, eps, nbr, d2, cov,
+        k_knn_escalate<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, adj, lvs, L, listA, counts + 2, k, eps, nbr, d2, cov,
                                                                 counts + 0, exact);
-    k_knn_exact<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, idx->pts_orig, lvs, L, exact, counts + 0, k, eps, nbr,
+    k_knn_exact<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, adj, idx->pts_orig, lvs, L, exact, counts + 0, k, eps, nbr,
                                                           d2, cov, counts + 1, ovf);
     k_knn_bruteforce<KCAP><<<(unsigned)std::min<int64_t>(m, 1024), kBFBlock, 0, s>>>(
         src, idx->pts_orig, idx->n, ovf, counts + 1, k, eps, nbr, d2, cov);

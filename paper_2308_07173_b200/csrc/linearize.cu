@@ -37,6 +37,9 @@ struct Levels {
     Grid lv[kMaxLevels];
     int n;
     int ring_level;  // finest level with cell >= r/2: rings there reach the gate in <= 3 steps
+    const int* adj_off;  // level-0 voxel adjacency lists (index.cu)
+    const int2* adj_rng;
+    const unsigned char* adj_code;
 };
 
 // Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) over all
@@ -75,7 +78,20 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         int2 rl[27];
         float lbl[27];
         int nr = 0;
-        if (active) {
+        int a0 = 0, a1 = 0;
+        bool use_adj = false;
+        if (active && lvs.adj_off != nullptr) {
+            const int2 own = cell_lookup(g, G.cx, G.cy, G.cz);
+            if (own.y > own.x) {
+                use_adj = true;
+                a0 = __ldg(lvs.adj_off + own.x);
+                a1 = __ldg(lvs.adj_off + own.x + 1);
+            }
+        }
+        const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
+        const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
+        const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
+        if (active && !use_adj) {
             const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
             const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
             const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
@@ -108,16 +124,29 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 ++nr;
             }
         }
-        int ri = 0, pos = 0, end = 0;
+        int ri = use_adj ? a0 : 0;
+        const int rend = use_adj ? a1 : nr;
+        int pos = 0, end = 0;
         while (true) {
-            while (pos == end && ri < nr) {
-                if (lbl[ri] * kRel > bound()) {
-                    ++ri;
-                    continue;
+            while (pos == end && ri < rend) {
+                int2 r;
+                float lb2;
+                if (use_adj) {
+                    r = __ldg(lvs.adj_rng + ri);
+                    const int code = __ldg(lvs.adj_code + ri);
+                    const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
+                    const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
+                    const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
+                    const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
+                    lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                } else {
+                    r = rl[ri];
+                    lb2 = lbl[ri];
                 }
-                pos = rl[ri].x;
-                end = rl[ri].y;
                 ++ri;
+                if (lb2 * kRel > bound()) continue;
+                pos = r.x;
+                end = r.y;
             }
             const bool has = pos < end;
             if (!__any_sync(0xffffffffu, has)) break;
@@ -397,16 +426,24 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // 29 components x 8 sub-ranges (fixed split of the block index range)
+    // 29 components x 8 interleaved sub-sequences (block b goes to sub b % 8), the
+    // loads of each thread batched 8 at a time (independent, in flight together),
+    // summed in a fixed order: deterministic and latency-tolerant
     constexpr int kSub = 8;
     __shared__ double part[kSub][kNumAcc + 1];
     const int nb = gridDim.x;
     if (threadIdx.x < kSub * (kNumAcc + 1)) {
         const int c = threadIdx.x % (kNumAcc + 1), sub = threadIdx.x / (kNumAcc + 1);
-        const int chunk = (nb + kSub - 1) / kSub;
-        const int b0 = sub * chunk, b1 = min(nb, b0 + chunk);
         double v = 0.0;
-        for (int b = b0; b < b1; ++b) v += __ldcg(partials + (int64_t)b * (kNumAcc + 1) + c);
+        int b = sub;
+        for (; b + 7 * kSub < nb; b += 8 * kSub) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partials + (int64_t)(b + u * kSub) * (kNumAcc + 1) + c);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v += t[u];
+        }
+        for (; b < nb; b += kSub) v += __ldcg(partials + (int64_t)b * (kNumAcc + 1) + c);
         part[sub][c] = v;
     }
     __syncthreads();
@@ -447,6 +484,9 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
+    lvs.adj_off = tgt->adj_off;
+    lvs.adj_rng = tgt->adj_rng;
+    lvs.adj_code = tgt->adj_code;
     lvs.ring_level = lvs.n - 1;
     for (int l = 0; l < lvs.n; ++l)
         if (2.0f * tgt->lv[l].cell >= max_corr_dist) {

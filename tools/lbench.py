@@ -11,6 +11,16 @@ import paper_2308_07173_b200 as g
 
 sc, mp, T, T0 = gen.config_c3()
 md = torch.from_numpy(np.array(mp)).cuda()
+if os.environ.get("LB_SORT"):  # Morton-sort the source as gicp_align does
+    c = np.floor(sc / 0.5).astype(np.int64) + (1 << 20)
+    def spread(v):
+        v = v & 0x1fffff
+        r = np.zeros_like(v)
+        for b in range(21):
+            r |= ((v >> b) & 1) << (3 * b)
+        return r
+    key = spread(c[:, 0]) | (spread(c[:, 1]) << 1) | (spread(c[:, 2]) << 2)
+    sc = np.ascontiguousarray(sc[np.argsort(key, kind="stable")])
 sd = torch.from_numpy(np.array(sc)).cuda()
 im = g.build_index(md, 0.5)
 cm = torch.from_numpy(gen.random_covariances(len(mp), 2)).cuda()
