@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -164,7 +166,7 @@ GICP_API void gicp_index_free(gicp_index idx) {
     cudaFreeAsync(idx->pts_orig, s);
     cudaFreeAsync(idx->hash_mem, s);
     if (idx->cov_sorted) cudaFreeAsync(idx->cov_sorted, s);
-    if (idx->adj_off) cudaFreeAsync(idx->adj_off, s);
+    if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
     if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
     if (idx->adj_code) cudaFreeAsync(idx->adj_code, s);
     cudaGetLastError();
@@ -298,6 +300,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
             return rc;
         return check_cuda(cudaStreamSynchronize(s), "align sync");
     };
+    const bool debug = getenv("GICP_DEBUG_ALIGN") != nullptr;
     double T[16];
     std::memcpy(T, T0, sizeof(T));
     double lambda = -1.0, nu = 2.0, err = 0.0;
@@ -373,6 +376,9 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         }
         const double mw = std::fmax(std::fabs(delta[0]), std::fmax(std::fabs(delta[1]), std::fabs(delta[2])));
         const double mv = std::fmax(std::fabs(delta[3]), std::fmax(std::fabs(delta[4]), std::fabs(delta[5])));
+        if (debug)
+            fprintf(stderr, "[gicp align] it=%d e=%.6f n=%lld lambda=%.3e |dw|=%.3e |dv|=%.3e\n", it, err,
+                    (long long)inl, lambda, mw, mv);
         if (mw < prm->rot_eps && mv < prm->trans_eps) {
             converged = 1;
             break;

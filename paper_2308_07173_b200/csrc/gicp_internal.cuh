@@ -149,10 +149,9 @@ struct gicp_index_s {
     float4* pts = nullptr;
     float4* pts_orig = nullptr;
     gicp::HashEntry* hash_mem = nullptr;  // all levels' tables, one allocation
-    int* adj_off = nullptr;               // [n+1] level-0 adjacency offsets (nonzero span at voxel heads)
-    int2* adj_rng = nullptr;              // [adj_total] neighbour voxel ranges, nearest-first per voxel
-    unsigned char* adj_code = nullptr;    // [adj_total] offset code (dx+1)*9 + (dy+1)*3 + (dz+1)
-    int64_t adj_total = 0;
+    int2* adj_oc = nullptr;               // [n] (offset, count) of the level-0 adjacency list, at voxel heads
+    int2* adj_rng = nullptr;              // neighbour voxel ranges, nearest-first per voxel
+    unsigned char* adj_code = nullptr;    // offset codes (dx+1)*9 + (dy+1)*3 + (dz+1)
     float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
     const float* cov_attached = nullptr;  // the caller's original-order array they were copied from
     int device = 0;

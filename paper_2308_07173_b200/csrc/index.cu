@@ -146,34 +146,49 @@ __device__ __constant__ signed char c_adj_order[27][3] = {
     {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
     {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
 
-template <bool FILL>
-__global__ void k_adjacency(const unsigned long long* __restrict__ keys, const float* __restrict__ xyz,
-                            const int* __restrict__ perm, int64_t n, Grid g, int* __restrict__ off,
+__device__ __forceinline__ unsigned compact3(unsigned long long v) {
+    v &= 0x1249249249249249ull;
+    v = (v ^ (v >> 2)) & 0x10c30c30c30c30c3ull;
+    v = (v ^ (v >> 4)) & 0x100f00f00f00f00full;
+    v = (v ^ (v >> 8)) & 0x1f0000ff0000ffull;
+    v = (v ^ (v >> 16)) & 0x1f00000000ffffull;
+    v = (v ^ (v >> 32)) & 0x1fffffull;
+    return (unsigned)v;
+}
+
+// one warp per level-0 hash slot: lane c < 27 probes neighbour c of the slot's
+// voxel (27 independent probes in flight per warp); the non-empty ones are
+// compacted in nearest-first order with a ballot and appended at an atomically
+// reserved offset (the list ORDER in memory is scheduling-dependent, the list of
+// every voxel is not); (offset, count) is stored at the voxel's first point.
+__global__ void k_adjacency(Grid g, int64_t cap, int* __restrict__ total, int2* __restrict__ oc,
                             int2* __restrict__ rng_out, unsigned char* __restrict__ code_out) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const bool head = (i == 0 || keys[i - 1] != keys[i]);
-    if (!head) {
-        if (!FILL) off[i] = 0;
-        return;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= cap) return;
+    const HashEntry e = g.hash[w];
+    if (e.key == kEmptyKey) return;  // warp-uniform
+    const int cx = (int)compact3(e.key), cy = (int)compact3(e.key >> 1), cz = (int)compact3(e.key >> 2);
+    int2 r = make_int2(0, 0);
+    int dx = 0, dy = 0, dz = 0;
+    if (lane < 27) {
+        dx = c_adj_order[lane][0];
+        dy = c_adj_order[lane][1];
+        dz = c_adj_order[lane][2];
+        r = cell_lookup(g, cx + dx, cy + dy, cz + dz);
     }
-    const int64_t j = perm[i];
-    const int cx = cell_coord(xyz[3 * j], g.ox, g.inv_cell), cy = cell_coord(xyz[3 * j + 1], g.oy, g.inv_cell),
-              cz = cell_coord(xyz[3 * j + 2], g.oz, g.inv_cell);
-    int cnt = 0;
-    int o = FILL ? off[i] : 0;
-    for (int c = 0; c < 27; ++c) {
-        const int dx = c_adj_order[c][0], dy = c_adj_order[c][1], dz = c_adj_order[c][2];
-        const int2 r = cell_lookup(g, cx + dx, cy + dy, cz + dz);
-        if (r.y <= r.x) continue;
-        if (FILL) {
-            rng_out[o] = r;
-            code_out[o] = (unsigned char)((dx + 1) * 9 + (dy + 1) * 3 + (dz + 1));
-            ++o;
-        }
-        ++cnt;
+    const bool ne = lane < 27 && r.y > r.x;
+    const unsigned mask = __ballot_sync(0xffffffffu, ne);
+    const int cnt = __popc(mask);
+    int base = 0;
+    if (lane == 0) base = atomicAdd(total, cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ne) {
+        const int o = base + __popc(mask & ((1u << lane) - 1));
+        rng_out[o] = r;
+        code_out[o] = (unsigned char)((dx + 1) * 9 + (dy + 1) * 3 + (dz + 1));
     }
-    if (!FILL) off[i] = cnt;
+    if (lane == 0) oc[e.start] = make_int2(base, cnt);
 }
 
 __global__ void k_fill_hash(HashEntry* H, int64_t cap) {
@@ -358,7 +373,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if (idx->pts) cudaFreeAsync(idx->pts, s);
         if (idx->pts_orig) cudaFreeAsync(idx->pts_orig, s);
         if (idx->hash_mem) cudaFreeAsync(idx->hash_mem, s);
-        if (idx->adj_off) cudaFreeAsync(idx->adj_off, s);
+        if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
         if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
         if (idx->adj_code) cudaFreeAsync(idx->adj_code, s);
         delete idx;
@@ -382,36 +397,22 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
     {
-        // level-0 adjacency: count, exclusive scan, fill
-        if (cudaMallocAsync(&idx->adj_off, (n + 1) * sizeof(int), s) != cudaSuccess) {
+        // level-0 adjacency lists, one pass (upper bound 27 entries per voxel)
+        const int64_t ub = 27 * std::max<int64_t>(counts[0], 1);
+        if (cudaMallocAsync(&idx->adj_oc, n * sizeof(int2), s) != cudaSuccess ||
+            cudaMallocAsync(&idx->adj_rng, ub * sizeof(int2), s) != cudaSuccess ||
+            cudaMallocAsync(&idx->adj_code, ub, s) != cudaSuccess) {
             cudaGetLastError();
             return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
         }
-        k_adjacency<false><<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, xyz, (int*)perm.p, n,
-                                                             idx->lv[0], idx->adj_off, nullptr, nullptr);
-        DevBuf cnt1, tmp;
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, idx->adj_off, idx->adj_off, (int)(n + 1), s);
-        if ((rc = alloc_async(tmp, tb, s))) return fail(rc);
-        if ((rc = check_cuda(cudaMemsetAsync(idx->adj_off + n, 0, sizeof(int), s), "memset"))) return fail(rc);
-        if ((rc = check_cuda(cub::DeviceScan::ExclusiveSum(tmp.p, tb, idx->adj_off, idx->adj_off, (int)(n + 1), s),
-                             "adjacency scan")))
-            return fail(rc);
-        int total = 0;
-        if ((rc = check_cuda(cudaMemcpyAsync(&total, idx->adj_off + n, sizeof(int), cudaMemcpyDeviceToHost, s),
-                             "D2H")))
-            return fail(rc);
-        if ((rc = check_cuda(cudaStreamSynchronize(s), "adjacency"))) return fail(rc);
-        idx->adj_total = total;
-        if (cudaMallocAsync(&idx->adj_rng, (size_t)std::max(total, 1) * sizeof(int2), s) != cudaSuccess ||
-            cudaMallocAsync(&idx->adj_code, (size_t)std::max(total, 1), s) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
-        }
-        k_adjacency<true><<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, xyz, (int*)perm.p, n,
-                                                            idx->lv[0], idx->adj_off, idx->adj_rng, idx->adj_code);
-        idx->device_bytes += (n + 1) * 4 + (int64_t)total * 9;
-        if ((rc = check_cuda(cudaGetLastError(), "adjacency kernels"))) return fail(rc);
+        DevBuf tot;
+        if ((rc = alloc_async(tot, 16, s))) return fail(rc);
+        if ((rc = check_cuda(cudaMemsetAsync(tot.p, 0, 16, s), "memset"))) return fail(rc);
+        const int64_t threads = idx->hash_cap[0] * 32;
+        k_adjacency<<<grid_for(threads, 256), 256, 0, s>>>(idx->lv[0], idx->hash_cap[0], (int*)tot.p, idx->adj_oc,
+                                                            idx->adj_rng, idx->adj_code);
+        idx->device_bytes += n * 8 + ub * 9;
+        if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);
     }
     if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
     *out = idx;

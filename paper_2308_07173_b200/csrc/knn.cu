@@ -199,7 +199,7 @@ struct FastShape {
 
 // level-0 voxel adjacency lists of the index (index.cu)
 struct AdjView {
-    const int* off;
+    const int2* oc;
     const int2* rng;
     const unsigned char* code;
 };
@@ -218,12 +218,13 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     int nr = 0;
     int a0 = 0, a1 = 0;
     bool use_adj = false;
-    if (active && g.level == 0 && adj.off != nullptr) {
+    if (active && g.level == 0 && adj.oc != nullptr) {
         const int2 own = cell_lookup(g, G.cx, G.cy, G.cz);
         if (own.y > own.x) {
             use_adj = true;
-            a0 = __ldg(adj.off + own.x);
-            a1 = __ldg(adj.off + own.x + 1);
+            const int2 oc = __ldg(adj.oc + own.x);
+            a0 = oc.x;
+            a1 = oc.x + oc.y;
         }
     }
     if (active && !use_adj) {
@@ -798,7 +799,7 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     Levels lvs;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
     // level 0 over every query, then one launch that climbs the pyramid for the rest
-    const AdjView adj{idx->adj_off, idx->adj_rng, idx->adj_code};
+    const AdjView adj{idx->adj_oc, idx->adj_rng, idx->adj_code};
     k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
                                                          cov, counts + 2, listA, counts + 0, exact, L == 1);
     if (L > 1)

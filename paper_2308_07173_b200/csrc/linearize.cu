@@ -37,7 +37,7 @@ struct Levels {
     Grid lv[kMaxLevels];
     int n;
     int ring_level;  // finest level with cell >= r/2: rings there reach the gate in <= 3 steps
-    const int* adj_off;  // level-0 voxel adjacency lists (index.cu)
+    const int2* adj_oc;  // level-0 voxel adjacency lists (index.cu)
     const int2* adj_rng;
     const unsigned char* adj_code;
 };
@@ -80,12 +80,13 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         int nr = 0;
         int a0 = 0, a1 = 0;
         bool use_adj = false;
-        if (active && lvs.adj_off != nullptr) {
+        if (active && lvs.adj_oc != nullptr) {
             const int2 own = cell_lookup(g, G.cx, G.cy, G.cz);
             if (own.y > own.x) {
                 use_adj = true;
-                a0 = __ldg(lvs.adj_off + own.x);
-                a1 = __ldg(lvs.adj_off + own.x + 1);
+                const int2 oc = __ldg(lvs.adj_oc + own.x);
+                a0 = oc.x;
+                a1 = oc.x + oc.y;
             }
         }
         const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
@@ -484,7 +485,7 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
-    lvs.adj_off = tgt->adj_off;
+    lvs.adj_oc = tgt->adj_oc;
     lvs.adj_rng = tgt->adj_rng;
     lvs.adj_code = tgt->adj_code;
     lvs.ring_level = lvs.n - 1;

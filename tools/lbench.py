@@ -25,6 +25,19 @@ sd = torch.from_numpy(np.array(sc)).cuda()
 im = g.build_index(md, 0.5)
 cm = torch.from_numpy(gen.random_covariances(len(mp), 2)).cuda()
 cs = torch.from_numpy(gen.random_covariances(len(sc), 1)).cuda()
+if os.environ.get("LB_REALCOV"):
+    _, _, cm = g.knn_cov_self(im, 20, 1e-3)
+    isc = g.build_index(sd, 0.0)
+    _, _, cs = g.knn_cov_self(isc, 20, 1e-3)
+if os.environ.get("LB_ALIGN"):
+    for it in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        Tr, info = g.align(sd, cs, im, cm, T0)
+        b.record()
+        torch.cuda.synchronize()
+        print(f"align: {a.elapsed_time(b):.2f} ms, {info.iterations} it, converged {info.converged}, "
+              f"|dt| {np.linalg.norm(Tr[:3, 3] - T[:3, 3]):.4f}")
 out = torch.empty(29, dtype=torch.float64, device="cuda")
 if os.environ.get("LB_ATTACH"):
     g.attach_cov(im, cm)
