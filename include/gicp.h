@@ -146,7 +146,9 @@ int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, float* d2,
  *   p'  = R p + t in fp64 (a-th row: fma(R_a2, p_z, fma(R_a1, p_y, fma(R_a0, p_x, t_a))))
  *   s   = fl32(p');  j* = argmin_j (d2(s, q_j), j) over ALL targets (d2 as gicp_knn)
  *   inlier iff d2 < fl32(r*r);   d = q_j* - p';  M = (C^q_j* + R C^p_i R^T)^-1
- *   J = [skew(p') | -I3] (left perturbation T <- Exp(delta) T, delta = (omega, v))
+ *   J = [skew(p' - c) | -I3] for the perturbation T <- Tr(c) Exp(delta) Tr(-c) T,
+ *   delta = (omega, v): a rotation about the pivot c, then a translation
+ *   (reading R13; c = 0 is the plain left perturbation)
  *   out29 = sum over inliers of J^T M J (21 upper-triangle entries, row-major),
  *           J^T M d (6), d^T M d (1), inlier count (1)  -- fp64, deterministic
  *           fixed-order reduction (bitwise reproducible run to run).
@@ -154,6 +156,9 @@ int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, float* d2,
  *   tgt           index built on the target cloud; tgt_cov [nt][6] fp32 in the
  *                 target's ORIGINAL order (device).
  *   T (host)      4x4 row-major fp64 (rigid).
+ *   pivot (host)  fp64 [3] rotation pivot c in the target frame, or NULL for the
+ *                 origin; gicp_align uses the source origin mapped by T (the
+ *                 sensor), which keeps lever arms short in map coordinates.
  *   max_corr_dist gate r in metres (> 0).
  *   flags         GICP_LIN_REUSE_CORR: skip the search and use corr[] as given
  *                 (entries < 0 are outliers); GICP_LIN_ERROR_ONLY: only e and the
@@ -165,14 +170,15 @@ int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, float* d2,
 enum { GICP_LIN_REUSE_CORR = 1, GICP_LIN_ERROR_ONLY = 2 };
 
 int gicp_linearize(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, const float* tgt_cov,
-                   const double T[16] /* host */, float max_corr_dist, int flags, double* out29, int32_t* corr,
-                   void* stream);
+                   const double T[16] /* host */, const double* pivot /* host, nullable */, float max_corr_dist,
+                   int flags, double* out29, int32_t* corr, void* stream);
 
 /* ---------------------------------------------------------------------------
  * gicp_align -- host Levenberg-Marquardt over gicp_linearize (T = argmin ...,
  * PAPER.md l.396-402; the optimiser is DESIGN.md reading R13):
- *   per iteration: linearize at T (search), lambda init 1e-9 max diag(H), up to
- *   10 inner trials solving (H + lambda I) delta = -b (LDL^T), T' = Exp(delta) T,
+ *   per iteration: pivot c = T's translation, linearize at T (search), lambda
+ *   init 1e-9 max diag(H), up to 10 inner trials solving (H + lambda I) delta = -b
+ *   (LDL^T), T' = Tr(c) Exp(delta) Tr(-c) T,
  *   e' = linearize(T', REUSE_CORR, ERROR_ONLY), gain rho = (e - e')/(delta^T
  *   (lambda delta - b)); accept iff rho > 0 (lambda *= max(1/3, 1 - (2 rho - 1)^3))
  *   else lambda *= nu, nu *= 2; converged when the ACCEPTED step has

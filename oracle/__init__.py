@@ -57,7 +57,9 @@ def lib():
         L.oracle_d2.restype = f32
         L.oracle_jacobi3.argtypes = [P, P, P]
         L.oracle_covariance.argtypes = [P, i64, P, i64, i32, f64, P, P, P, i32]
-        L.oracle_linearize.argtypes = [P, P, i64, P, P, i64, P, f32, i32, P, P, P, i32]
+        L.oracle_linearize.argtypes = [P, P, i64, P, P, i64, P, P, f32, i32, P, P, P, i32]
+        L.oracle_pivoted_exp.argtypes = [P, P, P]
+        L.oracle_pivoted_exp.restype = None
         L.oracle_se3_exp.argtypes = [P, P]
         L.oracle_se3_exp.restype = None
         L.oracle_ldlt_solve6.argtypes = [P, P, P]
@@ -121,8 +123,9 @@ def covariance(xyz, nbr, eps=1e-3, nthreads=0):
     return cov, gap, S6
 
 
-def linearize(src, src_cov, tgt, tgt_cov, T, max_corr_dist=1.0, corr=None, nthreads=0):
-    """O3: (out29, absum29, corr). With corr given: REUSE_CORR (no search)."""
+def linearize(src, src_cov, tgt, tgt_cov, T, max_corr_dist=1.0, corr=None, nthreads=0, pivot=None):
+    """O3: (out29, absum29, corr). With corr given: REUSE_CORR (no search).
+    pivot: the point the rotation of the perturbation is about (default origin)."""
     src, tgt = _f32(src), _f32(tgt)
     src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
     T = np.ascontiguousarray(T, dtype=np.float64)
@@ -134,8 +137,10 @@ def linearize(src, src_cov, tgt, tgt_cov, T, max_corr_dist=1.0, corr=None, nthre
         flags = LIN_REUSE_CORR
     else:
         corr = np.empty(src.shape[0], np.int32)
+    piv = None if pivot is None else np.ascontiguousarray(pivot, dtype=np.float64)
     rc = lib().oracle_linearize(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
-                                _ptr(T), max_corr_dist, flags, _ptr(out), _ptr(ab), _ptr(corr), nthreads)
+                                _ptr(T), None if piv is None else _ptr(piv), max_corr_dist, flags, _ptr(out),
+                                _ptr(ab), _ptr(corr), nthreads)
     if rc != OK:
         raise OracleError(rc, "oracle_linearize")
     return out, ab, corr
@@ -145,6 +150,14 @@ def se3_exp(delta):
     delta = np.ascontiguousarray(delta, dtype=np.float64)
     T = np.empty((4, 4))
     lib().oracle_se3_exp(_ptr(delta), _ptr(T))
+    return T
+
+
+def pivoted_exp(delta, pivot):
+    delta = np.ascontiguousarray(delta, dtype=np.float64)
+    c = np.ascontiguousarray(pivot, dtype=np.float64)
+    T = np.empty((4, 4))
+    lib().oracle_pivoted_exp(_ptr(delta), _ptr(c), _ptr(T))
     return T
 
 

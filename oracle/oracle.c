@@ -341,10 +341,14 @@ static inline void nm_add(neumaier* a, double x) {
 }
 
 /* per-point term of one inlier: H (21 upper, row-major), b (6), e.
- * J = [skew(p') | -I3]; H = J^T M J; b = J^T M d; e = d^T M d. */
-static void point_terms(const double pp[3], const double d[3], const double M[9], double out[28]) {
+ * J = [skew(p' - c) | -I3] for the pivoted left perturbation
+ * T <- Tr(c) Exp(delta) Tr(-c) T (reading R13); H = J^T M J;
+ * b = J^T M d; e = d^T M d. */
+static void point_terms(const double pp_in[3], const double c[3], const double d[3], const double M[9],
+                        double out[28]) {
+    const double pp[3] = {pp_in[0] - c[0], pp_in[1] - c[1], pp_in[2] - c[2]};
     double J[3][6];
-    /* skew(p') = [[0,-z,y],[z,0,-x],[-y,x,0]] */
+    /* skew(p' - c) = [[0,-z,y],[z,0,-x],[-y,x,0]] */
     J[0][0] = 0.0;
     J[0][1] = -pp[2];
     J[0][2] = pp[1];
@@ -403,8 +407,9 @@ static int64_t nn_sw(const float* tgt, int64_t nt, const float s[3], float* best
  * sum of |term| per component (the tolerance scale). corr (nullable unless
  * REUSE_CORR) = j* or -1. */
 int oracle_linearize(const float* src, const float* src_cov, int64_t ns, const float* tgt, const float* tgt_cov,
-                     int64_t nt, const double T[16], float max_corr_dist, int flags, double* out29,
-                     double* absum29, int32_t* corr, int nthreads) {
+                     int64_t nt, const double T[16], const double* pivot, float max_corr_dist, int flags,
+                     double* out29, double* absum29, int32_t* corr, int nthreads) {
+    const double c0[3] = {pivot ? pivot[0] : 0.0, pivot ? pivot[1] : 0.0, pivot ? pivot[2] : 0.0};
     if (!src || !src_cov || !tgt || !tgt_cov || !T || !out29 || ns < 0 || nt <= 0) return ORACLE_EINVAL;
     if ((flags & LIN_REUSE_CORR) && !corr) return ORACLE_EINVAL;
     if (!(max_corr_dist > 0.0f)) return ORACLE_EINVAL;
@@ -476,7 +481,7 @@ int oracle_linearize(const float* src, const float* src_cov, int64_t ns, const f
             continue;
         }
         double term[28];
-        point_terms(pp, d, M, term);
+        point_terms(pp, c0, d, M, term);
         for (int c = 0; c < 28; ++c) {
             nm_add(&acc[c], term[c]);
             ab[c] += fabs(term[c]);
@@ -546,6 +551,18 @@ static void mat4_mul(const double A[16], const double B[16], double C[16]) {
         }
     memcpy(C, t, sizeof(t));
 }
+
+/* Tr(c) Exp(delta) Tr(-c): rotation about the pivot c (reading R13) */
+void oracle_pivoted_exp(const double delta[6], const double c[3], double T[16]) {
+    double E[16];
+    oracle_se3_exp(delta, E);
+    memcpy(T, E, sizeof(E));
+    for (int a = 0; a < 3; ++a) {
+        double rc = E[4 * a + 0] * c[0] + E[4 * a + 1] * c[1] + E[4 * a + 2] * c[2];
+        T[4 * a + 3] = E[4 * a + 3] + c[a] - rc;
+    }
+}
+#define pivoted_exp oracle_pivoted_exp
 
 /* solve (A) x = y for 6x6 SPD A by LDL^T (no pivoting). returns -1 if not PD */
 int oracle_ldlt_solve6(const double A[36], const double y[6], double x[6]) {
@@ -619,7 +636,9 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
     int64_t inl = 0;
     for (it = 1; it <= prm->max_iter; ++it) {
         double o29[29];
-        rc = oracle_linearize(src, src_cov, ns, tgt, tgt_cov, nt, T, prm->max_corr_dist, 0, o29, NULL, corr,
+        /* pivot: the source frame origin in the target frame (the sensor) */
+        const double piv[3] = {T[3], T[7], T[11]};
+        rc = oracle_linearize(src, src_cov, ns, tgt, tgt_cov, nt, T, piv, prm->max_corr_dist, 0, o29, NULL, corr,
                               nthreads);
         if (rc != ORACLE_OK) break;
         inl = (int64_t)o29[28];
@@ -639,7 +658,7 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
                 break;
             }
             double dT[16];
-            oracle_se3_exp(delta, dT);
+            pivoted_exp(delta, piv, dT);
             mat4_mul(dT, T, T);
         } else {
             if (lambda < 0) {
@@ -662,11 +681,11 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
                     continue;
                 }
                 double dT[16], Tn[16];
-                oracle_se3_exp(delta, dT);
+                pivoted_exp(delta, piv, dT);
                 mat4_mul(dT, T, Tn);
                 double o2[29];
-                rc = oracle_linearize(src, src_cov, ns, tgt, tgt_cov, nt, Tn, prm->max_corr_dist, LIN_REUSE_CORR,
-                                      o2, NULL, corr, nthreads);
+                rc = oracle_linearize(src, src_cov, ns, tgt, tgt_cov, nt, Tn, piv, prm->max_corr_dist,
+                                      LIN_REUSE_CORR, o2, NULL, corr, nthreads);
                 if (rc != ORACLE_OK) break;
                 double en = o2[27];
                 double den = 0.0;

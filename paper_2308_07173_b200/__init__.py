@@ -61,7 +61,7 @@ _lib.gicp_knn.argtypes = [_P, _P, _i64, _i32, _P, _P, _P]
 _lib.gicp_knn_self.argtypes = [_P, _i32, _P, _P, _P]
 _lib.gicp_covariances.argtypes = [_P, _i64, _P, _i64, _i32, _f32, _P, _P]
 _lib.gicp_knn_cov_self.argtypes = [_P, _i32, _f32, _P, _P, _P, _P]
-_lib.gicp_linearize.argtypes = [_P, _P, _i64, _P, _P, _P, _f32, _i32, _P, _P, _P]
+_lib.gicp_linearize.argtypes = [_P, _P, _i64, _P, _P, _P, _P, _f32, _i32, _P, _P, _P]
 _lib.gicp_align.argtypes = [_P, _P, _i64, _P, _P, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
                             _P]
 
@@ -194,8 +194,10 @@ def _T(T) -> np.ndarray:
 
 
 def linearize(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, tgt_cov: torch.Tensor, T, max_corr_dist=1.0,
-              corr: torch.Tensor | None = None, reuse_corr: bool = False, error_only: bool = False, out=None):
-    """Returns (out29 float64 device tensor [29], corr int32 device tensor [ns])."""
+              corr: torch.Tensor | None = None, reuse_corr: bool = False, error_only: bool = False, out=None,
+              pivot=None):
+    """Returns (out29 float64 device tensor [29], corr int32 device tensor [ns]).
+    pivot: rotation pivot (3,) of the perturbation, default the origin."""
     src = _pts(src, "src")
     ns = src.shape[0]
     Th = _T(T)
@@ -205,9 +207,10 @@ def linearize(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, tgt_cov: tor
             raise ValueError("reuse_corr needs corr")
         corr = torch.empty(ns, dtype=torch.int32, device=src.device)
     flags = (LIN_REUSE_CORR if reuse_corr else 0) | (LIN_ERROR_ONLY if error_only else 0)
+    piv = None if pivot is None else np.ascontiguousarray(np.asarray(pivot, dtype=np.float64).reshape(3))
     _check(_lib.gicp_linearize(_dptr(src), _dptr(src_cov.contiguous()), ns, tgt.handle, _dptr(tgt_cov.contiguous()),
-                               Th.ctypes.data_as(_P), float(max_corr_dist), flags, _dptr(out29), _dptr(corr),
-                               _stream()))
+                               Th.ctypes.data_as(_P), None if piv is None else piv.ctypes.data_as(_P),
+                               float(max_corr_dist), flags, _dptr(out29), _dptr(corr), _stream()))
     return out29, corr
 
 

@@ -85,6 +85,12 @@ void se3_exp(const double d[6], double E[16]) {
     E[15] = 1.0;
 }
 
+// Tr(c) Exp(delta) Tr(-c): the perturbation rotates about the pivot c
+void pivoted_exp(const double d[6], const double c[3], double E[16]) {
+    se3_exp(d, E);
+    for (int a = 0; a < 3; ++a) E[4 * a + 3] += c[a] - (E[4 * a] * c[0] + E[4 * a + 1] * c[1] + E[4 * a + 2] * c[2]);
+}
+
 void mul44(const double A[16], const double B[16], double C[16]) {
     double t[16];
     for (int a = 0; a < 4; ++a)
@@ -241,8 +247,8 @@ GICP_API int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, f
 }
 
 GICP_API int gicp_linearize(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, const float* tgt_cov,
-                            const double T[16], float max_corr_dist, int flags, double* out29, int32_t* corr,
-                            void* stream) {
+                            const double T[16], const double* pivot, float max_corr_dist, int flags, double* out29,
+                            int32_t* corr, void* stream) {
     if (!tgt || !tgt_cov || !T || !out29) return set_error(GICP_EINVAL, "gicp_linearize: null pointer");
     if (ns < 0 || ns >= (1ll << 31) - 1) return set_error(GICP_EINVAL, "gicp_linearize: ns out of range");
     if (ns > 0 && (!src || !src_cov)) return set_error(GICP_EINVAL, "gicp_linearize: null source");
@@ -253,7 +259,9 @@ GICP_API int gicp_linearize(const float* src, const float* src_cov, int64_t ns, 
     if (flags & ~(GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY)) return set_error(GICP_EINVAL, "gicp_linearize: flags");
     if (!finite_T(T)) return set_error(GICP_EINVAL, "gicp_linearize: non-finite T");
     init_pool_once();
-    return launch_linearize(src, src_cov, ns, tgt, tgt_cov, T, max_corr_dist, flags, out29, corr,
+    if (pivot && !(std::isfinite(pivot[0]) && std::isfinite(pivot[1]) && std::isfinite(pivot[2])))
+        return set_error(GICP_EINVAL, "gicp_linearize: non-finite pivot");
+    return launch_linearize(src, src_cov, ns, tgt, tgt_cov, T, pivot, max_corr_dist, flags, out29, corr,
                             (cudaStream_t)stream);
 }
 
@@ -292,9 +300,10 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         cudaFreeAsync(scratch, s);
         return rc0;
     }
+    double piv[3] = {0.0, 0.0, 0.0};
     auto lin = [&](const double* T, int flags) -> int {
-        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, prm->max_corr_dist, flags | kLinCorrSpos, d_out,
-                                  d_corr, s, &ls);
+        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, flags | kLinCorrSpos,
+                                  d_out, d_corr, s, &ls);
         if (rc) return rc;
         if ((rc = check_cuda(cudaMemcpyAsync(h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
             return rc;
@@ -307,6 +316,10 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     int converged = 0, it = 0, rc = GICP_OK;
     int64_t inl = 0;
     for (it = 1; it <= prm->max_iter; ++it) {
+        // pivot: the source frame origin in the target frame (the sensor position)
+        piv[0] = T[3];
+        piv[1] = T[7];
+        piv[2] = T[11];
         if ((rc = lin(T, 0))) break;
         inl = (int64_t)h[28];
         if (inl < 6) {
@@ -327,7 +340,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 break;
             }
             double E[16];
-            se3_exp(delta, E);
+            pivoted_exp(delta, piv, E);
             mul44(E, T, T);
         } else {
             if (lambda < 0) {
@@ -349,7 +362,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                     continue;
                 }
                 double E[16], Tn[16];
-                se3_exp(delta, E);
+                pivoted_exp(delta, piv, E);
                 mul44(E, T, Tn);
                 if ((rc = lin(Tn, GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY))) break;
                 const double en = h[27];

@@ -29,6 +29,7 @@ constexpr int kMaxRing = 16;
 struct Pose {
     double R[9];
     double t[3];
+    double c[3];  // pivot of the rotational perturbation (reading R13)
     float Rf[9];
 };
 
@@ -294,7 +295,8 @@ __device__ __forceinline__ void accumulate_point(const Pose& P, const double pp[
     const float mdz = M02 * dx + M12 * dy + M22 * dz;
     acc[27] += (double)(dx * mdx + dy * mdy + dz * mdz);
     if (ERROR_ONLY) return;
-    const float px = (float)pp[0], py = (float)pp[1], pz = (float)pp[2];
+    // lever arm about the pivot (fp64 difference, then fp32)
+    const float px = (float)(pp[0] - P.c[0]), py = (float)(pp[1] - P.c[1]), pz = (float)(pp[2] - P.c[2]);
     // P = skew(p') = [[0,-z,y],[z,0,-x],[-y,x,0]];  MP = M P
     const float MP00 = M01 * pz - M02 * py, MP01 = -M00 * pz + M02 * px, MP02 = M00 * py - M01 * px;
     const float MP10 = M11 * pz - M12 * py, MP11 = -M01 * pz + M12 * px, MP12 = M01 * py - M11 * px;
@@ -465,8 +467,8 @@ __global__ void k_zero29(double* out29) {
 }  // namespace
 
 int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
-                     const float* tgt_cov, const double T[16], float max_corr_dist, int flags, double* out29,
-                     int32_t* corr, cudaStream_t s, const LinScratch* pre) {
+                     const float* tgt_cov, const double T[16], const double* pivot, float max_corr_dist, int flags,
+                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre) {
     if (ns == 0) {
         k_zero29<<<1, 32, 0, s>>>(out29);
         return check_cuda(cudaGetLastError(), "linearize launch");
@@ -478,6 +480,7 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
             P.Rf[3 * a + b] = (float)T[4 * a + b];
         }
         P.t[a] = T[4 * a + 3];
+        P.c[a] = pivot ? pivot[a] : 0.0;
     }
     volatile float r2v = max_corr_dist * max_corr_dist;  // fp32 product
     const float r2 = r2v;

@@ -201,6 +201,11 @@ def test_linearize_c1(orc, variant):
         o29, ab, ocorr = orc.linearize(src, cs, tgt, ct, T, 1.0)
         assert np.array_equal(H(corr), ocorr)
         assert_lin_parity(H(out), o29, ab)
+        # with a rotation pivot (gicp_align's parametrisation)
+        c = T[:3, 3] + np.array([0.3, -0.2, 0.1])
+        outp, _ = g.linearize(D(src), D(cs), idx, D(ct), T, 1.0, pivot=c)
+        op29, abp, _ = orc.linearize(src, cs, tgt, ct, T, 1.0, pivot=c)
+        assert_lin_parity(H(outp), op29, abp)
         # REUSE_CORR and ERROR_ONLY paths
         out2, _ = g.linearize(D(src), D(cs), idx, D(ct), T, 1.0, corr=corr, reuse_corr=True, error_only=True)
         h2 = H(out2)
@@ -242,8 +247,8 @@ def test_linearize_c2_scan_to_scan(orc):
     cs, ct = _covs_oracle(orc, src, 20), _covs_oracle(orc, tgt, 20)
     idx = g.build_index(D(tgt), 0.0)
     for T in (T0, T_rel):
-        out, corr = g.linearize(D(src), D(cs), idx, D(ct), T, 1.0)
-        o29, ab, ocorr = orc.linearize(src, cs, tgt, ct, T, 1.0)
+        out, corr = g.linearize(D(src), D(cs), idx, D(ct), T, 1.0, pivot=T[:3, 3])
+        o29, ab, ocorr = orc.linearize(src, cs, tgt, ct, T, 1.0, pivot=T[:3, 3])
         assert np.array_equal(H(corr), ocorr)
         assert_lin_parity(H(out), o29, ab)
 
@@ -328,7 +333,7 @@ def test_c3_fullsize_sampled(orc):
     src = np.ascontiguousarray(sc[sub])
     cs = gen.random_covariances(len(src), 1)
     ct = gen.random_covariances(len(mp), 2)
-    out, corr = g.linearize(D(src), D(cs), idx, D(ct), T0, 1.0)
-    o29, ab, ocorr = orc.linearize(src, cs, mp, ct, T0, 1.0)
+    out, corr = g.linearize(D(src), D(cs), idx, D(ct), T0, 1.0, pivot=T0[:3, 3])
+    o29, ab, ocorr = orc.linearize(src, cs, mp, ct, T0, 1.0, pivot=T0[:3, 3])
     assert np.array_equal(H(corr), ocorr)
     assert_lin_parity(H(out), o29, ab)

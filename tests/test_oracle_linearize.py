@@ -199,3 +199,46 @@ def test_errors(orc):
     p = gen.uniform_cloud(10, 1)
     with pytest.raises(orc.OracleError):
         orc.linearize(p, _eye_cov(10), p, _eye_cov(10), np.eye(4), 0.0)
+
+
+def test_pivoted_exp_fixes_the_pivot(orc):
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        c = rng.normal(size=3) * 300
+        w = rng.normal(size=3) * 0.1
+        E = orc.pivoted_exp(np.concatenate([w, np.zeros(3)]), c)
+        assert np.allclose(E[:3, :3] @ c + E[:3, 3], c, atol=1e-9)       # rotation about c
+        v = rng.normal(size=3)
+        E2 = orc.pivoted_exp(np.concatenate([np.zeros(3), v]), c)
+        assert np.allclose(E2[:3, :3], np.eye(3)) and np.allclose(E2[:3, 3], v)
+
+
+def test_pivoted_jacobian_finite_differences(orc):
+    # with a pivot c, J = [skew(p' - c) | -I] for T <- Tr(c) Exp(delta) Tr(-c) T:
+    # b = 1/2 de/ddelta (isotropic source covariances) and H the GN quadratic form
+    tgt = (gen.corner_scene(11, 0.002) + np.array([480.0, -250.0, 3.0], np.float32)).astype(np.float32)
+    src = (gen.corner_scene(12, 0.002) + np.array([480.0, -250.0, 3.0], np.float32)).astype(np.float32)
+    nbr, _ = orc.knn(tgt, tgt, 10)
+    ct = orc.covariance(tgt, nbr)[0].astype(np.float32)
+    cs = _eye_cov(len(src)) * np.float32(0.01)
+    c = np.array([478.0, -251.0, 2.0])
+    T = gen.make_T(gen.euler_to_R(0.001, -0.002, 0.003), [0.05, -0.04, 0.02])
+    out, ab, corr = orc.linearize(src, cs, tgt, ct, T, 1.0, pivot=c)
+    b = out[21:27]
+    h = 1e-6
+    for a in range(6):
+        u = np.zeros(6)
+        u[a] = h
+        ep = orc.linearize(src, cs, tgt, ct, orc.pivoted_exp(u, c) @ T, 1.0, corr=corr, pivot=c)[0][27]
+        em = orc.linearize(src, cs, tgt, ct, orc.pivoted_exp(-u, c) @ T, 1.0, corr=corr, pivot=c)[0][27]
+        assert math.isclose((ep - em) / (2 * h), 2 * b[a], rel_tol=1e-5, abs_tol=1e-6 * ab[21 + a])
+    # exact copy at T = I: quadratic form of H
+    out, ab, corr = orc.linearize(tgt, ct, tgt, ct, np.eye(4), 1.0, pivot=c)
+    Hm = _H(out)
+    t = 1e-5
+    for a in range(6):
+        E = np.zeros(6)
+        E[a] = 1.0
+        ep = orc.linearize(tgt, ct, tgt, ct, orc.pivoted_exp(t * E, c), 1.0, corr=corr, pivot=c)[0][27]
+        em = orc.linearize(tgt, ct, tgt, ct, orc.pivoted_exp(-t * E, c), 1.0, corr=corr, pivot=c)[0][27]
+        assert math.isclose((ep + em) / (2 * t * t), Hm[a, a], rel_tol=1e-4)
