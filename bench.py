@@ -64,7 +64,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -74,7 +74,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -84,10 +84,13 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Samples received during [t0, t1] (host clock; the whole run if None)."""
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if t0 is not None and not (t0 <= ts <= t1):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -129,8 +132,8 @@ def reference_main(args, rank, world):
     cores = os.cpu_count() or 1
     n_q = args.ref_queries
     vals = []
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        run_oracle_sample(max(16, n_q // 8))
+    for _ in range(min(args.warmup, 1)):
+        run_oracle_sample(max(16, n_q // 16))
     for s in range(args.steps):
         v, dt = run_oracle_sample(n_q, seed=77 + s)
         vals.append(v)
@@ -158,11 +161,11 @@ def reference_main(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-queries", type=int, default=1000)
-    ap.add_argument("--cpu-queries", type=int, default=600, help="oracle sample for cpu_baseline")
+    ap.add_argument("--ref-queries", type=int, default=20000, help="oracle sample per reference step")
+    ap.add_argument("--cpu-queries", type=int, default=60000, help="oracle sample for cpu_baseline (~10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -214,14 +217,15 @@ def main():
         iscan.free()
         return T, info
 
-    # warm-up
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    rec = []
-    step_ms = []
+    # warm-up (the clock sampler starts first: nvidia-smi needs ~0.1-0.5 s to come up)
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        time.sleep(0.3)
+        rec = []
+        step_ms = []
+        t_start = time.time()
         for _ in range(args.steps):
             flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the timed region
             if world > 1:
@@ -234,7 +238,9 @@ def main():
             t1.record(stream)
             torch.cuda.synchronize()
             step_ms.append(t0.elapsed_time(t1))
-    clocks = clk.summary()
+        t_end = time.time()
+        time.sleep(0.15)
+    clocks = clk.summary(t_start, t_end + 0.1)
 
     ms = statistics.mean(step_ms)
     if world > 1:

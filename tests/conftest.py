@@ -13,6 +13,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running oracle check")
 
 
+def pytest_sessionstart(session):
+    # build the CUDA library (nvcc cross-compiles without a GPU) before any test
+    # imports the binding; load build.py by path (the package needs the .so)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gicp_build", os.path.join(ROOT, "paper_2308_07173_b200",
+                                                                             "build.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    m.build()
+
+
 @pytest.fixture(scope="session")
 def orc():
     import oracle

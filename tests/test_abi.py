@@ -18,9 +18,12 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2308_07173_b200 import build
-    path = build.build()
-    return path
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gicp_build", os.path.join(ROOT, "paper_2308_07173_b200",
+                                                                             "build.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m.build()
 
 
 def test_header_declares_the_north_star_calls():
