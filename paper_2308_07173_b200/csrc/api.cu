@@ -276,12 +276,12 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     cudaStream_t s = (cudaStream_t)stream;
     double* h = pinned29();
     if (!h) return set_error(GICP_ENOMEM, "gicp_align: pinned buffer");
-    // one scratch block for the whole alignment: out29 | done counter | block
-    // partials | correspondences | Morton-sorted copies of the source and its
-    // covariances
+    // one scratch block for the whole alignment: out (31 doubles) | done counter |
+    // block partials | two correspondence buffers | Morton-sorted copies of the
+    // source and its covariances
     const int64_t nsa = ns > 0 ? ns : 1;
     const size_t lin_bytes = linearize_scratch_bytes(nsa);
-    const size_t bytes = 512 + lin_bytes + nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256;
+    const size_t bytes = 512 + lin_bytes + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256;
     char* scratch = nullptr;
     if (cudaMallocAsync((void**)&scratch, bytes, s) != cudaSuccess) {
         cudaGetLastError();
@@ -291,8 +291,9 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     LinScratch ls;
     ls.done = (unsigned*)(scratch + 256);
     ls.partials = (double*)(scratch + 512);
-    int32_t* d_corr = (int32_t*)(scratch + 512 + lin_bytes);
-    float* src_p = (float*)(((uintptr_t)(d_corr + nsa) + 15) & ~(uintptr_t)15);
+    int32_t* corr_a = (int32_t*)(scratch + 512 + lin_bytes);
+    int32_t* corr_b = corr_a + nsa;
+    float* src_p = (float*)(((uintptr_t)(corr_b + nsa) + 15) & ~(uintptr_t)15);
     float* cov_p = src_p + 3 * nsa;
     int rc0 = check_cuda(cudaMemsetAsync(ls.done, 0, sizeof(unsigned), s), "memset");
     if (!rc0 && ns > 0) rc0 = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s);
@@ -300,12 +301,13 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         cudaFreeAsync(scratch, s);
         return rc0;
     }
-    double piv[3] = {0.0, 0.0, 0.0};
-    auto lin = [&](const double* T, int flags) -> int {
-        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, flags | kLinCorrSpos,
-                                  d_out, d_corr, s, &ls);
+    // one launch + one sync per evaluation: `old` != nullptr also evaluates the
+    // trial cost with the previous correspondences (values 29, 30)
+    auto lin = [&](const double* T, const double* piv, int32_t* corr, const int32_t* old) -> int {
+        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, kLinCorrSpos, d_out,
+                                  corr, s, &ls, old);
         if (rc) return rc;
-        if ((rc = check_cuda(cudaMemcpyAsync(h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
+        if ((rc = check_cuda(cudaMemcpyAsync(h, d_out, 31 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
             return rc;
         return check_cuda(cudaStreamSynchronize(s), "align sync");
     };
@@ -315,23 +317,23 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     double lambda = -1.0, nu = 2.0, err = 0.0;
     int converged = 0, it = 0, rc = GICP_OK;
     int64_t inl = 0;
-    for (it = 1; it <= prm->max_iter; ++it) {
-        // pivot: the source frame origin in the target frame (the sensor position)
-        piv[0] = T[3];
-        piv[1] = T[7];
-        piv[2] = T[11];
-        if ((rc = lin(T, 0))) break;
-        inl = (int64_t)h[28];
+    // pivot: the source frame origin in the target frame (the sensor position)
+    double piv[3] = {T[3], T[7], T[11]};
+    double lin29[29];  // the linearisation at the current T (about piv), corr in corr_a
+    if ((rc = lin(T, piv, corr_a, nullptr)) == GICP_OK) std::memcpy(lin29, h, sizeof(lin29));
+    for (it = 1; rc == GICP_OK && it <= prm->max_iter; ++it) {
+        inl = (int64_t)lin29[28];
         if (inl < 6) {
             rc = set_error(GICP_EDEGENERATE, "gicp_align: fewer than 6 correspondences");
             break;
         }
         double Hm[36], b[6], delta[6] = {0, 0, 0, 0, 0, 0};
         for (int a = 0, o = 0; a < 6; ++a)
-            for (int c = a; c < 6; ++c, ++o) Hm[6 * a + c] = Hm[6 * c + a] = h[o];
-        for (int a = 0; a < 6; ++a) b[a] = h[21 + a];
-        const double e = h[27];
+            for (int c = a; c < 6; ++c, ++o) Hm[6 * a + c] = Hm[6 * c + a] = lin29[o];
+        for (int a = 0; a < 6; ++a) b[a] = lin29[21 + a];
+        const double e = lin29[27];
         err = e;
+        bool done_now = false;
         if (!prm->lm) {
             double nb[6];
             for (int a = 0; a < 6; ++a) nb[a] = -b[a];
@@ -364,13 +366,19 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 double E[16], Tn[16];
                 pivoted_exp(delta, piv, E);
                 mul44(E, T, Tn);
-                if ((rc = lin(Tn, GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY))) break;
-                const double en = h[27];
+                // trial: e' with the current correspondences at Tn, and speculatively
+                // the full linearisation at Tn (needed next if the step is accepted)
+                const double pn[3] = {Tn[3], Tn[7], Tn[11]};
+                if ((rc = lin(Tn, pn, corr_b, corr_a))) break;
+                const double en = h[29];
                 double den = 0.0;
                 for (int a = 0; a < 6; ++a) den += delta[a] * (lambda * delta[a] - b[a]);
                 const double rho = (e - en) / den;
                 if (rho > 0) {
                     std::memcpy(T, Tn, sizeof(T));
+                    std::memcpy(piv, pn, sizeof(piv));
+                    std::memcpy(lin29, h, sizeof(lin29));
+                    std::swap(corr_a, corr_b);
                     const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);
                     lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
                     nu = 2.0;
@@ -386,6 +394,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 converged = 1;
                 break;
             }
+            done_now = true;  // lin29 already holds the linearisation at the new T
         }
         const double mw = std::fmax(std::fabs(delta[0]), std::fmax(std::fabs(delta[1]), std::fabs(delta[2])));
         const double mv = std::fmax(std::fabs(delta[3]), std::fmax(std::fabs(delta[4]), std::fabs(delta[5])));
@@ -395,6 +404,12 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         if (mw < prm->rot_eps && mv < prm->trans_eps) {
             converged = 1;
             break;
+        }
+        if (!done_now) {  // Gauss-Newton: linearise at the new T
+            piv[0] = T[3];
+            piv[1] = T[7];
+            piv[2] = T[11];
+            if ((rc = lin(T, piv, corr_a, nullptr)) == GICP_OK) std::memcpy(lin29, h, sizeof(lin29));
         }
     }
     cudaFreeAsync(scratch, s);

@@ -180,7 +180,8 @@ constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positi
 size_t linearize_scratch_bytes(int64_t ns);
 int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                      const float* tgt_cov, const double T[16], const double* pivot, float max_corr_dist, int flags,
-                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre = nullptr);
+                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre = nullptr,
+                     const int32_t* corr_old = nullptr);
 int attach_covariances(gicp_index_s* idx, const float* cov, cudaStream_t s);
 int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
                 cudaStream_t s);

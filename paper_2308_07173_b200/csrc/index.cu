@@ -82,48 +82,96 @@ __global__ void k_keys(const float* __restrict__ xyz, int64_t n, Grid g, unsigne
     vals[i] = (int)i;
 }
 
-// occupied voxels per level
+// occupied voxels per level (warp reduce -> block smem counters -> one global
+// atomic per level per block)
 __global__ void k_level_count(const unsigned long long* __restrict__ keys, int64_t n, int L, int* __restrict__ cnt) {
+    __shared__ int sc[kMaxLevels];
+    if (threadIdx.x < kMaxLevels) sc[threadIdx.x] = 0;
+    __syncthreads();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const unsigned long long k = i < n ? keys[i] : 0ull;
     const unsigned long long kp = (i > 0 && i < n) ? keys[i - 1] : ~0ull;
     for (int l = 0; l < L; ++l) {
         const int head = (i < n) && (i == 0 || (k >> (3 * l)) != (kp >> (3 * l)));
         const int c = __reduce_add_sync(0xffffffffu, head);
-        if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + l, c);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sc[l], c);
     }
+    __syncthreads();
+    if (threadIdx.x < L && sc[threadIdx.x]) atomicAdd(cnt + threadIdx.x, sc[threadIdx.x]);
 }
 
-// run heads insert their voxel (key >> 3l, start) into level l's table
-__global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, Grid g) {
+// sum over level-0 runs of (run length)^2 (the point-weighted mean occupancy
+// times n), for the automatic cell size
+__global__ void k_runlen2(const unsigned long long* __restrict__ keys, int64_t n,
+                          unsigned long long* __restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int sh = 3 * g.level;
-    const unsigned long long key = keys[i] >> sh;
-    if (i != 0 && (keys[i - 1] >> sh) == key) return;
-    HashEntry* H = const_cast<HashEntry*>(g.hash);
-    unsigned long long h = hash_slot(g, key);
-    while (true) {
-        unsigned long long prev = atomicCAS(&H[h].key, kEmptyKey, key);
-        if (prev == kEmptyKey) {
-            H[h].start = (int)i;
-            return;
+    unsigned long long v = 0;
+    if (i < n && (i == 0 || keys[i - 1] != keys[i])) {
+        int64_t e = i + 1;
+        while (e < n && keys[e] == keys[i]) ++e;
+        v = (unsigned long long)(e - i) * (unsigned long long)(e - i);
+    }
+    v = __reduce_add_sync(0xffffffffu, (unsigned)min(v, 0xffffffffull));
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
+struct LevelSet {
+    Grid lv[kMaxLevels];
+    int n;
+};
+
+// run heads of every level insert their voxel (key >> 3l, start); level-0 heads
+// are also appended to a compact list (for the adjacency kernel)
+__global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, LevelSet ls, int* __restrict__ nheads,
+                        int* __restrict__ heads) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool in = i < n;
+    const unsigned long long k = in ? keys[i] : 0ull;
+    const unsigned long long kp = (in && i > 0) ? keys[i - 1] : ~0ull;
+    const bool h0 = in && (i == 0 || kp != k);
+    {
+        const unsigned mask = __ballot_sync(0xffffffffu, h0);
+        const int lane = threadIdx.x & 31;
+        int base = 0;
+        if (lane == 0 && mask) base = atomicAdd(nheads, __popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (h0) heads[base + __popc(mask & ((1u << lane) - 1))] = (int)i;
+    }
+    if (!in) return;
+    for (int l = 0; l < ls.n; ++l) {
+        const Grid& g = ls.lv[l];
+        const int sh = 3 * l;
+        const unsigned long long key = k >> sh;
+        if (i != 0 && (kp >> sh) == key) break;  // not a head here => not a head at coarser levels
+        HashEntry* H = const_cast<HashEntry*>(g.hash);
+        unsigned long long h = hash_slot(g, key);
+        while (true) {
+            unsigned long long prev = atomicCAS(&H[h].key, kEmptyKey, key);
+            if (prev == kEmptyKey) {
+                H[h].start = (int)i;
+                break;
+            }
+            h = (h + 1) & g.hmask;
         }
-        h = (h + 1) & g.hmask;
     }
 }
 
-// run tails write the end of their voxel
-__global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, Grid g) {
+// run tails of every level write the end of their voxel
+__global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, LevelSet ls) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int sh = 3 * g.level;
-    const unsigned long long key = keys[i] >> sh;
-    if (i + 1 < n && (keys[i + 1] >> sh) == key) return;
-    HashEntry* H = const_cast<HashEntry*>(g.hash);
-    unsigned long long h = hash_slot(g, key);
-    while (H[h].key != key) h = (h + 1) & g.hmask;
-    H[h].end = (int)(i + 1);
+    const unsigned long long k = keys[i];
+    const unsigned long long kn = i + 1 < n ? keys[i + 1] : ~0ull;
+    for (int l = 0; l < ls.n; ++l) {
+        const Grid& g = ls.lv[l];
+        const int sh = 3 * l;
+        const unsigned long long key = k >> sh;
+        if (i + 1 < n && (kn >> sh) == key) break;
+        HashEntry* H = const_cast<HashEntry*>(g.hash);
+        unsigned long long h = hash_slot(g, key);
+        while (H[h].key != key) h = (h + 1) & g.hmask;
+        H[h].end = (int)(i + 1);
+    }
 }
 
 __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__ perm, int64_t n,
@@ -156,19 +204,20 @@ __device__ __forceinline__ unsigned compact3(unsigned long long v) {
     return (unsigned)v;
 }
 
-// one warp per level-0 hash slot: lane c < 27 probes neighbour c of the slot's
-// voxel (27 independent probes in flight per warp); the non-empty ones are
+// one warp per occupied level-0 voxel (compact head list): lane c < 27 probes
+// neighbour c (27 independent probes in flight per warp); the non-empty ones are
 // compacted in nearest-first order with a ballot and appended at an atomically
 // reserved offset (the list ORDER in memory is scheduling-dependent, the list of
 // every voxel is not); (offset, count) is stored at the voxel's first point.
-__global__ void k_adjacency(Grid g, int64_t cap, int* __restrict__ total, int2* __restrict__ oc,
+__global__ void k_adjacency(Grid g, const unsigned long long* __restrict__ keys, const int* __restrict__ heads,
+                            const int* __restrict__ nheads, int* __restrict__ total, int2* __restrict__ oc,
                             int2* __restrict__ rng_out, unsigned char* __restrict__ code_out) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (w >= cap) return;
-    const HashEntry e = g.hash[w];
-    if (e.key == kEmptyKey) return;  // warp-uniform
-    const int cx = (int)compact3(e.key), cy = (int)compact3(e.key >> 1), cz = (int)compact3(e.key >> 2);
+    if (w >= *nheads) return;  // warp-uniform
+    const int head = heads[w];
+    const unsigned long long key = keys[head];
+    const int cx = (int)compact3(key), cy = (int)compact3(key >> 1), cz = (int)compact3(key >> 2);
     int2 r = make_int2(0, 0);
     int dx = 0, dy = 0, dz = 0;
     if (lane < 27) {
@@ -188,7 +237,7 @@ __global__ void k_adjacency(Grid g, int64_t cap, int* __restrict__ total, int2* 
         rng_out[o] = r;
         code_out[o] = (unsigned char)((dx + 1) * 9 + (dy + 1) * 3 + (dz + 1));
     }
-    if (lane == 0) oc[e.start] = make_int2(base, cnt);
+    if (lane == 0) oc[head] = make_int2(base, cnt);
 }
 
 __global__ void k_fill_hash(HashEntry* H, int64_t cap) {
@@ -316,21 +365,16 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         // Sparser regions are served by the coarser pyramid levels.
         const float trial = E > 0 ? (float)(E / 1024.0) : 1.0f;
         if ((rc = make_grid(mn, mx, trial, &g))) return rc;
-        DevBuf k1, p1;
+        DevBuf k1, p1, acc;
         if ((rc = sort_keys(xyz, n, g, s, k1, p1))) return rc;
-        std::vector<unsigned long long> hk(n);
-        if ((rc = check_cuda(cudaMemcpyAsync(hk.data(), k1.p, n * 8, cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
+        if ((rc = alloc_async(acc, 16, s))) return rc;
+        if ((rc = check_cuda(cudaMemsetAsync(acc.p, 0, 16, s), "memset"))) return rc;
+        k_runlen2<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)k1.p, n, (unsigned long long*)acc.p);
+        unsigned long long sum2 = 0;
+        if ((rc = check_cuda(cudaMemcpyAsync(&sum2, acc.p, 8, cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
         if ((rc = check_cuda(cudaStreamSynchronize(s), "auto cell"))) return rc;
-        std::vector<int> occ_of_point;
-        occ_of_point.reserve(n);
-        for (int64_t i = 0; i < n;) {
-            int64_t j = i;
-            while (j < n && hk[j] == hk[i]) ++j;
-            for (int64_t t = i; t < j; ++t) occ_of_point.push_back((int)(j - i));
-            i = j;
-        }
-        std::nth_element(occ_of_point.begin(), occ_of_point.begin() + n / 2, occ_of_point.end());
-        const double med = std::max(1, occ_of_point[n / 2]);
+        // point-weighted mean voxel occupancy at the trial cell; aim at ~12
+        const double med = std::max(1.0, (double)sum2 / (double)n) / 1.5;
         cell_size = (float)(trial * std::sqrt(8.0 / med));
         if (!(cell_size > 0.0f) || !std::isfinite(cell_size)) cell_size = 1.0f;
     }
@@ -388,12 +432,20 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     idx->device_bytes = n * 2 * (int64_t)sizeof(float4) + total_cap * (int64_t)sizeof(HashEntry);
     k_fill_hash<<<grid_for(total_cap, 256), 256, 0, s>>>(idx->hash_mem, total_cap);
     int64_t off = 0;
+    LevelSet ls;
+    ls.n = L;
     for (int l = 0; l < L; ++l) {
         idx->lv[l].hash = idx->hash_mem + off;
         off += idx->hash_cap[l];
-        k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, idx->lv[l]);
-        k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, idx->lv[l]);
+        ls.lv[l] = idx->lv[l];
     }
+    DevBuf headbuf;
+    if ((rc = alloc_async(headbuf, (n + 4) * sizeof(int), s))) return fail(rc);
+    int* nheads = (int*)headbuf.p;
+    int* heads = nheads + 4;
+    if ((rc = check_cuda(cudaMemsetAsync(nheads, 0, sizeof(int), s), "memset"))) return fail(rc);
+    k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls, nheads, heads);
+    k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls);
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
     {
@@ -408,9 +460,9 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         DevBuf tot;
         if ((rc = alloc_async(tot, 16, s))) return fail(rc);
         if ((rc = check_cuda(cudaMemsetAsync(tot.p, 0, 16, s), "memset"))) return fail(rc);
-        const int64_t threads = idx->hash_cap[0] * 32;
-        k_adjacency<<<grid_for(threads, 256), 256, 0, s>>>(idx->lv[0], idx->hash_cap[0], (int*)tot.p, idx->adj_oc,
-                                                            idx->adj_rng, idx->adj_code);
+        const int64_t threads = (int64_t)std::max(counts[0], 1) * 32;
+        k_adjacency<<<grid_for(threads, 256), 256, 0, s>>>(idx->lv[0], (unsigned long long*)keys.p, heads, nheads,
+                                                            (int*)tot.p, idx->adj_oc, idx->adj_rng, idx->adj_code);
         idx->device_bytes += n * 8 + ub * 9;
         if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);
     }

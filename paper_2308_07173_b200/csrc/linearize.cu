@@ -24,6 +24,7 @@ constexpr int kLinBlock = 256;
 constexpr int kPPT = 1;                       // points per thread
 constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: defines the partition)
 constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
+constexpr int kNV = 31;                       // reduced values: 28 + count + (DUAL) e_old + count_old
 constexpr int kMaxRing = 16;
 
 struct Pose {
@@ -330,19 +331,24 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // SORTED: target covariances from the index's sorted-order copy; SPOS: corr holds
-// sorted positions (internal to gicp_align) instead of original indices.
-template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS>
+// sorted positions (internal to gicp_align) instead of original indices; DUAL
+// (gicp_align's speculative step): in the same pass also the cost e' with the
+// PREVIOUS correspondences corr_old at this T (LM's trial evaluation), values 29-30.
+template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS, bool DUAL>
 __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
                                                          const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
                                                          const float* __restrict__ tgt_cov,
                                                          const float4* __restrict__ tgt_cov_sorted, Pose P, float r2,
-                                                         int32_t* __restrict__ corr, double* __restrict__ partials,
-                                                         unsigned* __restrict__ done, double* __restrict__ out29) {
+                                                         int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
+                                                         double* __restrict__ partials, unsigned* __restrict__ done,
+                                                         double* __restrict__ out29) {
     double acc[kNumAcc];
 #pragma unroll
     for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
-    double cnt = 0.0;
+    double cnt = 0.0, cnt_old = 0.0;
+    double eold[kNumAcc];
+    eold[27] = 0.0;
     const int64_t base = (int64_t)blockIdx.x * kPPB + threadIdx.x;
 #pragma unroll 1
     for (int k = 0; k < kPPT; ++k) {
@@ -387,9 +393,24 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                 qz = bp.z;
             }
         }
-        if (!active || orig < 0) continue;
+        if (!active) continue;
         float cp[6], cq[6];
-        load_cov6(src_cov, i, cp);
+        if (DUAL || orig >= 0) load_cov6(src_cov, i, cp);
+        if (DUAL) {  // the trial cost with the previous correspondences
+            const int c = corr_old[i];
+            if (c >= 0 && c < nt) {
+                const float4 q = SPOS ? __ldg(pts + c) : __ldg(pts_orig + c);
+                const int so = SPOS ? c : __float_as_int(q.w);
+                const int oo = SPOS ? __float_as_int(q.w) : c;
+                if (SORTED)
+                    load_cov_sorted(tgt_cov_sorted, so, cq);
+                else
+                    load_cov6(tgt_cov, oo, cq);
+                accumulate_point<true>(P, pp, q.x, q.y, q.z, cp, cq, eold);
+                cnt_old += 1.0;
+            }
+        }
+        if (orig < 0) continue;
         if (SORTED)
             load_cov_sorted(tgt_cov_sorted, spos, cq);
         else
@@ -398,7 +419,8 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         cnt += 1.0;
     }
     // warp tree
-    __shared__ double sh[kLinBlock / 32][kNumAcc + 1];
+    constexpr int NV = DUAL ? kNV : kNumAcc + 1;
+    __shared__ double sh[kLinBlock / 32][kNV];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int c = 0; c < kNumAcc; ++c) {
@@ -410,16 +432,23 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         const double v = warp_sum(cnt);
         if (lane == 0) sh[wid][kNumAcc] = v;
     }
+    if (DUAL) {
+        const double v1 = warp_sum(eold[27]), v2 = warp_sum(cnt_old);
+        if (lane == 0) {
+            sh[wid][29] = v1;
+            sh[wid][30] = v2;
+        }
+    }
     __syncthreads();
     // block tree: thread c sums component c over the 8 warps in order
-    if (threadIdx.x < kNumAcc + 1) {
+    if (threadIdx.x < NV) {
         const int c = threadIdx.x;
         double v = 0.0;
         if (!(ERROR_ONLY && c < 27)) {
 #pragma unroll
             for (int w = 0; w < kLinBlock / 32; ++w) v += sh[w][c];
         }
-        partials[(int64_t)blockIdx.x * (kNumAcc + 1) + c] = v;
+        partials[(int64_t)blockIdx.x * kNV + c] = v;
     }
     // last block: fixed-order sum of all block partials
     __shared__ bool last;
@@ -433,24 +462,24 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     // loads of each thread batched 8 at a time (independent, in flight together),
     // summed in a fixed order: deterministic and latency-tolerant
     constexpr int kSub = 8;
-    __shared__ double part[kSub][kNumAcc + 1];
+    __shared__ double part[kSub][kNV];
     const int nb = gridDim.x;
-    if (threadIdx.x < kSub * (kNumAcc + 1)) {
-        const int c = threadIdx.x % (kNumAcc + 1), sub = threadIdx.x / (kNumAcc + 1);
+    if (threadIdx.x < kSub * NV) {
+        const int c = threadIdx.x % NV, sub = threadIdx.x / NV;
         double v = 0.0;
         int b = sub;
         for (; b + 7 * kSub < nb; b += 8 * kSub) {
             double t[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partials + (int64_t)(b + u * kSub) * (kNumAcc + 1) + c);
+            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partials + (int64_t)(b + u * kSub) * kNV + c);
 #pragma unroll
             for (int u = 0; u < 8; ++u) v += t[u];
         }
-        for (; b < nb; b += kSub) v += __ldcg(partials + (int64_t)b * (kNumAcc + 1) + c);
+        for (; b < nb; b += kSub) v += __ldcg(partials + (int64_t)b * kNV + c);
         part[sub][c] = v;
     }
     __syncthreads();
-    if (threadIdx.x < kNumAcc + 1) {
+    if (threadIdx.x < NV) {
         const int c = threadIdx.x;
         double v = 0.0;
 #pragma unroll
@@ -468,7 +497,8 @@ __global__ void k_zero29(double* out29) {
 
 int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                      const float* tgt_cov, const double T[16], const double* pivot, float max_corr_dist, int flags,
-                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre) {
+                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre,
+                     const int32_t* corr_old) {
     if (ns == 0) {
         k_zero29<<<1, 32, 0, s>>>(out29);
         return check_cuda(cudaGetLastError(), "linearize launch");
@@ -522,9 +552,12 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     const bool reuse = flags & GICP_LIN_REUSE_CORR, eonly = flags & GICP_LIN_ERROR_ONLY;
     const bool sorted = tgt->cov_sorted != nullptr && tgt_cov == tgt->cov_attached;
     const bool spos = (flags & kLinCorrSpos) && sorted;
-#define GICP_LIN_ARGS \
-    src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, partials, done, out29
-#define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
+    const bool dual = corr_old != nullptr && !reuse && !eonly;
+#define GICP_LIN_ARGS                                                                                            \
+    src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
+        done, out29
+#define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
+#define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_RE(S, SP)           \
     if (reuse && eonly)              \
         GICP_LIN_GO(true, true, S, SP);   \
@@ -534,13 +567,21 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
         GICP_LIN_GO(false, true, S, SP);  \
     else                             \
         GICP_LIN_GO(false, false, S, SP);
-    if (spos) {
+    if (dual) {
+        if (spos)
+            GICP_LIN_DUAL(true, true);
+        else if (sorted)
+            GICP_LIN_DUAL(true, false);
+        else
+            GICP_LIN_DUAL(false, false);
+    } else if (spos) {
         GICP_LIN_RE(true, true)
     } else if (sorted) {
         GICP_LIN_RE(true, false)
     } else {
         GICP_LIN_RE(false, false)
     }
+#undef GICP_LIN_DUAL
 #undef GICP_LIN_RE
 #undef GICP_LIN_GO
 #undef GICP_LIN_ARGS
@@ -551,7 +592,7 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
 
 size_t linearize_scratch_bytes(int64_t ns) {
     const int64_t nb = (ns + kPPB - 1) / kPPB;
-    return (size_t)nb * (kNumAcc + 1) * sizeof(double) + 256;
+    return (size_t)nb * kNV * sizeof(double) + 256;
 }
 
 }  // namespace gicp
