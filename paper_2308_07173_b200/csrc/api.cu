@@ -366,10 +366,24 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 double E[16], Tn[16];
                 pivoted_exp(delta, piv, E);
                 mul44(E, T, Tn);
-                // trial: e' with the current correspondences at Tn, and speculatively
-                // the full linearisation at Tn (needed next if the step is accepted)
+                // trial: e' with the current correspondences at Tn. The first trial of
+                // an iteration is usually accepted, so it also computes, speculatively,
+                // the full linearisation at Tn in the same pass; later trials (after a
+                // rejection) evaluate e' alone and linearise only once accepted.
                 const double pn[3] = {Tn[3], Tn[7], Tn[11]};
-                if ((rc = lin(Tn, pn, corr_b, corr_a))) break;
+                const bool spec = inner == 0;
+                if (spec) {
+                    if ((rc = lin(Tn, pn, corr_b, corr_a))) break;
+                } else {
+                    rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, Tn, pn, prm->max_corr_dist,
+                                          kLinCorrSpos | GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY, d_out, corr_a, s,
+                                          &ls);
+                    if (!rc) rc = check_cuda(cudaMemcpyAsync(h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s),
+                                             "D2H");
+                    if (!rc) rc = check_cuda(cudaStreamSynchronize(s), "align sync");
+                    if (rc) break;
+                    h[29] = h[27];
+                }
                 const double en = h[29];
                 double den = 0.0;
                 for (int a = 0; a < 6; ++a) den += delta[a] * (lambda * delta[a] - b[a]);
@@ -377,6 +391,9 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 if (rho > 0) {
                     std::memcpy(T, Tn, sizeof(T));
                     std::memcpy(piv, pn, sizeof(piv));
+                    if (!spec) {  // linearise at the accepted pose now
+                        if ((rc = lin(T, piv, corr_b, nullptr))) break;
+                    }
                     std::memcpy(lin29, h, sizeof(lin29));
                     std::swap(corr_a, corr_b);
                     const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);

@@ -127,33 +127,34 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 ++nr;
             }
         }
-        int ri = use_adj ? a0 : 0;
-        const int rend = use_adj ? a1 : nr;
-        int pos = 0, end = 0;
-        while (true) {
-            while (pos == end && ri < rend) {
-                int2 r;
+        // entry-major, warp-uniform: step k tests every lane's k-th voxel against
+        // min(best, r2) (predicated: load, decode, bound) and the lanes whose voxel
+        // survives scan it together (inner loop = the longest surviving range).
+        // Nearest-first order makes almost every voxel after the own one prunable.
+        const int cnt = use_adj ? a1 - a0 : nr;
+        const int kmax = __reduce_max_sync(0xffffffffu, active ? cnt : 0);
+        for (int k = 0; k < kmax; ++k) {
+            int2 r = make_int2(0, 0);
+            if (k < cnt) {
                 float lb2;
                 if (use_adj) {
-                    r = __ldg(lvs.adj_rng + ri);
-                    const int code = __ldg(lvs.adj_code + ri);
+                    r = __ldg(lvs.adj_rng + a0 + k);
+                    const int code = __ldg(lvs.adj_code + a0 + k);
                     const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
                     const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
                     const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
                     const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
                     lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
                 } else {
-                    r = rl[ri];
-                    lb2 = lbl[ri];
+                    r = rl[k];
+                    lb2 = lbl[k];
                 }
-                ++ri;
-                if (lb2 * kRel > bound()) continue;
-                pos = r.x;
-                end = r.y;
+                if (lb2 * kRel > bound()) r = make_int2(0, 0);
             }
-            const bool has = pos < end;
-            if (!__any_sync(0xffffffffu, has)) break;
-            if (has) consider(pos++);
+            const int len = r.y - r.x;
+            const int lmax = __reduce_max_sync(0xffffffffu, len);
+            for (int j = 0; j < lmax; ++j)
+                if (j < len) consider(r.x + j);
         }
         if (!active) return;
         const float m = cube_margin(G, s, slack, 1);
