@@ -41,8 +41,10 @@ __device__ __forceinline__ void plane_cov(float s00, float s01, float s02, float
             const double p = ((l - c2) * l + c1) * l - c0;
             const double dp = (3.0 * l - 2.0 * c2) * l + c1;
             if (!(dp > 0.0)) break;
-            const double step = p / dp;
-            const double ln = l - step;
+            // left of the root p < 0; p >= 0 means rounding noise at the root (the
+            // iterate would oscillate by an ulp instead of reaching a fixed point)
+            if (!(p < 0.0)) break;
+            const double ln = l - p / dp;
             if (ln == l) break;
             l = ln;
         }

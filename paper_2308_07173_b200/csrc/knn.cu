@@ -33,6 +33,15 @@ namespace gicp {
 namespace {
 
 constexpr int kBlock = 128;
+#ifndef GICP_KNN_PROF
+#define GICP_KNN_PROF 0  // diagnostics build: per-warp step/replacement counters
+#endif
+#if GICP_KNN_PROF
+__device__ unsigned long long g_kprof[16];
+#define KPROF(x) x
+#else
+#define KPROF(x)
+#endif
 #ifndef GICP_KNN_MINB
 #define GICP_KNN_MINB 6
 #endif
@@ -272,46 +281,49 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     int cnt = 0;
     unsigned long long top = 0ull;  // root (max) once cnt == K
     unsigned tie = 0xffffffffu;
-    int ri = use_adj ? a0 : 0;
-    const int rend = use_adj ? a1 : nr;
-    int pos = 0, end = 0;
-    while (true) {
-        // advance exhausted lanes to their next non-pruned range
-        while (pos == end && ri < rend) {
-            int2 r;
-            float lb2;
-            if (use_adj) {
-                r = __ldg(adj.rng + ri);
-                const int code = __ldg(adj.code + ri);
-                const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
-                const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
-                const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
-                const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
-                lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
-            } else {
-                r = rl[ri];
-                lb2 = lbl[ri];
+    // predicated replace-root + sift-down (padding slots hold 0-keys), issued once for the warp
+    auto sift = [&](const bool repl, const unsigned long long key, const unsigned th) {
+        const unsigned hi = hi32(key);
+        int i = 0;
+        bool moving = repl;
+#pragma unroll
+        for (int lev = 0; lev < D; ++lev) {
+            const int l = 2 * i + 1;
+            unsigned long long cv, rv;
+            if (moving) {
+                cv = HSLOT(l);
+                rv = HSLOT(l + 1);
             }
-            ++ri;
-            if (cnt == K && lb2 * kRel > __uint_as_float(hi32(top))) continue;
-            pos = r.x;
-            end = r.y;
+            const bool pr = EXACT ? rv > cv : hi32(rv) > hi32(cv);
+            const unsigned long long ch = pr ? rv : cv;
+            const bool mv = moving && (EXACT ? ch > key : hi32(ch) > hi);
+            if (mv) HSLOT(i) = ch;
+            i = mv ? l + (int)pr : i;
+            moving = mv;
         }
-        const bool has = pos < end;
-        if (!__any_sync(0xffffffffu, has)) break;
+        if (repl) {
+            HSLOT(i) = key;
+            top = HSLOT(0);
+            if (!EXACT && hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
+        }
+    };
+    // one candidate step for the whole warp (lanes without a candidate idle)
+    KPROF(unsigned p_steps = 0; unsigned p_fill = 0; unsigned p_repl = 0; unsigned p_lrepl = 0; unsigned p_cand = 0;
+          unsigned p_ent = 0; unsigned p_adv = 0;)
+    auto step = [&](const bool has, const int j) {
         unsigned hi = 0xffffffffu, pay = 0u;
-        const int j = pos;
         if (has) {
             const float4 p = __ldg(pts + j);
             hi = __float_as_uint(dist2(G.qx, G.qy, G.qz, p.x, p.y, p.z));
             pay = EXACT ? __float_as_uint(p.w) : (unsigned)j;
-            ++pos;
         }
         const unsigned long long key = ((unsigned long long)hi << 32) | pay;
         const bool fill = has && cnt < K;
         const unsigned th = hi32(top);
         const bool repl = has && cnt == K && (EXACT ? key < top : hi < th);
         if (!EXACT && has && cnt == K && hi == th) tie = min(tie, hi);  // rejected key tied with the K-th
+        KPROF(p_steps++; p_fill += __any_sync(0xffffffffu, fill); p_repl += __any_sync(0xffffffffu, repl);
+              p_lrepl += repl; p_cand += has;)
         if (__any_sync(0xffffffffu, fill)) {
             // predicated sift-up from slot cnt
             int i = cnt;
@@ -333,32 +345,52 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
                 if (cnt == K) top = HSLOT(0);
             }
         }
-        if (__any_sync(0xffffffffu, repl)) {
-            // predicated replace-root + sift-down (padding slots hold 0-keys)
-            int i = 0;
-            bool moving = repl;
-#pragma unroll
-            for (int lev = 0; lev < D; ++lev) {
-                const int l = 2 * i + 1;
-                unsigned long long cv, rv;
-                if (moving) {
-                    cv = HSLOT(l);
-                    rv = HSLOT(l + 1);
-                }
-                const bool pr = EXACT ? rv > cv : hi32(rv) > hi32(cv);
-                const unsigned long long ch = pr ? rv : cv;
-                const bool mv = moving && (EXACT ? ch > key : hi32(ch) > hi);
-                if (mv) HSLOT(i) = ch;
-                i = mv ? l + (int)pr : i;
-                moving = mv;
+        if (__any_sync(0xffffffffu, repl)) sift(repl, key, th);
+        };
+    int ri = use_adj ? a0 : 0;
+    const int rend = use_adj ? a1 : nr;
+    int pos = 0, end = 0;
+    while (true) {
+        // advance exhausted lanes to their next non-pruned range
+        KPROF(const unsigned e0 = p_ent;)
+        while (pos == end && ri < rend) {
+            KPROF(p_ent++;)
+            int2 r;
+            float lb2;
+            if (use_adj) {
+                r = __ldg(adj.rng + ri);
+                const int code = __ldg(adj.code + ri);
+                const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
+                const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
+                const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
+                const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
+                lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+            } else {
+                r = rl[ri];
+                lb2 = lbl[ri];
             }
-            if (repl) {
-                HSLOT(i) = key;
-                top = HSLOT(0);
-                if (!EXACT && hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
-            }
+            ++ri;
+            if (cnt == K && lb2 * kRel > __uint_as_float(hi32(top))) continue;
+            pos = r.x;
+            end = r.y;
+        }
+        KPROF(p_adv += __reduce_max_sync(0xffffffffu, p_ent - e0);)
+        const bool has = pos < end;
+        if (!__any_sync(0xffffffffu, has)) break;
+        step(has, pos);
+        if (has) ++pos;
+    }
+#if GICP_KNN_PROF
+    if (g.level == 0 && !EXACT) {
+        const unsigned full = 0xffffffffu;
+        const unsigned v[8] = {p_steps, p_fill, p_repl, __reduce_add_sync(full, p_lrepl), __reduce_max_sync(full, p_lrepl),
+                               __reduce_add_sync(full, p_cand), __reduce_add_sync(full, p_ent), p_adv};
+        if ((threadIdx.x & 31) == 0) {
+            for (int i = 0; i < 8; ++i) atomicAdd(&g_kprof[i], (unsigned long long)v[i]);
+            atomicAdd(&g_kprof[8], 1ull);
         }
     }
+#endif
     if (!active) return 0;
     if (cnt < K) return 1;
     const float m = cube_margin(G, s, slack, 1);
@@ -813,6 +845,16 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
         int h[4] = {0, 0, 0, 0};
         cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
+#if GICP_KNN_PROF
+        unsigned long long pv[16];
+        cudaMemcpyFromSymbol(pv, g_kprof, sizeof(pv));
+        const double w = (double)pv[8];
+        fprintf(stderr, "[gicp knn prof] warps=%.0f per warp: steps %.1f fill-steps %.1f repl-steps %.1f lane-repl %.1f "
+                "max-lane-repl %.1f lane-cand %.1f lane-entries %.1f adv-iters %.1f\n", w, pv[0] / w, pv[1] / w,
+                pv[2] / w, pv[3] / w, pv[4] / w, pv[5] / w, pv[6] / w, pv[7] / w);
+        for (auto& x : pv) x = 0;
+        cudaMemcpyToSymbol(g_kprof, pv, sizeof(pv));
+#endif
         fprintf(stderr, "[gicp knn] m=%lld levels=%d escalated=%d exact=%d bruteforce=%d\n", (long long)m, L, h[2],
                 h[0], h[1]);
         if (h[0] > 0) {
