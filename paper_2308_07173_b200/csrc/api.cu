@@ -174,7 +174,6 @@ GICP_API void gicp_index_free(gicp_index idx) {
     if (idx->cov_sorted) cudaFreeAsync(idx->cov_sorted, s);
     if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
     if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
-    if (idx->adj_code) cudaFreeAsync(idx->adj_code, s);
     cudaGetLastError();
     delete idx;
 }

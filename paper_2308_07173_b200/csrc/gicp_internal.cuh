@@ -150,8 +150,7 @@ struct gicp_index_s {
     float4* pts_orig = nullptr;
     gicp::HashEntry* hash_mem = nullptr;  // all levels' tables, one allocation
     int2* adj_oc = nullptr;               // [n] (offset, count) of the level-0 adjacency list, at voxel heads
-    int2* adj_rng = nullptr;              // neighbour voxel ranges, nearest-first per voxel
-    unsigned char* adj_code = nullptr;    // offset codes (dx+1)*9 + (dy+1)*3 + (dz+1)
+    int2* adj_rng = nullptr;              // neighbour voxels, nearest-first per voxel: {start, count<<6 | code}
     float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
     const float* cov_attached = nullptr;  // the caller's original-order array they were copied from
     int device = 0;
@@ -172,6 +171,26 @@ int launch_knn(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_
 int launch_covariances(const float* xyz, int64_t n, const int32_t* nbr, int64_t m, int k, float eps, float* cov,
                        cudaStream_t s);
 // preallocated linearize scratch (gicp_align): block partials + done counter
+// Packed level-0 adjacency entry (index.cu k_adjacency): x = first point of the
+// neighbour voxel in pts, y = (count << 6) | code, code = (dx+1) | (dy+1) << 2 |
+// (dz+1) << 4 for the neighbour's offset (dx, dy, dz) in {-1,0,1}^3.
+constexpr int kAdjCountShift = 6;
+constexpr int kAdjMaxCount = (1 << (31 - kAdjCountShift)) - 1;
+__host__ __device__ __forceinline__ unsigned adj_pack(int count, int dx, int dy, int dz) {
+    return ((unsigned)count << kAdjCountShift) | (unsigned)(dx + 1) | ((unsigned)(dy + 1) << 2) |
+           ((unsigned)(dz + 1) << 4);
+}
+// squared lower bound of the distance from the query to the neighbour voxel: per
+// axis the gap to the face on the offset's side (lo for -1, hi for +1, 0 for 0)
+__device__ __forceinline__ float adj_lb2(unsigned w, float lox, float hix, float loy, float hiy, float loz, float hiz) {
+    const unsigned bx = w & 3u, by = (w >> 2) & 3u, bz = (w >> 4) & 3u;
+    const float gx = bx == 0u ? lox : (bx == 2u ? hix : 0.0f);
+    const float gy = by == 0u ? loy : (by == 2u ? hiy : 0.0f);
+    const float gz = bz == 0u ? loz : (bz == 2u ? hiz : 0.0f);
+    return __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+}
+__device__ __forceinline__ int2 adj_range(int2 e) { return make_int2(e.x, e.x + (int)((unsigned)e.y >> kAdjCountShift)); }
+
 struct LinScratch {
     unsigned* done;
     double* partials;

@@ -186,7 +186,7 @@ __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__
 
 // Level-0 voxel adjacency lists: for every occupied voxel, its
 // non-empty voxels among the 27 around it, nearest-first, as (start, end) ranges
-// of pts plus a 5-bit offset code (dx+1)*9 + (dy+1)*3 + (dz+1). A query in an
+// of pts packed with the offset code (adj_pack, gicp_internal.cuh). A query in an
 // occupied voxel reads this shared list instead of probing the hash 27 times.
 __device__ __constant__ signed char c_adj_order[27][3] = {
     {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
@@ -211,7 +211,7 @@ __device__ __forceinline__ unsigned compact3(unsigned long long v) {
 // every voxel is not); (offset, count) is stored at the voxel's first point.
 __global__ void k_adjacency(Grid g, const unsigned long long* __restrict__ keys, const int* __restrict__ heads,
                             const int* __restrict__ nheads, int* __restrict__ total, int2* __restrict__ oc,
-                            int2* __restrict__ rng_out, unsigned char* __restrict__ code_out) {
+                            int2* __restrict__ rng_out) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= *nheads) return;  // warp-uniform
@@ -234,8 +234,9 @@ __global__ void k_adjacency(Grid g, const unsigned long long* __restrict__ keys,
     base = __shfl_sync(0xffffffffu, base, 0);
     if (ne) {
         const int o = base + __popc(mask & ((1u << lane) - 1));
-        rng_out[o] = r;
-        code_out[o] = (unsigned char)((dx + 1) * 9 + (dy + 1) * 3 + (dz + 1));
+        const int c = r.y - r.x;
+        if (c > kAdjMaxCount) atomicOr(total + 1, 1);  // count does not fit the packing: no lists
+        rng_out[o] = make_int2(r.x, (int)adj_pack(c, dx, dy, dz));
     }
     if (lane == 0) oc[head] = make_int2(base, cnt);
 }
@@ -419,7 +420,6 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if (idx->hash_mem) cudaFreeAsync(idx->hash_mem, s);
         if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
         if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
-        if (idx->adj_code) cudaFreeAsync(idx->adj_code, s);
         delete idx;
         return code;
     };
@@ -448,12 +448,12 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls);
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
+    int adj_overflow = 0;
     {
         // level-0 adjacency lists, one pass (upper bound 27 entries per voxel)
         const int64_t ub = 27 * std::max<int64_t>(counts[0], 1);
         if (cudaMallocAsync(&idx->adj_oc, n * sizeof(int2), s) != cudaSuccess ||
-            cudaMallocAsync(&idx->adj_rng, ub * sizeof(int2), s) != cudaSuccess ||
-            cudaMallocAsync(&idx->adj_code, ub, s) != cudaSuccess) {
+            cudaMallocAsync(&idx->adj_rng, ub * sizeof(int2), s) != cudaSuccess) {
             cudaGetLastError();
             return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
         }
@@ -462,11 +462,20 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if ((rc = check_cuda(cudaMemsetAsync(tot.p, 0, 16, s), "memset"))) return fail(rc);
         const int64_t threads = (int64_t)std::max(counts[0], 1) * 32;
         k_adjacency<<<grid_for(threads, 256), 256, 0, s>>>(idx->lv[0], (unsigned long long*)keys.p, heads, nheads,
-                                                            (int*)tot.p, idx->adj_oc, idx->adj_rng, idx->adj_code);
-        idx->device_bytes += n * 8 + ub * 9;
+                                                            (int*)tot.p, idx->adj_oc, idx->adj_rng);
+        idx->device_bytes += n * 8 + ub * 8;
         if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);
+        if ((rc = check_cuda(cudaMemcpyAsync(&adj_overflow, (int*)tot.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s),
+                             "adjacency flag")))
+            return fail(rc);
     }
     if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
+    if (adj_overflow) {  // a voxel too full for the packed entry: queries probe the hash instead
+        cudaFreeAsync(idx->adj_oc, s);
+        cudaFreeAsync(idx->adj_rng, s);
+        idx->adj_oc = nullptr;
+        idx->adj_rng = nullptr;
+    }
     *out = idx;
     return GICP_OK;
 }

@@ -209,8 +209,7 @@ struct FastShape {
 // level-0 voxel adjacency lists of the index (index.cu)
 struct AdjView {
     const int2* oc;
-    const int2* rng;
-    const unsigned char* code;
+    const int2* rng;  // packed entries (adj_pack)
 };
 
 template <int KCAP, bool EXACT = false>
@@ -304,24 +303,26 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
         if (repl) {
             HSLOT(i) = key;
             top = HSLOT(0);
-            if (!EXACT && hi32(top) == th) tie = min(tie, th);  // evicted key tied with the new K-th
+            if (!EXACT && hi32(top) == th) tie = th;  // evicted key tied with the new K-th
         }
     };
     // one candidate step for the whole warp (lanes without a candidate idle)
     KPROF(unsigned p_steps = 0; unsigned p_fill = 0; unsigned p_repl = 0; unsigned p_lrepl = 0; unsigned p_cand = 0;
           unsigned p_ent = 0; unsigned p_adv = 0;)
-    auto step = [&](const bool has, const int j) {
+    auto step = [&](const bool has, const int j, const float4 p) {
         unsigned hi = 0xffffffffu, pay = 0u;
         if (has) {
-            const float4 p = __ldg(pts + j);
             hi = __float_as_uint(dist2(G.qx, G.qy, G.qz, p.x, p.y, p.z));
             pay = EXACT ? __float_as_uint(p.w) : (unsigned)j;
         }
         const unsigned long long key = ((unsigned long long)hi << 32) | pay;
         const bool fill = has && cnt < K;
         const unsigned th = hi32(top);
-        const bool repl = has && cnt == K && (EXACT ? key < top : hi < th);
-        if (!EXACT && has && cnt == K && hi == th) tie = min(tie, hi);  // rejected key tied with the K-th
+        // top == 0 until the heap is full and an idle lane has hi = ~0, so neither
+        // needs its own test. A recorded tie value is the K-th at that time, which
+        // never increases: the last one recorded is the smallest.
+        const bool repl = EXACT ? (has && cnt == K && key < top) : hi < th;
+        if (!EXACT && hi == th) tie = hi;  // rejected key tied with the K-th
         KPROF(p_steps++; p_fill += __any_sync(0xffffffffu, fill); p_repl += __any_sync(0xffffffffu, repl);
               p_lrepl += repl; p_cand += has;)
         if (__any_sync(0xffffffffu, fill)) {
@@ -350,6 +351,11 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     int ri = use_adj ? a0 : 0;
     const int rend = use_adj ? a1 : nr;
     int pos = 0, end = 0;
+    // software pipeline: the next adjacency entry and the next candidate point are
+    // loaded one advance / one step ahead, so their latency overlaps the heap work
+    int2 ne = make_int2(0, 0);
+    if (use_adj && ri < rend) ne = __ldg(adj.rng + ri);
+    float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
     while (true) {
         // advance exhausted lanes to their next non-pruned range
         KPROF(const unsigned e0 = p_ent;)
@@ -358,13 +364,10 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
             int2 r;
             float lb2;
             if (use_adj) {
-                r = __ldg(adj.rng + ri);
-                const int code = __ldg(adj.code + ri);
-                const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
-                const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
-                const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
-                const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
-                lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                const int2 e = ne;
+                if (ri + 1 < rend) ne = __ldg(adj.rng + ri + 1);
+                r = adj_range(e);
+                lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
             } else {
                 r = rl[ri];
                 lb2 = lbl[ri];
@@ -373,24 +376,16 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
             if (cnt == K && lb2 * kRel > __uint_as_float(hi32(top))) continue;
             pos = r.x;
             end = r.y;
+            pn = __ldg(pts + pos);
         }
         KPROF(p_adv += __reduce_max_sync(0xffffffffu, p_ent - e0);)
         const bool has = pos < end;
         if (!__any_sync(0xffffffffu, has)) break;
-        step(has, pos);
+        const float4 p = pn;
+        if (pos + 1 < end) pn = __ldg(pts + pos + 1);
+        step(has, pos, p);
         if (has) ++pos;
     }
-#if GICP_KNN_PROF
-    if (g.level == 0 && !EXACT) {
-        const unsigned full = 0xffffffffu;
-        const unsigned v[8] = {p_steps, p_fill, p_repl, __reduce_add_sync(full, p_lrepl), __reduce_max_sync(full, p_lrepl),
-                               __reduce_add_sync(full, p_cand), __reduce_add_sync(full, p_ent), p_adv};
-        if ((threadIdx.x & 31) == 0) {
-            for (int i = 0; i < 8; ++i) atomicAdd(&g_kprof[i], (unsigned long long)v[i]);
-            atomicAdd(&g_kprof[8], 1ull);
-        }
-    }
-#endif
     if (!active) return 0;
     if (cnt < K) return 1;
     const float m = cube_margin(G, s, slack, 1);
@@ -831,7 +826,7 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     Levels lvs;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
     // level 0 over every query, then one launch that climbs the pyramid for the rest
-    const AdjView adj{idx->adj_oc, idx->adj_rng, idx->adj_code};
+    const AdjView adj{idx->adj_oc, idx->adj_rng};
     k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
                                                          cov, counts + 2, listA, counts + 0, exact, L == 1);
     if (L > 1)

@@ -41,7 +41,6 @@ struct Levels {
     int ring_level;  // finest level with cell >= r/2: rings there reach the gate in <= 3 steps
     const int2* adj_oc;  // level-0 voxel adjacency lists (index.cu)
     const int2* adj_rng;
-    const unsigned char* adj_code;
 };
 
 // Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) over all
@@ -138,13 +137,9 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             if (k < cnt) {
                 float lb2;
                 if (use_adj) {
-                    r = __ldg(lvs.adj_rng + a0 + k);
-                    const int code = __ldg(lvs.adj_code + a0 + k);
-                    const int dx = code / 9 - 1, dy = (code / 3) % 3 - 1, dz = code % 3 - 1;
-                    const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
-                    const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
-                    const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
-                    lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                    const int2 e = __ldg(lvs.adj_rng + a0 + k);
+                    r = adj_range(e);
+                    lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
                 } else {
                     r = rl[k];
                     lb2 = lbl[k];
@@ -521,7 +516,6 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
     lvs.adj_oc = tgt->adj_oc;
     lvs.adj_rng = tgt->adj_rng;
-    lvs.adj_code = tgt->adj_code;
     lvs.ring_level = lvs.n - 1;
     for (int l = 0; l < lvs.n; ++l)
         if (2.0f * tgt->lv[l].cell >= max_corr_dist) {
