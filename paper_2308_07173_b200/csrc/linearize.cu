@@ -15,6 +15,9 @@
 // partials [nblocks][29] -> the last block to finish sums them in block order.
 // Every step has a fixed order, so out29 is bitwise reproducible and independent
 // of the SM count / scheduling.
+#include <cstdio>
+#include <cstdlib>
+
 #include "gicp_internal.cuh"
 
 namespace gicp {
@@ -26,6 +29,19 @@ constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: define
 constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
 constexpr int kNV = 31;                       // reduced values: 28 + count + (DUAL) e_old + count_old
 constexpr int kMaxRing = 16;
+#ifndef GICP_LIN_PROF
+#define GICP_LIN_PROF 0  // diagnostics build: search stage counts and warp-duration histogram
+#endif
+#if GICP_LIN_PROF
+__device__ unsigned long long g_lprof[40];  // [0..3] stage counts, [4] max warp cycles, [8..39] log2 histogram
+#define LPROF(x) x
+#else
+#define LPROF(x)
+#endif
+#ifndef GICP_LIN_UNROLL
+#define GICP_LIN_UNROLL 4
+#endif
+constexpr int kUnroll = GICP_LIN_UNROLL;  // candidates loaded together in the level-0 scan
 
 struct Pose {
     double R[9];
@@ -58,8 +74,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     bj = -1;
     bp = make_float3(0.f, 0.f, 0.f);
     auto bound = [&]() { return fminf(__uint_as_float((unsigned)(best >> 32)), r2); };
-    auto consider = [&](int j) {
-        const float4 p = __ldg(pts + j);
+    auto consider_p = [&](int j, const float4 p) {
         const float d2 = dist2(qx, qy, qz, p.x, p.y, p.z);
         const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
         if (key < best) {
@@ -68,6 +83,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             bj = j;
         }
     };
+    auto consider = [&](int j) { consider_p(j, __ldg(pts + j)); };
     auto scan = [&](int2 rng) {
         for (int j = rng.x; j < rng.y; ++j) consider(j);
     };
@@ -132,12 +148,17 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         // Nearest-first order makes almost every voxel after the own one prunable.
         const int cnt = use_adj ? a1 - a0 : nr;
         const int kmax = __reduce_max_sync(0xffffffffu, active ? cnt : 0);
+        // the next entry is loaded one entry ahead; candidates go kUnroll at a time
+        // (independent loads in flight together: the search is latency-bound)
+        int2 ne = make_int2(0, 0);
+        if (use_adj && cnt > 0) ne = __ldg(lvs.adj_rng + a0);
         for (int k = 0; k < kmax; ++k) {
             int2 r = make_int2(0, 0);
             if (k < cnt) {
                 float lb2;
                 if (use_adj) {
-                    const int2 e = __ldg(lvs.adj_rng + a0 + k);
+                    const int2 e = ne;
+                    if (k + 1 < cnt) ne = __ldg(lvs.adj_rng + a0 + k + 1);
                     r = adj_range(e);
                     lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
                 } else {
@@ -148,8 +169,15 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             }
             const int len = r.y - r.x;
             const int lmax = __reduce_max_sync(0xffffffffu, len);
-            for (int j = 0; j < lmax; ++j)
-                if (j < len) consider(r.x + j);
+            for (int j = 0; j < lmax; j += kUnroll) {
+                float4 pv[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    if (j + u < len) pv[u] = __ldg(pts + r.x + j + u);
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    if (j + u < len) consider_p(r.x + j + u, pv[u]);
+            }
         }
         if (!active) return;
         const float m = cube_margin(G, s, slack, 1);
@@ -157,6 +185,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) return;
     }
     // (2) per lane: coarser levels' cubes up to ring_level, then rings there
+    LPROF(atomicAdd(&g_lprof[1], 1ull);)
     for (int l = 1; l <= lvs.ring_level; ++l) {
         const Grid& g = lvs.lv[l];
         const QGeom G = make_geom(g, qx, qy, qz);
@@ -179,9 +208,11 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         const float s = g.cell, slack = g.slack;
         const int R0 = max(max(max(-G.cx, G.cx - (g.nx - 1)), max(-G.cy, G.cy - (g.ny - 1))),
                            max(-G.cz, G.cz - (g.nz - 1)));
+        LPROF(atomicAdd(&g_lprof[2], 1ull);)
         for (int R = 2;; ++R) {
             if (R < R0) R = R0;
             if (R > max(R0, 1) + kMaxRing) {
+                LPROF(atomicAdd(&g_lprof[3], 1ull);)
                 overflow = 1;
                 return;
             }
@@ -376,7 +407,17 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             unsigned long long best;
             float3 bp;
             int bj, ovf;
+            LPROF(const long long t0 = clock64();)
             nn_search(pts, lvs, active, sx, sy, sz, r2, best, bp, bj, ovf);
+            LPROF({
+                const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
+                const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
+                if ((threadIdx.x & 31) == 0) {
+                    atomicAdd(&g_lprof[0], 1ull);
+                    atomicMax(&g_lprof[4], (unsigned long long)mx);
+                    atomicAdd(&g_lprof[8 + min(31, 31 - __clz(mx | 1))], 1ull);
+                }
+            })
             if (active) {
                 if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp, bj);
                 const float bd2 = __uint_as_float((unsigned)(best >> 32));
@@ -582,6 +623,20 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
 #undef GICP_LIN_ARGS
     const int rc = check_cuda(cudaGetLastError(), "linearize launch");
     if (scratch) cudaFreeAsync(scratch, s);
+#if GICP_LIN_PROF
+    if (getenv("GICP_DEBUG_STATS")) {
+        unsigned long long h[40];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(h, g_lprof, sizeof(h));
+        fprintf(stderr, "[gicp lin prof] warps=%llu fallback=%llu rings=%llu overflow=%llu max-warp-cycles=%llu hist:",
+                h[0], h[1], h[2], h[3], h[4]);
+        for (int b = 8; b < 40; ++b)
+            if (h[b]) fprintf(stderr, " 2^%d:%llu", b - 8, h[b]);
+        fprintf(stderr, "\n");
+        for (auto& x : h) x = 0;
+        cudaMemcpyToSymbol(g_lprof, h, sizeof(h));
+    }
+#endif
     return rc;
 }
 

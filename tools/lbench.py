@@ -58,3 +58,14 @@ for name, TT, kw in (("T_true", T, {}), ("T0", T0, {}), ("T_true reuse+err", T, 
         if r >= 2:
             ts.append(a.elapsed_time(b))
     print(f"linearize {name}: median {1e3 * np.median(ts):.1f} us  inliers {out[28].item():.0f}")
+# back-to-back launches: per-call device time once the queue is ahead of the GPU
+for name, TT, kw in (("T_true", T, {}), ("T0", T0, {}), ("T_true reuse+err", T, dict(reuse_corr=True, error_only=True))):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.linearize(sd, cs, im, cm, TT, 1.0, corr=corr, out=out, **kw)
+    torch.cuda._sleep(2_000_000)
+    a.record()
+    for r in range(50):
+        g.linearize(sd, cs, im, cm, TT, 1.0, corr=corr, out=out, **kw)
+    b.record()
+    torch.cuda.synchronize()
+    print(f"linearize {name} x50 loop: {1e3 * a.elapsed_time(b) / 50:.1f} us/call")
