@@ -73,19 +73,29 @@ GICP_HD unsigned long long hash_slot(const Grid& g, unsigned long long key) {
     return (key * 0x9E3779B97F4A7C15ull) >> (64 - g.hbits);
 }
 
+// [start, end) of the voxel with Morton key `key` at level g, or an empty range.
+// Linear probing, two slots per step: both loads are issued together, so a probe
+// chain costs half as many dependent round trips to L2.
+__device__ __forceinline__ int2 hash_find(const Grid& g, unsigned long long key) {
+    const int4* __restrict__ H = reinterpret_cast<const int4*>(g.hash);
+    unsigned long long h = hash_slot(g, key);
+    while (true) {
+        const int4 a = __ldg(H + h), b = __ldg(H + ((h + 1) & g.hmask));
+        const unsigned long long ka = (unsigned long long)(unsigned)a.x | ((unsigned long long)(unsigned)a.y << 32);
+        const unsigned long long kb = (unsigned long long)(unsigned)b.x | ((unsigned long long)(unsigned)b.y << 32);
+        if (ka == key) return make_int2(a.z, a.w);
+        if (ka == kEmptyKey) return make_int2(0, 0);
+        if (kb == key) return make_int2(b.z, b.w);
+        if (kb == kEmptyKey) return make_int2(0, 0);
+        h = (h + 2) & g.hmask;
+    }
+}
+
 // Returns [start, end) of the voxel (cx, cy, cz) of level g in pts, or an empty range.
 __device__ __forceinline__ int2 cell_lookup(const Grid& g, int cx, int cy, int cz) {
     if ((unsigned)cx >= (unsigned)g.nx || (unsigned)cy >= (unsigned)g.ny || (unsigned)cz >= (unsigned)g.nz)
         return make_int2(0, 0);
-    const unsigned long long key = cell_key(cx, cy, cz);
-    unsigned long long h = hash_slot(g, key);
-    while (true) {
-        const int4 e = __ldg(reinterpret_cast<const int4*>(g.hash) + h);
-        const unsigned long long k = (unsigned long long)(unsigned)e.x | ((unsigned long long)(unsigned)e.y << 32);
-        if (k == key) return make_int2(e.z, e.w);
-        if (k == kEmptyKey) return make_int2(0, 0);
-        h = (h + 1) & g.hmask;
-    }
+    return hash_find(g, cell_key(cx, cy, cz));
 }
 
 // The fp32 squared distance in the fixed order (reading R9):

@@ -19,6 +19,10 @@
 
 #include "gicp_internal.cuh"
 
+#ifndef GICP_AUTO_OCC
+#define GICP_AUTO_OCC 8.0  // target point-weighted voxel occupancy of the automatic cell
+#endif
+
 namespace gicp {
 namespace {
 
@@ -188,11 +192,10 @@ __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__
 // non-empty voxels among the 27 around it, nearest-first, as (start, end) ranges
 // of pts packed with the offset code (adj_pack, gicp_internal.cuh). A query in an
 // occupied voxel reads this shared list instead of probing the hash 27 times.
-__device__ __constant__ signed char c_adj_order[27][3] = {
-    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
-    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
-    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
-    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+// nearest-first neighbour order (own, 6 faces, 12 edges, 8 corners):
+//   (0,0,0) (-1,0,0) (1,0,0) (0,-1,0) (0,1,0) (0,0,-1) (0,0,1) (-1,-1,0) (1,-1,0)
+//   (-1,1,0) (1,1,0) (-1,0,-1) (1,0,-1) (-1,0,1) (1,0,1) (0,-1,-1) (0,1,-1) (0,-1,1)
+//   (0,1,1) (-1,-1,-1) (1,-1,-1) (-1,1,-1) (1,1,-1) (-1,-1,1) (1,-1,1) (-1,1,1) (1,1,1)
 
 __device__ __forceinline__ unsigned compact3(unsigned long long v) {
     v &= 0x1249249249249249ull;
@@ -206,39 +209,66 @@ __device__ __forceinline__ unsigned compact3(unsigned long long v) {
 
 // one warp per occupied level-0 voxel (compact head list): lane c < 27 probes
 // neighbour c (27 independent probes in flight per warp); the non-empty ones are
-// compacted in nearest-first order with a ballot and appended at an atomically
-// reserved offset (the list ORDER in memory is scheduling-dependent, the list of
-// every voxel is not); (offset, count) is stored at the voxel's first point.
-__global__ void k_adjacency(Grid g, const unsigned long long* __restrict__ keys, const int* __restrict__ heads,
-                            const int* __restrict__ nheads, int* __restrict__ total, int2* __restrict__ oc,
-                            int2* __restrict__ rng_out) {
+// compacted in nearest-first order with a ballot and appended at an offset the
+// BLOCK reserves with one atomic (a single global counter hit once per warp
+// serialises at the L2: ~0.5 ns per atomic x 2.6e5 voxels); the list ORDER in
+// memory is scheduling-dependent, the list of every voxel is not; (offset,
+// count) is stored at the voxel's first point.
+constexpr int kAdjBlock = 256;
+__global__ void __launch_bounds__(kAdjBlock) k_adjacency(Grid g, const unsigned long long* __restrict__ keys,
+                                                          const int* __restrict__ heads, const int* __restrict__ nheads,
+                                                          int* __restrict__ total, int2* __restrict__ oc,
+                                                          int2* __restrict__ rng_out) {
+    __shared__ int wcnt[kAdjBlock / 32];
+    __shared__ int bbase;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= *nheads) return;  // warp-uniform
-    const int head = heads[w];
-    const unsigned long long key = keys[head];
-    const int cx = (int)compact3(key), cy = (int)compact3(key >> 1), cz = (int)compact3(key >> 2);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool valid = w < *nheads;  // warp-uniform; every warp reaches the barriers
+    // lane c < 27 takes neighbour c of the nearest-first order above, read
+    // from three packed immediates (6-bit codes adj_pack uses) -- a per-lane index
+    // into __constant__ memory would serialise 27 ways
+    const unsigned long long W = lane < 10 ? 0x612425159456515ull : (lane < 20 ? 0x2984906690611aull : 0x2aa2280a202ull);
+    const unsigned code = (unsigned)(W >> (6 * (lane % 10))) & 63u;
+    const int dx = (int)(code & 3u) - 1, dy = (int)((code >> 2) & 3u) - 1, dz = (int)((code >> 4) & 3u) - 1;
+    int head = 0;
     int2 r = make_int2(0, 0);
-    int dx = 0, dy = 0, dz = 0;
-    if (lane < 27) {
-        dx = c_adj_order[lane][0];
-        dy = c_adj_order[lane][1];
-        dz = c_adj_order[lane][2];
-        r = cell_lookup(g, cx + dx, cy + dy, cz + dz);
+    if (valid && lane < 27) {
+        head = heads[w];
+        // neighbour key by dilated-integer increments of the voxel's Morton key; a
+        // step off the grid yields a key no voxel has (empty lookup)
+        const unsigned long long key = keys[head];
+        const unsigned long long MX = 0x1249249249249249ull, MY = MX << 1, MZ = MX << 2;
+        auto step = [](unsigned long long k, unsigned long long M, int d) {
+            return d < 0 ? ((k - 1ull) & M) : (d > 0 ? (((k | ~M) + 1ull) & M) : k);
+        };
+        const unsigned long long nk = step(key & MX, MX, dx) | step(key & MY, MY, dy) | step(key & MZ, MZ, dz);
+        r = hash_find(g, nk);
+    } else if (valid) {
+        head = heads[w];
     }
     const bool ne = lane < 27 && r.y > r.x;
     const unsigned mask = __ballot_sync(0xffffffffu, ne);
     const int cnt = __popc(mask);
-    int base = 0;
-    if (lane == 0) base = atomicAdd(total, cnt);
-    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane == 0) wcnt[wid] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < kAdjBlock / 32; ++i) {
+            const int c = wcnt[i];
+            wcnt[i] = t;
+            t += c;
+        }
+        bbase = t > 0 ? atomicAdd(total, t) : 0;
+    }
+    __syncthreads();
+    const int base = bbase + wcnt[wid];
     if (ne) {
         const int o = base + __popc(mask & ((1u << lane) - 1));
         const int c = r.y - r.x;
         if (c > kAdjMaxCount) atomicOr(total + 1, 1);  // count does not fit the packing: no lists
         rng_out[o] = make_int2(r.x, (int)adj_pack(c, dx, dy, dz));
     }
-    if (lane == 0) oc[head] = make_int2(base, cnt);
+    if (valid && lane == 0) oc[head] = make_int2(base, cnt);
 }
 
 __global__ void k_fill_hash(HashEntry* H, int64_t cap) {
@@ -290,7 +320,7 @@ int make_grid(const float mn[3], const float mx[3], float cell, Grid* g) {
         volatile float d = mx[a] - mn[a];
         volatile float t = d * g->inv_cell;
         double c = std::floor((double)t);
-        if (!(c + 1 <= kMaxAxisCells))
+        if (!(c + 1 < kMaxAxisCells))  // < 2^21: a +1 step off the grid never wraps the Morton key
             return set_error(GICP_ERANGE, "voxel grid exceeds 2^21 cells on an axis; increase cell_size");
         dims[a] = (int)c + 1;
     }
@@ -376,7 +406,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if ((rc = check_cuda(cudaStreamSynchronize(s), "auto cell"))) return rc;
         // point-weighted mean voxel occupancy at the trial cell; aim at ~12
         const double med = std::max(1.0, (double)sum2 / (double)n) / 1.5;
-        cell_size = (float)(trial * std::sqrt(8.0 / med));
+        cell_size = (float)(trial * std::sqrt(GICP_AUTO_OCC / med));
         if (!(cell_size > 0.0f) || !std::isfinite(cell_size)) cell_size = 1.0f;
     }
     if ((rc = make_grid(mn, mx, cell_size, &g))) return rc;
@@ -461,7 +491,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if ((rc = alloc_async(tot, 16, s))) return fail(rc);
         if ((rc = check_cuda(cudaMemsetAsync(tot.p, 0, 16, s), "memset"))) return fail(rc);
         const int64_t threads = (int64_t)std::max(counts[0], 1) * 32;
-        k_adjacency<<<grid_for(threads, 256), 256, 0, s>>>(idx->lv[0], (unsigned long long*)keys.p, heads, nheads,
+        k_adjacency<<<grid_for(threads, kAdjBlock), kAdjBlock, 0, s>>>(idx->lv[0], (unsigned long long*)keys.p, heads, nheads,
                                                             (int*)tot.p, idx->adj_oc, idx->adj_rng);
         idx->device_bytes += n * 8 + ub * 8;
         if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);

@@ -248,7 +248,6 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
         const bool okx[3] = {G.cx - 1 >= 0 && G.cx - 1 < g.nx, G.cx >= 0 && G.cx < g.nx, G.cx + 1 >= 0 && G.cx + 1 < g.nx};
         const bool oky[3] = {G.cy - 1 >= 0 && G.cy - 1 < g.ny, G.cy >= 0 && G.cy < g.ny, G.cy + 1 >= 0 && G.cy + 1 < g.ny};
         const bool okz[3] = {G.cz - 1 >= 0 && G.cz - 1 < g.nz, G.cz >= 0 && G.cz < g.nz, G.cz + 1 >= 0 && G.cz + 1 < g.nz};
-        const int4* __restrict__ Hh = reinterpret_cast<const int4*>(g.hash);
 #pragma unroll
         for (int c = 0; c < 27; ++c) {
             // nearest-first order: own, faces, edges, corners (same table as c_off27)
@@ -260,15 +259,9 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
             const int ix = off[c][0] + 1, iy = off[c][1] + 1, iz = off[c][2] + 1;
             if (!(okx[ix] && oky[iy] && okz[iz])) continue;
             const unsigned long long key = kxs[ix] | kys[iy] | kzs[iz];
-            unsigned long long h = hash_slot(g, key);
-            int4 e = __ldg(Hh + h);
-            while (((unsigned long long)(unsigned)e.x | ((unsigned long long)(unsigned)e.y << 32)) != key &&
-                   !(e.x == -1 && e.y == -1)) {
-                h = (h + 1) & g.hmask;
-                e = __ldg(Hh + h);
-            }
-            if (e.x == -1 && e.y == -1) continue;  // empty slot: voxel not occupied
-            rl[nr] = make_int2(e.z, e.w);
+            const int2 e = hash_find(g, key);
+            if (e.y <= e.x) continue;  // voxel not occupied
+            rl[nr] = e;
             lbl[nr] = __fmaf_rn(gzs[iz], gzs[iz], __fmaf_rn(gys[iy], gys[iy], gxs[ix] * gxs[ix]));
             ++nr;
         }
@@ -769,12 +762,12 @@ __global__ void __launch_bounds__(kBFBlock) k_knn_bruteforce(QuerySrc src, const
     }
 }
 
-__global__ void k_query_keys(const float* __restrict__ q, int64_t m, Grid g, unsigned long long* __restrict__ keys,
-                             int* __restrict__ vals) {
+__global__ void k_query_keys(const float* __restrict__ q, int64_t m, Grid g, unsigned long long empty,
+                             unsigned long long* __restrict__ keys, int* __restrict__ vals) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= m) return;
     const float x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
-    unsigned long long key = kEmptyKey;
+    unsigned long long key = empty;  // non-finite queries last
     if (isfinite(x) && isfinite(y) && isfinite(z)) {
         const int cx = min(max(cell_coord(x, g.ox, g.inv_cell), 0), g.nx - 1);
         const int cy = min(max(cell_coord(y, g.oy, g.inv_cell), 0), g.ny - 1);
@@ -875,14 +868,23 @@ int run_ext(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* 
     if ((rc = keys_in.alloc(m * 8, s)) || (rc = keys_out.alloc(m * 8, s)) || (rc = vals_in.alloc(m * 4, s)) ||
         (rc = perm.alloc(m * 4, s)))
         return rc;
-    k_query_keys<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(q, m, idx->lv[0], (unsigned long long*)keys_in.p,
+    // sort on the key bits in use (clamped voxel coordinates), not all 64
+    auto bits_for = [](int d) {
+        int b = 0;
+        while ((1 << b) < d) ++b;
+        return b;
+    };
+    const Grid& g0 = idx->lv[0];
+    const int bits = std::max(1, 3 * std::max(bits_for(g0.nx), std::max(bits_for(g0.ny), bits_for(g0.nz))));
+    const unsigned long long empty = bits >= 64 ? kEmptyKey : (1ull << bits) - 1ull;
+    k_query_keys<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(q, m, g0, empty, (unsigned long long*)keys_in.p,
                                                               (int*)vals_in.p);
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned long long*)keys_in.p, (unsigned long long*)keys_out.p,
-                                    (int*)vals_in.p, (int*)perm.p, (int)m, 0, 64, s);
+                                    (int*)vals_in.p, (int*)perm.p, (int)m, 0, bits, s);
     if ((rc = temp.alloc(tb, s))) return rc;
     cub::DeviceRadixSort::SortPairs(temp.p, tb, (unsigned long long*)keys_in.p, (unsigned long long*)keys_out.p,
-                                    (int*)vals_in.p, (int*)perm.p, (int)m, 0, 64, s);
+                                    (int*)vals_in.p, (int*)perm.p, (int)m, 0, bits, s);
     return run_queries<KCAP>(idx, q, (int*)perm.p, m, k, 0.f, nbr, d2, nullptr, s);
 }
 

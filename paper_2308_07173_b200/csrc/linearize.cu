@@ -113,7 +113,6 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
             const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
             const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
-            const int4* __restrict__ Hh = reinterpret_cast<const int4*>(g.hash);
 #pragma unroll
             for (int c = 0; c < 27; ++c) {
                 constexpr signed char off[27][3] = {
@@ -129,15 +128,9 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                     __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
                 if (lb2 * kRel > r2) continue;  // beyond the gate: cannot hold an inlier
                 const unsigned long long key = cell_key(cx, cy, cz);
-                unsigned long long h = hash_slot(g, key);
-                int4 e = __ldg(Hh + h);
-                while (((unsigned long long)(unsigned)e.x | ((unsigned long long)(unsigned)e.y << 32)) != key &&
-                       !(e.x == -1 && e.y == -1)) {
-                    h = (h + 1) & g.hmask;
-                    e = __ldg(Hh + h);
-                }
-                if (e.x == -1 && e.y == -1) continue;
-                rl[nr] = make_int2(e.z, e.w);
+                const int2 e = hash_find(g, key);
+                if (e.y <= e.x) continue;
+                rl[nr] = e;
                 lbl[nr] = lb2;
                 ++nr;
             }

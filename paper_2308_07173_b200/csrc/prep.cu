@@ -30,8 +30,10 @@ __global__ void k_source_keys(const float* __restrict__ src, int64_t n, float in
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         float t = src[3 * i + a] * inv;
-        t = fminf(fmaxf(t, -1048575.0f), 1048575.0f);  // 21-bit range around the frame origin
-        c[a] = (unsigned)((int)floorf(t) + (1 << 20));
+        // 10 bits per axis around the frame origin (+-512 cells; the order only
+        // serves locality, so clamping far points costs locality, never results)
+        t = fminf(fmaxf(t, -512.0f), 511.0f);
+        c[a] = (unsigned)((int)floorf(t) + 512);
     }
     keys[i] = cell_key((int)c[0], (int)c[1], (int)c[2]);
     vals[i] = (int)i;
@@ -70,7 +72,7 @@ int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, 
     void* buf = nullptr;
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                    (int*)nullptr, (int*)nullptr, (int)ns, 0, 63, s);
+                                    (int*)nullptr, (int*)nullptr, (int)ns, 0, 30, s);
     const size_t bytes = ns * (8 + 8 + 4 + 4) + tb + 64;
     if (cudaMallocAsync(&buf, bytes, s) != cudaSuccess) {
         cudaGetLastError();
@@ -83,7 +85,7 @@ int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, 
     void* temp = (void*)(((uintptr_t)(v_out + ns) + 15) & ~(uintptr_t)15);
     const unsigned g = (unsigned)((ns + 255) / 256);
     k_source_keys<<<g, 256, 0, s>>>(src, ns, 1.0f / cell, k_in, v_in);
-    cub::DeviceRadixSort::SortPairs(temp, tb, k_in, k_out, v_in, v_out, (int)ns, 0, 63, s);
+    cub::DeviceRadixSort::SortPairs(temp, tb, k_in, k_out, v_in, v_out, (int)ns, 0, 30, s);
     k_gather_source<<<g, 256, 0, s>>>(src, src_cov, v_out, ns, src_p, cov_p);
     const int rc = check_cuda(cudaGetLastError(), "source sort");
     cudaFreeAsync(buf, s);
