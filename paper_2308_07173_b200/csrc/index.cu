@@ -63,13 +63,29 @@ __global__ void k_bbox(const float* __restrict__ xyz, int64_t n, int* __restrict
         }
         bad |= __shfl_xor_sync(0xffffffffu, bad, off);
     }
+    // block reduce, then one set of atomics per block (same-address atomics from
+    // every warp would serialise at the L2)
+    __shared__ int sh[32][7];
+    const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            atomicMin(out + a, mn[a]);
-            atomicMax(out + 3 + a, mx[a]);
+            sh[wid][a] = mn[a];
+            sh[wid][3 + a] = mx[a];
         }
-        if (bad) atomicAdd(out + 6, 1);
+        sh[wid][6] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x < 7) {
+        const int c = threadIdx.x;
+        int v = sh[0][c];
+        for (int w = 1; w < nw; ++w) v = c < 3 ? min(v, sh[w][c]) : (c < 6 ? max(v, sh[w][c]) : (v | sh[w][c]));
+        if (c < 3)
+            atomicMin(out + c, v);
+        else if (c < 6)
+            atomicMax(out + c, v);
+        else if (v)
+            atomicAdd(out + 6, 1);
     }
 }
 
@@ -196,16 +212,6 @@ __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__
 //   (0,0,0) (-1,0,0) (1,0,0) (0,-1,0) (0,1,0) (0,0,-1) (0,0,1) (-1,-1,0) (1,-1,0)
 //   (-1,1,0) (1,1,0) (-1,0,-1) (1,0,-1) (-1,0,1) (1,0,1) (0,-1,-1) (0,1,-1) (0,-1,1)
 //   (0,1,1) (-1,-1,-1) (1,-1,-1) (-1,1,-1) (1,1,-1) (-1,-1,1) (1,-1,1) (-1,1,1) (1,1,1)
-
-__device__ __forceinline__ unsigned compact3(unsigned long long v) {
-    v &= 0x1249249249249249ull;
-    v = (v ^ (v >> 2)) & 0x10c30c30c30c30c3ull;
-    v = (v ^ (v >> 4)) & 0x100f00f00f00f00full;
-    v = (v ^ (v >> 8)) & 0x1f0000ff0000ffull;
-    v = (v ^ (v >> 16)) & 0x1f00000000ffffull;
-    v = (v ^ (v >> 32)) & 0x1fffffull;
-    return (unsigned)v;
-}
 
 // one warp per occupied level-0 voxel (compact head list): lane c < 27 probes
 // neighbour c (27 independent probes in flight per warp); the non-empty ones are

@@ -62,14 +62,6 @@ __device__ __forceinline__ void topk_insert(unsigned long long (&L)[KCAP], unsig
     L[0] = below ? x : L[0];
 }
 
-// compare-and-swap on the d2 bits (high word); ties are handled by the callers
-__device__ __forceinline__ void cas_hi(unsigned long long& a, unsigned long long& b) {
-    const bool sw = hi32(b) < hi32(a);
-    const unsigned long long lo = sw ? b : a;
-    b = sw ? a : b;
-    a = lo;
-}
-
 // Batcher odd-even merge sort network on N register keys. The comparator list is
 // generated at compile time (constexpr) so every register index is a constant
 // after unrolling. N = 20 -> 103 comparators.

@@ -33,7 +33,8 @@ constexpr int kMaxRing = 16;
 #define GICP_LIN_PROF 0  // diagnostics build: search stage counts and warp-duration histogram
 #endif
 #if GICP_LIN_PROF
-__device__ unsigned long long g_lprof[40];  // [0..3] stage counts, [4] max warp cycles, [8..39] log2 histogram
+__device__ unsigned long long g_lprof[80];  // [0..3] stage counts, [4] max search cycles, [5] sum search, [6] sum total,
+                                            // [7] max total, [8..39] log2 hist search, [40..71] log2 hist total
 #define LPROF(x) x
 #else
 #define LPROF(x)
@@ -67,23 +68,25 @@ struct Levels {
 // unsearched point below min(best, r2)) does not settle continue per lane:
 // coarser levels up to `ring_level`, then ring expansion there.
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
-                                          float qy, float qz, float r2, unsigned long long& best, float3& bp, int& bj,
+                                          float qy, float qz, float r2, unsigned long long& best, int& bj,
                                           int& overflow) {
-    best = kEmptyKey;
+    // the key (d2 bits << 32 | original index) is kept as two words: the common
+    // case (d2 larger) is one 32-bit compare, and only the sorted position of the
+    // winner is tracked (its coordinates are loaded once, by the caller)
+    unsigned bh = 0xffffffffu, bo = 0xffffffffu;
     overflow = 0;
     bj = -1;
-    bp = make_float3(0.f, 0.f, 0.f);
-    auto bound = [&]() { return fminf(__uint_as_float((unsigned)(best >> 32)), r2); };
+    auto bound = [&]() { return fminf(__uint_as_float(bh), r2); };
     auto consider_p = [&](int j, const float4 p) {
-        const float d2 = dist2(qx, qy, qz, p.x, p.y, p.z);
-        const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
-        if (key < best) {
-            best = key;
-            bp = make_float3(p.x, p.y, p.z);
-            bj = j;
-        }
+        const unsigned h = __float_as_uint(dist2(qx, qy, qz, p.x, p.y, p.z));
+        const unsigned o = __float_as_uint(p.w);
+        const bool better = h < bh || (h == bh && o < bo);
+        bh = better ? h : bh;
+        bo = better ? o : bo;
+        bj = better ? j : bj;
     };
     auto consider = [&](int j) { consider_p(j, __ldg(pts + j)); };
+    auto finish = [&]() { best = ((unsigned long long)bh << 32) | bo; };
     auto scan = [&](int2 rng) {
         for (int j = rng.x; j < rng.y; ++j) consider(j);
     };
@@ -172,10 +175,13 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                     if (j + u < len) consider_p(r.x + j + u, pv[u]);
             }
         }
-        if (!active) return;
+        if (!active) { finish(); return; }
         const float m = cube_margin(G, s, slack, 1);
-        if (m > 0.0f && bound() < m * m * kRel) return;
-        if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) return;
+        if (m > 0.0f && bound() < m * m * kRel) { finish(); return; }
+        if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) {
+            finish();
+            return;
+        }
     }
     // (2) per lane: coarser levels' cubes up to ring_level, then rings there
     LPROF(atomicAdd(&g_lprof[1], 1ull);)
@@ -192,8 +198,11 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                     scan(cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz));
                 }
         const float m = cube_margin(G, s, slack, 1);
-        if (m > 0.0f && bound() < m * m * kRel) return;
-        if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) return;
+        if (m > 0.0f && bound() < m * m * kRel) { finish(); return; }
+        if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) {
+            finish();
+            return;
+        }
     }
     {
         const Grid& g = lvs.lv[lvs.ring_level];
@@ -207,7 +216,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             if (R > max(R0, 1) + kMaxRing) {
                 LPROF(atomicAdd(&g_lprof[3], 1ull);)
                 overflow = 1;
-                return;
+                { finish(); return; }
             }
             const int z0 = max(-R, -G.cz), z1 = min(R, g.nz - 1 - G.cz);
             const int y0 = max(-R, -G.cy), y1 = min(R, g.ny - 1 - G.cy);
@@ -232,17 +241,18 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 }
             }
             const float mR = cube_margin(G, s, slack, R);
-            if (mR > 0.0f && bound() < mR * mR * kRel) return;
+            if (mR > 0.0f && bound() < mR * mR * kRel) { finish(); return; }
             if (G.cx - R <= 0 && G.cx + R >= g.nx - 1 && G.cy - R <= 0 && G.cy + R >= g.ny - 1 && G.cz - R <= 0 &&
                 G.cz + R >= g.nz - 1)
-                return;
+                { finish(); return; }
         }
     }
+    finish();
 }
 
 // brute-force fallback for overflowed searches (the caller handles one point)
 __device__ __forceinline__ void nn_bruteforce(const float4* __restrict__ pts, int64_t n, float qx, float qy, float qz,
-                                              unsigned long long& best, float3& bp, int& bj) {
+                                              unsigned long long& best, int& bj) {
     best = kEmptyKey;
     for (int64_t j = 0; j < n; ++j) {
         const float4 p = __ldg(pts + j);
@@ -250,7 +260,6 @@ __device__ __forceinline__ void nn_bruteforce(const float4* __restrict__ pts, in
         const unsigned long long key = ((unsigned long long)__float_as_uint(d2) << 32) | __float_as_uint(p.w);
         if (key < best) {
             best = key;
-            bp = make_float3(p.x, p.y, p.z);
             bj = (int)j;
         }
     }
@@ -363,6 +372,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                                                          int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
                                                          double* __restrict__ partials, unsigned* __restrict__ done,
                                                          double* __restrict__ out29) {
+    LPROF(const long long tk0 = clock64();)
     double acc[kNumAcc];
 #pragma unroll
     for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
@@ -398,29 +408,32 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         } else {
             const float sx = (float)pp[0], sy = (float)pp[1], sz = (float)pp[2];
             unsigned long long best;
-            float3 bp;
             int bj, ovf;
             LPROF(const long long t0 = clock64();)
-            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bp, bj, ovf);
+            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bj, ovf);
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
                 if ((threadIdx.x & 31) == 0) {
                     atomicAdd(&g_lprof[0], 1ull);
+                    atomicAdd(&g_lprof[5], (unsigned long long)mx);
                     atomicMax(&g_lprof[4], (unsigned long long)mx);
                     atomicAdd(&g_lprof[8 + min(31, 31 - __clz(mx | 1))], 1ull);
                 }
             })
             if (active) {
-                if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bp, bj);
+                if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bj);
                 const float bd2 = __uint_as_float((unsigned)(best >> 32));
                 const bool inl = best != kEmptyKey && bd2 < r2;
                 orig = inl ? (int)(best & 0xffffffffu) : -1;
                 spos = inl ? bj : -1;
                 if (corr) corr[i] = SPOS ? spos : orig;
-                qx = bp.x;
-                qy = bp.y;
-                qz = bp.z;
+                if (inl) {
+                    const float4 q = __ldg(pts + bj);
+                    qx = q.x;
+                    qy = q.y;
+                    qz = q.z;
+                }
             }
         }
         if (!active) continue;
@@ -448,6 +461,15 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         accumulate_point<ERROR_ONLY>(P, pp, qx, qy, qz, cp, cq, acc);
         cnt += 1.0;
     }
+    LPROF({
+        const unsigned dt = (unsigned)min(clock64() - tk0, 0xffffffffll);
+        const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&g_lprof[6], (unsigned long long)mx);
+            atomicMax(&g_lprof[7], (unsigned long long)mx);
+            atomicAdd(&g_lprof[40 + min(31, 31 - __clz(mx | 1))], 1ull);
+        }
+    })
     // warp tree
     constexpr int NV = DUAL ? kNV : kNumAcc + 1;
     __shared__ double sh[kLinBlock / 32][kNV];
@@ -618,13 +640,17 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     if (scratch) cudaFreeAsync(scratch, s);
 #if GICP_LIN_PROF
     if (getenv("GICP_DEBUG_STATS")) {
-        unsigned long long h[40];
+        unsigned long long h[80];
         cudaStreamSynchronize(s);
         cudaMemcpyFromSymbol(h, g_lprof, sizeof(h));
-        fprintf(stderr, "[gicp lin prof] warps=%llu fallback=%llu rings=%llu overflow=%llu max-warp-cycles=%llu hist:",
-                h[0], h[1], h[2], h[3], h[4]);
+        const double w = h[0] ? (double)h[0] : 1.0;
+        fprintf(stderr, "[gicp lin prof] warps=%llu fallback=%llu rings=%llu overflow=%llu search avg %.0f max %llu | "
+                "total avg %.0f max %llu\n   search hist:", h[0], h[1], h[2], h[3], h[5] / w, h[4], h[6] / w, h[7]);
         for (int b = 8; b < 40; ++b)
             if (h[b]) fprintf(stderr, " 2^%d:%llu", b - 8, h[b]);
+        fprintf(stderr, "\n   total hist:");
+        for (int b = 40; b < 72; ++b)
+            if (h[b]) fprintf(stderr, " 2^%d:%llu", b - 40, h[b]);
         fprintf(stderr, "\n");
         for (auto& x : h) x = 0;
         cudaMemcpyToSymbol(g_lprof, h, sizeof(h));
