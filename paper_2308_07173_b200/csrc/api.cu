@@ -2,6 +2,7 @@
 // argument validation, thread-local errors, and the host LM loop of gicp_align.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -131,13 +132,56 @@ bool ldlt6(const double A[36], const double y[6], double x[6]) {
     return true;
 }
 
-double* pinned29() {
-    static thread_local double* p = nullptr;
-    if (!p && cudaMallocHost(&p, 64 * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        p = nullptr;
+// Host-mapped result block of gicp_align (per host thread): the last block of a
+// linearize launch writes out29 straight into it and then a sequence number to
+// `flag`; the host spins on the flag instead of a D2H copy + stream sync.
+struct MappedOut {
+    double* h = nullptr;             // host view: 32 doubles, then the flag
+    double* d = nullptr;             // device view of the same memory
+    volatile unsigned* flag = nullptr;
+    volatile unsigned* dflag = nullptr;
+    unsigned seq = 0;
+};
+MappedOut* mapped_out() {
+    static thread_local MappedOut m;
+    if (!m.h) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, 64 * sizeof(double), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, p, 0) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFreeHost(p);
+            return nullptr;
+        }
+        std::memset(p, 0, 64 * sizeof(double));
+        m.h = (double*)p;
+        m.d = (double*)dp;
+        m.flag = (volatile unsigned*)(m.h + 32);
+        m.dflag = (volatile unsigned*)(m.d + 32);
     }
-    return p;
+    return &m;
+}
+
+// wait for the launch that signals `seq`; polls the stream now and then so a
+// failed launch is reported instead of spinning forever
+int wait_mapped(MappedOut* m, unsigned seq, cudaStream_t s) {
+    for (unsigned long it = 1;; ++it) {
+        if (*m->flag == seq) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            return GICP_OK;
+        }
+        if ((it & 255) == 0) {
+            const cudaError_t e = cudaStreamQuery(s);
+            if (e == cudaSuccess) {
+                if (*m->flag == seq) continue;
+                return set_error(GICP_ECUDA, "gicp_align: linearize finished without its completion signal");
+            }
+            if (e != cudaErrorNotReady) return check_cuda(e, "gicp_align");
+        }
+    }
 }
 
 }  // namespace
@@ -273,8 +317,9 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     if (!finite_T(T0)) return set_error(GICP_EINVAL, "gicp_align: non-finite T0");
     init_pool_once();
     cudaStream_t s = (cudaStream_t)stream;
-    double* h = pinned29();
-    if (!h) return set_error(GICP_ENOMEM, "gicp_align: pinned buffer");
+    MappedOut* mo = mapped_out();
+    if (!mo) return set_error(GICP_ENOMEM, "gicp_align: host-mapped buffer");
+    const double* h = mo->h;
     // one scratch block for the whole alignment: out (31 doubles) | done counter |
     // block partials | two correspondence buffers | Morton-sorted copies of the
     // source and its covariances
@@ -286,7 +331,6 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         cudaGetLastError();
         return set_error(GICP_ENOMEM, "gicp_align: scratch allocation failed");
     }
-    double* d_out = (double*)scratch;
     LinScratch ls;
     ls.done = (unsigned*)(scratch + 256);
     ls.partials = (double*)(scratch + 512);
@@ -302,13 +346,15 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     }
     // one launch + one sync per evaluation: `old` != nullptr also evaluates the
     // trial cost with the previous correspondences (values 29, 30)
+    ls.flag = mo->dflag;
+    auto go = [&](const double* T, const double* piv, int flags, int32_t* corr, const int32_t* old) -> int {
+        ls.seq = ++mo->seq;
+        const int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, flags, mo->d,
+                                        corr, s, &ls, old);
+        return rc ? rc : wait_mapped(mo, ls.seq, s);
+    };
     auto lin = [&](const double* T, const double* piv, int32_t* corr, const int32_t* old) -> int {
-        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, kLinCorrSpos, d_out,
-                                  corr, s, &ls, old);
-        if (rc) return rc;
-        if ((rc = check_cuda(cudaMemcpyAsync(h, d_out, 31 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
-            return rc;
-        return check_cuda(cudaStreamSynchronize(s), "align sync");
+        return go(T, piv, kLinCorrSpos, corr, old);
     };
     const bool debug = getenv("GICP_DEBUG_ALIGN") != nullptr;
     double T[16];
@@ -374,16 +420,10 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 if (spec) {
                     if ((rc = lin(Tn, pn, corr_b, corr_a))) break;
                 } else {
-                    rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, Tn, pn, prm->max_corr_dist,
-                                          kLinCorrSpos | GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY, d_out, corr_a, s,
-                                          &ls);
-                    if (!rc) rc = check_cuda(cudaMemcpyAsync(h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s),
-                                             "D2H");
-                    if (!rc) rc = check_cuda(cudaStreamSynchronize(s), "align sync");
-                    if (rc) break;
-                    h[29] = h[27];
+                    if ((rc = go(Tn, pn, kLinCorrSpos | GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY, corr_a, nullptr)))
+                        break;
                 }
-                const double en = h[29];
+                const double en = spec ? h[29] : h[27];
                 double den = 0.0;
                 for (int a = 0; a < 6; ++a) den += delta[a] * (lambda * delta[a] - b[a]);
                 const double rho = (e - en) / den;

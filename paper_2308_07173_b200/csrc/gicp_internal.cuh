@@ -204,6 +204,10 @@ __device__ __forceinline__ int2 adj_range(int2 e) { return make_int2(e.x, e.x + 
 struct LinScratch {
     unsigned* done;
     double* partials;
+    // optional completion signal (gicp_align): after out29 is written, the last
+    // block stores `seq` to *flag (host-mapped memory) so the host can spin on it
+    volatile unsigned* flag = nullptr;
+    unsigned seq = 0;
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
 size_t linearize_scratch_bytes(int64_t ns);

@@ -371,7 +371,8 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                                                          const float4* __restrict__ tgt_cov_sorted, Pose P, float r2,
                                                          int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
                                                          double* __restrict__ partials, unsigned* __restrict__ done,
-                                                         double* __restrict__ out29) {
+                                                         double* __restrict__ out29, volatile unsigned* flag,
+                                                         unsigned seq) {
     LPROF(const long long tk0 = clock64();)
     double acc[kNumAcc];
 #pragma unroll
@@ -538,6 +539,11 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         for (int sub = 0; sub < kSub; ++sub) v += part[sub][c];
         out29[c] = v;
     }
+    if (flag) {  // out29 may be host-mapped: make it visible before the signal
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) *flag = seq;
+    }
     if (threadIdx.x == 0) *done = 0u;
 }
 
@@ -581,6 +587,8 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     void* scratch = nullptr;
     unsigned* done;
     double* partials;
+    volatile unsigned* flag = pre ? pre->flag : nullptr;
+    const unsigned seq = pre ? pre->seq : 0u;
     if (pre) {
         done = pre->done;
         partials = pre->partials;
@@ -606,7 +614,7 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
     const bool dual = corr_old != nullptr && !reuse && !eonly;
 #define GICP_LIN_ARGS                                                                                            \
     src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
-        done, out29
+        done, out29, flag, seq
 #define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_RE(S, SP)           \
