@@ -207,6 +207,37 @@ int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp_index tg
                const double T0[16] /* host */, const gicp_align_params* params /* host */,
                gicp_align_result* result /* host */, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Batched registration (many scans against one map).
+ * B registrations with concatenated sources: registration b owns source points
+ * [offsets[b], offsets[b+1]) of src / src_cov (device) and corr; offsets is a
+ * host int64 [B+1] array with offsets[0] = 0, non-decreasing.
+ *
+ * gicp_linearize_batched -- gicp_linearize for every registration in ONE launch:
+ *   T (host) fp64 [B][16], pivots (host) fp64 [B][3] or NULL (origins),
+ *   out29 (device) fp64 [B][29] (row b = registration b; zero for an empty
+ *   one). Each registration is partitioned and reduced exactly as a single
+ *   gicp_linearize over its own points, so row b is bitwise the single result.
+ *   Flags and errors as gicp_linearize. Asynchronous (stream-ordered).
+ *
+ * gicp_align_batched -- gicp_align for every registration, in lockstep: each
+ *   evaluation round (initial linearisation, LM trials, re-linearisation) is one
+ *   batched launch over the registrations that need it. Per registration the
+ *   iterates are those of gicp_align on it alone (bitwise). T0 (host) [B][16],
+ *   result (host) [B]. A registration with < 6 correspondences stops (its
+ *   result holds the last pose and inlier count) and the call returns
+ *   GICP_EDEGENERATE after finishing the others. Synchronous.
+ * ------------------------------------------------------------------------- */
+int gicp_linearize_batched(const float* src, const float* src_cov, const int64_t* offsets /* host [B+1] */, int B,
+                           gicp_index tgt, const float* tgt_cov, const double* T /* host [B][16] */,
+                           const double* pivots /* host [B][3] or NULL */, float max_corr_dist, int flags,
+                           double* out29 /* device [B][29] */, int32_t* corr, void* stream);
+
+int gicp_align_batched(const float* src, const float* src_cov, const int64_t* offsets /* host [B+1] */, int B,
+                       gicp_index tgt, const float* tgt_cov, const double* T0 /* host [B][16] */,
+                       const gicp_align_params* params /* host */, gicp_align_result* result /* host [B] */,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

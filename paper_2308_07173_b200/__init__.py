@@ -64,10 +64,13 @@ _lib.gicp_knn_cov_self.argtypes = [_P, _i32, _f32, _P, _P, _P, _P]
 _lib.gicp_linearize.argtypes = [_P, _P, _i64, _P, _P, _P, _P, _f32, _i32, _P, _P, _P]
 _lib.gicp_align.argtypes = [_P, _P, _i64, _P, _P, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
                             _P]
+_lib.gicp_linearize_batched.argtypes = [_P, _P, _P, _i32, _P, _P, _P, _P, _f32, _i32, _P, _P, _P]
+_lib.gicp_align_batched.argtypes = [_P, _P, _P, _i32, _P, _P, _P, ctypes.POINTER(AlignParams), _P, _P]
 
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
            "gicp_index_attach_cov",
-           "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align"]
+           "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
+           "gicp_linearize_batched", "gicp_align_batched"]
 
 
 class GicpError(RuntimeError):
@@ -233,6 +236,57 @@ def align(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, tgt_cov: torch.T
                            _stream()))
     T = np.array(r.T[:], dtype=np.float64).reshape(4, 4)
     return T, AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers))
+
+
+def _offsets(offsets, total):
+    o = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64).reshape(-1))
+    if o.size < 2 or o[0] != 0 or o[-1] != total:
+        raise ValueError("offsets must be [0, ..., n_points] with B+1 entries")
+    return o
+
+
+def linearize_batched(src: torch.Tensor, src_cov: torch.Tensor, offsets, tgt: Index, tgt_cov: torch.Tensor, Ts,
+                      max_corr_dist=1.0, pivots=None, corr: torch.Tensor | None = None, reuse_corr: bool = False,
+                      error_only: bool = False, out=None):
+    """B registrations in one launch: registration b owns src[offsets[b]:offsets[b+1]].
+    Returns (out float64 device [B, 29], corr int32 device [n])."""
+    src = _pts(src, "src")
+    ns = src.shape[0]
+    o = _offsets(offsets, ns)
+    B = o.size - 1
+    Th = np.ascontiguousarray(np.asarray(Ts, dtype=np.float64).reshape(B, 16))
+    piv = None if pivots is None else np.ascontiguousarray(np.asarray(pivots, dtype=np.float64).reshape(B, 3))
+    out = out if out is not None else torch.empty((B, 29), dtype=torch.float64, device=src.device)
+    if corr is None:
+        if reuse_corr:
+            raise ValueError("reuse_corr needs corr")
+        corr = torch.empty(ns, dtype=torch.int32, device=src.device)
+    flags = (LIN_REUSE_CORR if reuse_corr else 0) | (LIN_ERROR_ONLY if error_only else 0)
+    _check(_lib.gicp_linearize_batched(_dptr(src), _dptr(src_cov.contiguous()), o.ctypes.data_as(_P), B, tgt.handle,
+                                       _dptr(tgt_cov.contiguous()), Th.ctypes.data_as(_P),
+                                       None if piv is None else piv.ctypes.data_as(_P), float(max_corr_dist), flags,
+                                       _dptr(out), _dptr(corr), _stream()))
+    return out, corr
+
+
+def align_batched(src: torch.Tensor, src_cov: torch.Tensor, offsets, tgt: Index, tgt_cov: torch.Tensor, T0s,
+                  max_iter=64, lm=True, rot_eps=1e-6, trans_eps=1e-5, max_corr_dist=1.0, allow_degenerate=False):
+    """Lockstep LM for B registrations. Returns (T [B,4,4] float64 numpy, [AlignInfo] * B).
+    With allow_degenerate, registrations with < 6 correspondences are reported
+    (inliers < 6) instead of raising."""
+    src = _pts(src, "src")
+    o = _offsets(offsets, src.shape[0])
+    B = o.size - 1
+    T0h = np.ascontiguousarray(np.asarray(T0s, dtype=np.float64).reshape(B, 16))
+    p = AlignParams(int(max_iter), int(bool(lm)), float(rot_eps), float(trans_eps), float(max_corr_dist))
+    res = (AlignResult * B)()
+    rc = _lib.gicp_align_batched(_dptr(src), _dptr(src_cov.contiguous()), o.ctypes.data_as(_P), B, tgt.handle,
+                                 _dptr(tgt_cov.contiguous()), T0h.ctypes.data_as(_P), ctypes.byref(p),
+                                 ctypes.cast(res, _P), _stream())
+    if not (allow_degenerate and rc == EDEGENERATE):
+        _check(rc)
+    Ts = np.array([np.array(r.T[:], dtype=np.float64).reshape(4, 4) for r in res])
+    return Ts, [AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers)) for r in res]
 
 
 def version() -> int:

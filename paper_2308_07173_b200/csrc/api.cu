@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "gicp_internal.cuh"
 
@@ -337,7 +339,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     int32_t* corr_a = (int32_t*)(scratch + 512 + lin_bytes);
     int32_t* corr_b = corr_a + nsa;
     float* src_p = (float*)(((uintptr_t)(corr_b + nsa) + 15) & ~(uintptr_t)15);
-    float* cov_p = src_p + 3 * nsa;
+    float* cov_p = (float*)(((uintptr_t)(src_p + 3 * nsa) + 15) & ~(uintptr_t)15);  // float2 loads
     int rc0 = check_cuda(cudaMemsetAsync(ls.done, 0, sizeof(unsigned), s), "memset");
     if (!rc0 && ns > 0) rc0 = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s);
     if (rc0) {
@@ -475,4 +477,410 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     res->error = err;
     res->inliers = inl;
     return rc;
+}
+
+// ---- batched registration -----------------------------
+// B registrations of concatenated sources against one target in one launch per
+// evaluation. Every registration is partitioned into 256-point blocks exactly as
+// a single launch over its own points and reduced in the same order, so each
+// result is bitwise the single-registration result (tests/test_gpu_parity.py).
+namespace gicp {
+namespace {
+
+struct BatchScratch {
+    char* base = nullptr;
+    int4* btab = nullptr;
+    int64_t* offs = nullptr;
+    Pose* poses = nullptr;
+    LinScratch ls;
+    int64_t nb = 0;
+};
+
+// device scratch: block table, offsets, poses, per-registration counters (+1 for
+// the launch), block partials; `extra` bytes appended (16-B aligned) for the caller
+int batch_scratch(const int64_t* offsets, int B, size_t extra, cudaStream_t s, BatchScratch& bs, char** extra_p) {
+    std::vector<int4> tab;
+    for (int b = 0; b < B; ++b) {
+        const int64_t n = offsets[b + 1] - offsets[b];
+        const int nbk = (int)((n + kLinPPB - 1) / kLinPPB);
+        for (int k = 0; k < nbk; ++k) tab.push_back(make_int4(b, k, nbk, 0));
+    }
+    bs.nb = (int64_t)tab.size();
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t o_tab = 0, o_offs = al(o_tab + tab.size() * sizeof(int4)), o_pose = al(o_offs + (B + 1) * 8),
+                 o_done = al(o_pose + (size_t)B * sizeof(Pose)), o_part = al(o_done + (B + 1) * sizeof(unsigned)),
+                 o_extra = al(o_part + linearize_partials_bytes(std::max<int64_t>(bs.nb, 1)));
+    if (cudaMallocAsync((void**)&bs.base, o_extra + extra, s) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(GICP_ENOMEM, "batched linearize: scratch allocation failed");
+    }
+    bs.btab = (int4*)(bs.base + o_tab);
+    bs.offs = (int64_t*)(bs.base + o_offs);
+    bs.poses = (Pose*)(bs.base + o_pose);
+    bs.ls.done = (unsigned*)(bs.base + o_done);
+    bs.ls.partials = (double*)(bs.base + o_part);
+    if (extra_p) *extra_p = bs.base + o_extra;
+    int rc = GICP_OK;
+    if (!tab.empty())
+        rc = check_cuda(cudaMemcpyAsync(bs.btab, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice, s),
+                        "H2D");
+    if (!rc) rc = check_cuda(cudaMemcpyAsync(bs.offs, offsets, (B + 1) * 8, cudaMemcpyHostToDevice, s), "H2D");
+    if (!rc) rc = check_cuda(cudaMemsetAsync(bs.ls.done, 0, (B + 1) * sizeof(unsigned), s), "memset");
+    // (pageable H2D copies return once the source is staged: the vector may go)
+    if (rc) {
+        cudaFreeAsync(bs.base, s);
+        bs.base = nullptr;
+    }
+    return rc;
+}
+
+int check_offsets(const int64_t* offsets, int B, const char* fn) {
+    if (!offsets || B < 1) return set_error(GICP_EINVAL, std::string(fn) + ": offsets / B");
+    if (offsets[0] != 0) return set_error(GICP_EINVAL, std::string(fn) + ": offsets[0] must be 0");
+    for (int b = 0; b < B; ++b)
+        if (offsets[b + 1] < offsets[b]) return set_error(GICP_EINVAL, std::string(fn) + ": offsets not ascending");
+    if (offsets[B] >= (1ll << 31) - 1) return set_error(GICP_EINVAL, std::string(fn) + ": too many points");
+    return GICP_OK;
+}
+
+// host-mapped block of a batched align: B result rows of 32 doubles, the flag,
+// and the pinned staging copy of the poses
+struct MappedBatch {
+    char* h = nullptr;
+    char* d = nullptr;
+    size_t cap = 0;
+};
+MappedBatch* mapped_batch(size_t bytes) {
+    static thread_local MappedBatch m;
+    if (m.cap < bytes) {
+        if (m.h) cudaFreeHost(m.h);
+        m = MappedBatch{};
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, p, 0) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFreeHost(p);
+            return nullptr;
+        }
+        std::memset(p, 0, bytes);
+        m.h = (char*)p;
+        m.d = (char*)dp;
+        m.cap = bytes;
+    }
+    return &m;
+}
+
+}  // namespace
+}  // namespace gicp
+
+GICP_API int gicp_linearize_batched(const float* src, const float* src_cov, const int64_t* offsets, int B,
+                                    gicp_index tgt, const float* tgt_cov, const double* T, const double* pivots,
+                                    float max_corr_dist, int flags, double* out29, int32_t* corr, void* stream) {
+    int rc;
+    if ((rc = check_offsets(offsets, B, "gicp_linearize_batched"))) return rc;
+    const int64_t ns = offsets[B];
+    if (!tgt || !tgt_cov || !T || !out29) return set_error(GICP_EINVAL, "gicp_linearize_batched: null pointer");
+    if (ns > 0 && (!src || !src_cov)) return set_error(GICP_EINVAL, "gicp_linearize_batched: null source");
+    if (!(max_corr_dist > 0.0f) || !std::isfinite(max_corr_dist))
+        return set_error(GICP_EINVAL, "gicp_linearize_batched: max_corr_dist must be finite and > 0");
+    if ((flags & GICP_LIN_REUSE_CORR) && !corr && ns > 0)
+        return set_error(GICP_EINVAL, "gicp_linearize_batched: REUSE_CORR needs corr");
+    if (flags & ~(GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY))
+        return set_error(GICP_EINVAL, "gicp_linearize_batched: flags");
+    for (int b = 0; b < B; ++b) {
+        if (!finite_T(T + 16 * b)) return set_error(GICP_EINVAL, "gicp_linearize_batched: non-finite T");
+        if (pivots && !(std::isfinite(pivots[3 * b]) && std::isfinite(pivots[3 * b + 1]) &&
+                        std::isfinite(pivots[3 * b + 2])))
+            return set_error(GICP_EINVAL, "gicp_linearize_batched: non-finite pivot");
+    }
+    init_pool_once();
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((rc = check_cuda(cudaMemsetAsync(out29, 0, (size_t)B * 29 * sizeof(double), s), "memset"))) return rc;
+    if (ns == 0) return GICP_OK;
+    BatchScratch bs;
+    if ((rc = batch_scratch(offsets, B, 0, s, bs, nullptr))) return rc;
+    std::vector<Pose> poses(B);
+    int n_active = 0;
+    for (int b = 0; b < B; ++b) {
+        poses[b] = make_pose(T + 16 * b, pivots ? pivots + 3 * b : nullptr);
+        poses[b].active = offsets[b + 1] > offsets[b];
+        n_active += poses[b].active;
+    }
+    rc = check_cuda(cudaMemcpyAsync(bs.poses, poses.data(), B * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
+    if (!rc) {
+        BatchView bv;
+        bv.btab = bs.btab;
+        bv.offs = bs.offs;
+        bv.poses = bs.poses;
+        bv.n_scans = B;
+        bv.n_active = n_active;
+        bv.out_stride = 29;
+        // one correspondence buffer: current = other = corr (cur = 0, both pointers equal)
+        rc = launch_linearize_core(src, src_cov, ns, tgt, tgt_cov, poses[0], max_corr_dist, flags, out29, corr, s,
+                                   bs.ls, corr, bv, bs.nb);
+    }
+    cudaFreeAsync(bs.base, s);
+    return rc;
+}
+
+// Lockstep LM over B registrations: the per-registration logic is gicp_align's,
+// step for step; each evaluation round is ONE batched launch over the
+// registrations that need it (the others' blocks exit at once).
+GICP_API int gicp_align_batched(const float* src, const float* src_cov, const int64_t* offsets, int B,
+                                gicp_index tgt, const float* tgt_cov, const double* T0,
+                                const gicp_align_params* prm, gicp_align_result* res, void* stream) {
+    int rc;
+    if ((rc = check_offsets(offsets, B, "gicp_align_batched"))) return rc;
+    const int64_t ns = offsets[B];
+    if (!tgt || !tgt_cov || !T0 || !prm || !res || (ns > 0 && (!src || !src_cov)))
+        return set_error(GICP_EINVAL, "gicp_align_batched: null pointer");
+    if (prm->max_iter < 1) return set_error(GICP_EINVAL, "gicp_align_batched: max_iter < 1");
+    for (int b = 0; b < B; ++b)
+        if (!finite_T(T0 + 16 * b)) return set_error(GICP_EINVAL, "gicp_align_batched: non-finite T0");
+    init_pool_once();
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nsa = ns > 0 ? ns : 1;
+    // device: batch scratch + two correspondence buffers + the sorted source copy
+    BatchScratch bs;
+    char* ex = nullptr;
+    if ((rc = batch_scratch(offsets, B, 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64, s, bs, &ex)))
+        return rc;
+    int32_t* corrA = (int32_t*)ex;
+    int32_t* corrB = corrA + nsa;
+    float* src_p = (float*)(((uintptr_t)(corrB + nsa) + 15) & ~(uintptr_t)15);
+    float* cov_p = (float*)(((uintptr_t)(src_p + 3 * nsa) + 15) & ~(uintptr_t)15);  // float2 loads
+    if (ns > 0 && (rc = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s, bs.offs, B))) {
+        cudaFreeAsync(bs.base, s);
+        return rc;
+    }
+    // host-mapped: rows [B][32] | flag | pinned pose staging [B]
+    const size_t rows = (size_t)B * 32 * sizeof(double);
+    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)B * sizeof(Pose));
+    if (!mb) {
+        cudaFreeAsync(bs.base, s);
+        return set_error(GICP_ENOMEM, "gicp_align_batched: host-mapped buffer");
+    }
+    const double* H = (const double*)mb->h;
+    double* Hd = (double*)mb->d;
+    volatile unsigned* hflag = (volatile unsigned*)(mb->h + rows);
+    Pose* pst = (Pose*)(mb->h + rows + 256);
+    static thread_local unsigned seq = 0;
+    MappedOut mo;  // wait_mapped view of the flag
+    mo.flag = hflag;
+    bs.ls.flag = (volatile unsigned*)(mb->d + rows);
+
+    struct St {
+        double T[16], piv[3], lin29[29], Tn[16], pn[3], delta[6], Hm[36], b[6];
+        double lambda = -1.0, nu = 2.0, err = 0.0, e = 0.0;
+        int it = 0, converged = 0, done = 0, cur = 0, rc = GICP_OK, inner_ok = 0, accepted = 0, relin = 0;
+        int64_t inl = 0;
+    };
+    std::vector<St> st(B);
+    for (int b = 0; b < B; ++b) {
+        std::memcpy(st[b].T, T0 + 16 * b, sizeof(st[b].T));
+        st[b].piv[0] = st[b].T[3];
+        st[b].piv[1] = st[b].T[7];
+        st[b].piv[2] = st[b].T[11];
+        if (offsets[b + 1] == offsets[b]) {  // no points: no correspondences
+            st[b].done = 1;
+            st[b].rc = GICP_EDEGENERATE;
+        }
+    }
+    // one evaluation round: `who` selects the registrations, pose(b) their pose;
+    // DUAL reads the current buffer as corr_old and writes the other one
+    auto round = [&](auto who, auto pose, int flags) -> int {
+        int n_active = 0;
+        for (int b = 0; b < B; ++b) {
+            const bool a = who(b);
+            const double* Tp;
+            const double* pp;
+            pose(b, Tp, pp);
+            pst[b] = make_pose(Tp, pp);
+            pst[b].active = a;
+            pst[b].cur = st[b].cur;
+            n_active += a;
+        }
+        if (n_active == 0) return GICP_OK;
+        int r = check_cuda(cudaMemcpyAsync(bs.poses, pst, B * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
+        if (r) return r;
+        BatchView bv;
+        bv.btab = bs.btab;
+        bv.offs = bs.offs;
+        bv.poses = bs.poses;
+        bv.n_scans = B;
+        bv.n_active = n_active;
+        bv.out_stride = 32;
+        bs.ls.seq = ++seq;
+        r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags, Hd, corrA, s,
+                                  bs.ls, corrB, bv, bs.nb);
+        return r ? r : wait_mapped(&mo, bs.ls.seq, s);
+    };
+    auto at_T = [&](int b, const double*& Tp, const double*& pp) {
+        Tp = st[b].T;
+        pp = st[b].piv;
+    };
+    auto at_Tn = [&](int b, const double*& Tp, const double*& pp) {
+        Tp = st[b].Tn;
+        pp = st[b].pn;
+    };
+    auto keep = [&](int b) {  // take a full linearisation row: the other buffer becomes current
+        std::memcpy(st[b].lin29, H + 32 * b, sizeof(st[b].lin29));
+        st[b].cur ^= 1;
+    };
+    // initial linearisation of every registration
+    rc = round([&](int b) { return !st[b].done; }, at_T, kLinCorrSpos);
+    for (int b = 0; b < B && !rc; ++b)
+        if (!st[b].done) keep(b);
+    for (int it = 1; !rc && it <= prm->max_iter; ++it) {
+        bool any = false;
+        for (int b = 0; b < B; ++b) {
+            St& q = st[b];
+            if (q.done) continue;
+            q.it = it;
+            q.inl = (int64_t)q.lin29[28];
+            if (q.inl < 6) {
+                q.rc = GICP_EDEGENERATE;
+                q.done = 1;
+                continue;
+            }
+            for (int a = 0, o = 0; a < 6; ++a)
+                for (int c = a; c < 6; ++c, ++o) q.Hm[6 * a + c] = q.Hm[6 * c + a] = q.lin29[o];
+            for (int a = 0; a < 6; ++a) q.b[a] = q.lin29[21 + a];
+            q.e = q.lin29[27];
+            q.err = q.e;
+            for (int a = 0; a < 6; ++a) q.delta[a] = 0.0;
+            q.accepted = 0;
+            q.relin = 0;
+            any = true;
+            if (!prm->lm) {
+                double nb[6];
+                for (int a = 0; a < 6; ++a) nb[a] = -q.b[a];
+                if (!ldlt6(q.Hm, nb, q.delta)) {
+                    q.rc = GICP_EDEGENERATE;
+                    q.done = 1;
+                    continue;
+                }
+                double E[16];
+                pivoted_exp(q.delta, q.piv, E);
+                mul44(E, q.T, q.T);
+            } else if (q.lambda < 0) {
+                double mx = 0.0;
+                for (int a = 0; a < 6; ++a) mx = std::fmax(mx, q.Hm[7 * a]);
+                q.lambda = 1e-9 * mx;
+            }
+        }
+        if (!any) break;
+        if (prm->lm) {
+            // inner trials in lockstep: round 0 is the speculative DUAL launch
+            for (int inner = 0; inner < 10 && !rc; ++inner) {
+                bool want = false;
+                for (int b = 0; b < B; ++b) {
+                    St& q = st[b];
+                    q.inner_ok = 0;
+                    if (q.done || q.accepted) continue;
+                    double Hl[36], nb[6];
+                    std::memcpy(Hl, q.Hm, sizeof(Hl));
+                    for (int a = 0; a < 6; ++a) {
+                        Hl[7 * a] += q.lambda;
+                        nb[a] = -q.b[a];
+                    }
+                    if (!ldlt6(Hl, nb, q.delta)) {
+                        q.lambda *= q.nu;
+                        q.nu *= 2.0;
+                        continue;
+                    }
+                    double E[16];
+                    pivoted_exp(q.delta, q.piv, E);
+                    mul44(E, q.T, q.Tn);
+                    q.pn[0] = q.Tn[3];
+                    q.pn[1] = q.Tn[7];
+                    q.pn[2] = q.Tn[11];
+                    q.inner_ok = 1;
+                    want = true;
+                }
+                if (!want) continue;
+                const bool spec = inner == 0;
+                rc = round([&](int b) { return st[b].inner_ok == 1; }, at_Tn,
+                           spec ? (kLinCorrSpos | kLinDual)
+                                : (kLinCorrSpos | GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY));
+                if (rc) break;
+                for (int b = 0; b < B; ++b) {
+                    St& q = st[b];
+                    if (!q.inner_ok) continue;
+                    const double en = spec ? H[32 * b + 29] : H[32 * b + 27];
+                    double den = 0.0;
+                    for (int a = 0; a < 6; ++a) den += q.delta[a] * (q.lambda * q.delta[a] - q.b[a]);
+                    const double rho = (q.e - en) / den;
+                    if (rho > 0) {
+                        std::memcpy(q.T, q.Tn, sizeof(q.T));
+                        std::memcpy(q.piv, q.pn, sizeof(q.piv));
+                        if (spec)
+                            keep(b);
+                        else
+                            q.relin = 1;
+                        const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);
+                        q.lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
+                        q.nu = 2.0;
+                        q.err = en;
+                        q.accepted = 1;
+                    } else {
+                        q.lambda *= q.nu;
+                        q.nu *= 2.0;
+                    }
+                }
+            }
+            if (rc) break;
+            // registrations accepted after a rejection: linearise at the new pose
+            rc = round([&](int b) { return !st[b].done && st[b].relin == 1; }, at_T, kLinCorrSpos);
+            if (rc) break;
+            for (int b = 0; b < B; ++b)
+                if (!st[b].done && st[b].relin) keep(b);
+        }
+        bool relin_gn = false;
+        for (int b = 0; b < B; ++b) {
+            St& q = st[b];
+            if (q.done || q.it != it) continue;
+            if (prm->lm && !q.accepted) {  // no step decreases the cost: a (numerical) minimum
+                q.converged = 1;
+                q.done = 1;
+                continue;
+            }
+            const double mw = std::fmax(std::fabs(q.delta[0]), std::fmax(std::fabs(q.delta[1]), std::fabs(q.delta[2])));
+            const double mv = std::fmax(std::fabs(q.delta[3]), std::fmax(std::fabs(q.delta[4]), std::fabs(q.delta[5])));
+            if (mw < prm->rot_eps && mv < prm->trans_eps) {
+                q.converged = 1;
+                q.done = 1;
+                continue;
+            }
+            if (!prm->lm) {
+                q.piv[0] = q.T[3];
+                q.piv[1] = q.T[7];
+                q.piv[2] = q.T[11];
+                q.relin = 2;
+                relin_gn = true;
+            }
+        }
+        if (relin_gn) {  // Gauss-Newton: linearise at the new poses
+            rc = round([&](int b) { return !st[b].done && st[b].relin == 2; }, at_T, kLinCorrSpos);
+            for (int b = 0; b < B && !rc; ++b)
+                if (!st[b].done && st[b].relin == 2) keep(b);
+        }
+    }
+    cudaFreeAsync(bs.base, s);
+    int any_degenerate = 0;
+    for (int b = 0; b < B; ++b) {
+        std::memcpy(res[b].T, st[b].T, sizeof(res[b].T));
+        res[b].iterations = st[b].it;
+        res[b].converged = st[b].converged;
+        res[b].error = st[b].err;
+        res[b].inliers = st[b].inl;
+        any_degenerate |= st[b].rc == GICP_EDEGENERATE;
+    }
+    if (rc) return rc;
+    return any_degenerate ? set_error(GICP_EDEGENERATE, "gicp_align_batched: a registration has < 6 correspondences")
+                          : GICP_OK;
 }

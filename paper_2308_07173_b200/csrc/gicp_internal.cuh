@@ -201,6 +201,26 @@ __device__ __forceinline__ float adj_lb2(unsigned w, float lox, float hix, float
 }
 __device__ __forceinline__ int2 adj_range(int2 e) { return make_int2(e.x, e.x + (int)((unsigned)e.y >> kAdjCountShift)); }
 
+struct Pose {
+    double R[9];
+    double t[3];
+    double c[3];  // pivot of the rotational perturbation (reading R13)
+    float Rf[9];
+    int active;   // batched: the registration takes part in this launch
+    int cur;      // batched: which correspondence buffer is current (0: corr, 1: corr_old)
+};
+
+// batched launches (gicp_linearize_batched / gicp_align_batched): per block
+// {registration, block within it, its block count}, point offsets [B+1], poses [B]
+struct BatchView {
+    const int4* btab = nullptr;
+    const int64_t* offs = nullptr;
+    const Pose* poses = nullptr;
+    int n_scans = 1;
+    int n_active = 1;
+    int out_stride = 0;
+};
+
 struct LinScratch {
     unsigned* done;
     double* partials;
@@ -210,13 +230,25 @@ struct LinScratch {
     unsigned seq = 0;
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
+constexpr int kLinDual = 1 << 9;      // internal flag: also the trial cost with corr_old (values 29, 30)
+constexpr int kLinNV = 31;            // values a DUAL launch reduces per registration
+size_t linearize_partials_bytes(int64_t nblocks);
 size_t linearize_scratch_bytes(int64_t ns);
 int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                      const float* tgt_cov, const double T[16], const double* pivot, float max_corr_dist, int flags,
                      double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre = nullptr,
                      const int32_t* corr_old = nullptr);
+// the pose block of a launch: R, t (fp64 and fp32 R) and the perturbation pivot
+Pose make_pose(const double T[16], const double* pivot);
+// points per linearize block (the fixed partition of every registration)
+constexpr int kLinPPB = 256;
+// one launch over nb blocks: single (bv.btab == nullptr, P) or batched (bv)
+int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
+                          const float* tgt_cov, const Pose& P, float max_corr_dist, int flags, double* out29,
+                          int32_t* corr, cudaStream_t s, const LinScratch& scr, const int32_t* corr_old,
+                          const BatchView& bv, int64_t nb);
 int attach_covariances(gicp_index_s* idx, const float* cov, cudaStream_t s);
 int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
-                cudaStream_t s);
+                cudaStream_t s, const int64_t* offs = nullptr, int nseg = 1);
 
 }  // namespace gicp

@@ -26,6 +26,7 @@ namespace {
 constexpr int kLinBlock = 256;
 constexpr int kPPT = 1;                       // points per thread
 constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: defines the partition)
+static_assert(kPPB == kLinPPB, "kLinPPB (gicp_internal.cuh) is the partition");
 constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
 constexpr int kNV = 31;                       // reduced values: 28 + count + (DUAL) e_old + count_old
 constexpr int kMaxRing = 16;
@@ -44,12 +45,6 @@ __device__ unsigned long long g_lprof[80];  // [0..3] stage counts, [4] max sear
 #endif
 constexpr int kUnroll = GICP_LIN_UNROLL;  // candidates loaded together in the level-0 scan
 
-struct Pose {
-    double R[9];
-    double t[3];
-    double c[3];  // pivot of the rotational perturbation (reading R13)
-    float Rf[9];
-};
 
 
 struct Levels {
@@ -372,25 +367,51 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                                                          int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
                                                          double* __restrict__ partials, unsigned* __restrict__ done,
                                                          double* __restrict__ out29, volatile unsigned* flag,
-                                                         unsigned seq) {
+                                                         unsigned seq, BatchView bv) {
     LPROF(const long long tk0 = clock64();)
+    // batched launches: this block's registration, its block index within it and
+    // its point range; every registration is partitioned exactly like a single
+    // launch over its own points, so its result is bitwise the single one
+    int scan = 0, blk = blockIdx.x, nblk = gridDim.x;
+    int64_t p0 = 0, pend = ns;
+    if (bv.btab) {
+        const int4 e = bv.btab[blockIdx.x];
+        scan = e.x;
+        blk = e.y;
+        nblk = e.z;
+        if (!bv.poses[scan].active) return;  // block-uniform: converged registration
+        p0 = bv.offs[scan];
+        pend = bv.offs[scan + 1];
+    }
+    __shared__ Pose sP;
+    if (threadIdx.x == 0) sP = bv.btab ? bv.poses[scan] : P;
+    __syncthreads();
+    // correspondence buffers: single launches use (corr, corr_old) as given; a
+    // batched registration reads its current buffer (REUSE / DUAL's old) and
+    // writes the other one
+    if (bv.btab) {
+        int32_t* cur = sP.cur ? const_cast<int32_t*>(corr_old) : corr;
+        int32_t* oth = sP.cur ? corr : const_cast<int32_t*>(corr_old);
+        corr = REUSE ? cur : oth;
+        corr_old = cur;
+    }
     double acc[kNumAcc];
 #pragma unroll
     for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
     double cnt = 0.0, cnt_old = 0.0;
     double eold[kNumAcc];
     eold[27] = 0.0;
-    const int64_t base = (int64_t)blockIdx.x * kPPB + threadIdx.x;
+    const int64_t base = p0 + (int64_t)blk * kPPB + threadIdx.x;
 #pragma unroll 1
     for (int k = 0; k < kPPT; ++k) {
         const int64_t i = base + (int64_t)k * kLinBlock;
-        const bool active = i < ns;  // warp-uniform loop: every lane reaches the search
+        const bool active = i < pend;  // warp-uniform loop: every lane reaches the search
         double pp[3] = {0.0, 0.0, 0.0};
         if (active) {
             const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
 #pragma unroll
             for (int a = 0; a < 3; ++a)
-                pp[a] = __fma_rn(P.R[3 * a + 2], pz, __fma_rn(P.R[3 * a + 1], py, __fma_rn(P.R[3 * a], px, P.t[a])));
+                pp[a] = __fma_rn(sP.R[3 * a + 2], pz, __fma_rn(sP.R[3 * a + 1], py, __fma_rn(sP.R[3 * a], px, sP.t[a])));
         }
         int orig = -1, spos = -1;
         float qx = 0.f, qy = 0.f, qz = 0.f;
@@ -450,7 +471,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                     load_cov_sorted(tgt_cov_sorted, so, cq);
                 else
                     load_cov6(tgt_cov, oo, cq);
-                accumulate_point<true>(P, pp, q.x, q.y, q.z, cp, cq, eold);
+                accumulate_point<true>(sP, pp, q.x, q.y, q.z, cp, cq, eold);
                 cnt_old += 1.0;
             }
         }
@@ -459,7 +480,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             load_cov_sorted(tgt_cov_sorted, spos, cq);
         else
             load_cov6(tgt_cov, orig, cq);
-        accumulate_point<ERROR_ONLY>(P, pp, qx, qy, qz, cp, cq, acc);
+        accumulate_point<ERROR_ONLY>(sP, pp, qx, qy, qz, cp, cq, acc);
         cnt += 1.0;
     }
     LPROF({
@@ -503,20 +524,22 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         }
         partials[(int64_t)blockIdx.x * kNV + c] = v;
     }
-    // last block: fixed-order sum of all block partials
+    // last block (of the registration): fixed-order sum of its block partials
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = (atomicAdd(done, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) last = (atomicAdd(done + scan, 1u) == (unsigned)nblk - 1u);
     __syncthreads();
     if (!last) return;
     __threadfence();
+    partials += (int64_t)(blockIdx.x - blk) * kNV;  // the registration's first block
+    out29 += (int64_t)scan * bv.out_stride;
     // 29 components x 8 interleaved sub-sequences (block b goes to sub b % 8), the
     // loads of each thread batched 8 at a time (independent, in flight together),
     // summed in a fixed order: deterministic and latency-tolerant
     constexpr int kSub = 8;
     __shared__ double part[kSub][kNV];
-    const int nb = gridDim.x;
+    const int nb = nblk;
     if (threadIdx.x < kSub * NV) {
         const int c = threadIdx.x % NV, sub = threadIdx.x / NV;
         double v = 0.0;
@@ -539,12 +562,20 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         for (int sub = 0; sub < kSub; ++sub) v += part[sub][c];
         out29[c] = v;
     }
+    if (threadIdx.x == 0) done[scan] = 0u;
+    if (bv.btab) {  // the last registration to finish signals the launch
+        __shared__ bool fin;
+        __threadfence();
+        if (threadIdx.x == 0) fin = (atomicAdd(done + bv.n_scans, 1u) == (unsigned)bv.n_active - 1u);
+        __syncthreads();
+        if (!fin) return;
+        if (threadIdx.x == 0) done[bv.n_scans] = 0u;
+    }
     if (flag) {  // out29 may be host-mapped: make it visible before the signal
         __threadfence_system();
         __syncthreads();
         if (threadIdx.x == 0) *flag = seq;
     }
-    if (threadIdx.x == 0) *done = 0u;
 }
 
 __global__ void k_zero29(double* out29) {
@@ -553,15 +584,8 @@ __global__ void k_zero29(double* out29) {
 
 }  // namespace
 
-int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
-                     const float* tgt_cov, const double T[16], const double* pivot, float max_corr_dist, int flags,
-                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre,
-                     const int32_t* corr_old) {
-    if (ns == 0) {
-        k_zero29<<<1, 32, 0, s>>>(out29);
-        return check_cuda(cudaGetLastError(), "linearize launch");
-    }
-    Pose P;
+Pose make_pose(const double T[16], const double* pivot) {
+    Pose P{};
     for (int a = 0; a < 3; ++a) {
         for (int b = 0; b < 3; ++b) {
             P.R[3 * a + b] = T[4 * a + b];
@@ -570,9 +594,17 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
         P.t[a] = T[4 * a + 3];
         P.c[a] = pivot ? pivot[a] : 0.0;
     }
+    P.active = 1;
+    P.cur = 0;
+    return P;
+}
+
+int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
+                          const float* tgt_cov, const Pose& P, float max_corr_dist, int flags, double* out29,
+                          int32_t* corr, cudaStream_t s, const LinScratch& scr, const int32_t* corr_old,
+                          const BatchView& bv, int64_t nb) {
     volatile float r2v = max_corr_dist * max_corr_dist;  // fp32 product
     const float r2 = r2v;
-    const int64_t nb = (ns + kPPB - 1) / kPPB;
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
@@ -584,37 +616,19 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
             lvs.ring_level = l;
             break;
         }
-    void* scratch = nullptr;
-    unsigned* done;
-    double* partials;
-    volatile unsigned* flag = pre ? pre->flag : nullptr;
-    const unsigned seq = pre ? pre->seq : 0u;
-    if (pre) {
-        done = pre->done;
-        partials = pre->partials;
-    } else {
-        const size_t bytes = linearize_scratch_bytes(ns);
-        if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
-            cudaGetLastError();
-            return set_error(GICP_ENOMEM, "linearize scratch allocation failed");
-        }
-        done = (unsigned*)scratch;
-        partials = (double*)((char*)scratch + 256);
-        int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset");
-        if (rc) {
-            cudaFreeAsync(scratch, s);
-            return rc;
-        }
-    }
+    unsigned* done = scr.done;
+    double* partials = scr.partials;
+    volatile unsigned* flag = scr.flag;
+    const unsigned seq = scr.seq;
     // the counter is reset by the last block of every launch, so a preallocated
     // scratch stays valid across calls on one stream
     const bool reuse = flags & GICP_LIN_REUSE_CORR, eonly = flags & GICP_LIN_ERROR_ONLY;
     const bool sorted = tgt->cov_sorted != nullptr && tgt_cov == tgt->cov_attached;
     const bool spos = (flags & kLinCorrSpos) && sorted;
-    const bool dual = corr_old != nullptr && !reuse && !eonly;
+    const bool dual = (flags & kLinDual) && !reuse && !eonly;
 #define GICP_LIN_ARGS                                                                                            \
     src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
-        done, out29, flag, seq
+        done, out29, flag, seq, bv
 #define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_RE(S, SP)           \
@@ -644,28 +658,47 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
 #undef GICP_LIN_RE
 #undef GICP_LIN_GO
 #undef GICP_LIN_ARGS
-    const int rc = check_cuda(cudaGetLastError(), "linearize launch");
-    if (scratch) cudaFreeAsync(scratch, s);
-#if GICP_LIN_PROF
-    if (getenv("GICP_DEBUG_STATS")) {
-        unsigned long long h[80];
-        cudaStreamSynchronize(s);
-        cudaMemcpyFromSymbol(h, g_lprof, sizeof(h));
-        const double w = h[0] ? (double)h[0] : 1.0;
-        fprintf(stderr, "[gicp lin prof] warps=%llu fallback=%llu rings=%llu overflow=%llu search avg %.0f max %llu | "
-                "total avg %.0f max %llu\n   search hist:", h[0], h[1], h[2], h[3], h[5] / w, h[4], h[6] / w, h[7]);
-        for (int b = 8; b < 40; ++b)
-            if (h[b]) fprintf(stderr, " 2^%d:%llu", b - 8, h[b]);
-        fprintf(stderr, "\n   total hist:");
-        for (int b = 40; b < 72; ++b)
-            if (h[b]) fprintf(stderr, " 2^%d:%llu", b - 40, h[b]);
-        fprintf(stderr, "\n");
-        for (auto& x : h) x = 0;
-        cudaMemcpyToSymbol(g_lprof, h, sizeof(h));
+    return check_cuda(cudaGetLastError(), "linearize launch");
+}
+
+int launch_linearize(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
+                     const float* tgt_cov, const double T[16], const double* pivot, float max_corr_dist, int flags,
+                     double* out29, int32_t* corr, cudaStream_t s, const LinScratch* pre,
+                     const int32_t* corr_old) {
+    if (ns == 0) {
+        k_zero29<<<1, 32, 0, s>>>(out29);
+        return check_cuda(cudaGetLastError(), "linearize launch");
     }
-#endif
+    const Pose P = make_pose(T, pivot);
+    const int64_t nb = (ns + kPPB - 1) / kPPB;
+    void* scratch = nullptr;
+    LinScratch scr;
+    if (pre) {
+        scr = *pre;
+    } else {
+        const size_t bytes = linearize_scratch_bytes(ns);
+        if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(GICP_ENOMEM, "linearize scratch allocation failed");
+        }
+        scr.done = (unsigned*)scratch;
+        scr.partials = (double*)((char*)scratch + 256);
+        int rc = check_cuda(cudaMemsetAsync(scr.done, 0, sizeof(unsigned), s), "memset");
+        if (rc) {
+            cudaFreeAsync(scratch, s);
+            return rc;
+        }
+    }
+    // the counter is reset by the last block of every launch, so a preallocated
+    // scratch stays valid across calls on one stream
+    if (corr_old) flags |= kLinDual;
+    const int rc = launch_linearize_core(src, src_cov, ns, tgt, tgt_cov, P, max_corr_dist, flags, out29, corr, s, scr,
+                                         corr_old, BatchView{}, nb);
+    if (scratch) cudaFreeAsync(scratch, s);
     return rc;
 }
+
+size_t linearize_partials_bytes(int64_t nblocks) { return (size_t)nblocks * kNV * sizeof(double); }
 
 size_t linearize_scratch_bytes(int64_t ns) {
     const int64_t nb = (ns + kPPB - 1) / kPPB;

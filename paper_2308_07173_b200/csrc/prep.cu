@@ -22,8 +22,8 @@ __global__ void k_attach_cov(const float4* __restrict__ pts, const float* __rest
     out[2 * i + 1] = make_float4(c[4], c[5], 0.f, 0.f);
 }
 
-__global__ void k_source_keys(const float* __restrict__ src, int64_t n, float inv, unsigned long long* __restrict__ keys,
-                              int* __restrict__ vals) {
+__global__ void k_source_keys(const float* __restrict__ src, int64_t n, float inv, const int64_t* __restrict__ offs,
+                              int nseg, unsigned long long* __restrict__ keys, int* __restrict__ vals) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     unsigned c[3];
@@ -35,7 +35,16 @@ __global__ void k_source_keys(const float* __restrict__ src, int64_t n, float in
         t = fminf(fmaxf(t, -512.0f), 511.0f);
         c[a] = (unsigned)((int)floorf(t) + 512);
     }
-    keys[i] = cell_key((int)c[0], (int)c[1], (int)c[2]);
+    unsigned long long seg = 0;
+    if (offs) {  // batched: the registration of point i (largest s with offs[s] <= i) in the high bits
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (offs[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        seg = (unsigned long long)lo << 30;
+    }
+    keys[i] = seg | cell_key((int)c[0], (int)c[1], (int)c[2]);
     vals[i] = (int)i;
 }
 
@@ -68,11 +77,14 @@ int attach_covariances(gicp_index_s* idx, const float* cov, cudaStream_t s) {
 }
 
 int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
-                cudaStream_t s) {
+                cudaStream_t s, const int64_t* offs, int nseg) {
+    int segbits = 0;
+    while (offs && (1 << segbits) < nseg) ++segbits;
+    const int bits = 30 + segbits;
     void* buf = nullptr;
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                    (int*)nullptr, (int*)nullptr, (int)ns, 0, 30, s);
+                                    (int*)nullptr, (int*)nullptr, (int)ns, 0, bits, s);
     const size_t bytes = ns * (8 + 8 + 4 + 4) + tb + 64;
     if (cudaMallocAsync(&buf, bytes, s) != cudaSuccess) {
         cudaGetLastError();
@@ -84,8 +96,9 @@ int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, 
     int* v_out = v_in + ns;
     void* temp = (void*)(((uintptr_t)(v_out + ns) + 15) & ~(uintptr_t)15);
     const unsigned g = (unsigned)((ns + 255) / 256);
-    k_source_keys<<<g, 256, 0, s>>>(src, ns, 1.0f / cell, k_in, v_in);
-    cub::DeviceRadixSort::SortPairs(temp, tb, k_in, k_out, v_in, v_out, (int)ns, 0, 30, s);
+    k_source_keys<<<g, 256, 0, s>>>(src, ns, 1.0f / cell, offs, nseg, k_in, v_in);
+    // stable: within a registration the order is the single-registration order
+    cub::DeviceRadixSort::SortPairs(temp, tb, k_in, k_out, v_in, v_out, (int)ns, 0, bits, s);
     k_gather_source<<<g, 256, 0, s>>>(src, src_cov, v_out, ns, src_p, cov_p);
     const int rc = check_cuda(cudaGetLastError(), "source sort");
     cudaFreeAsync(buf, s);
