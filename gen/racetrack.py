@@ -503,6 +503,18 @@ def config_c4_scan(i: int, n_scan: int = 100_000):
     return sc, T, T @ perturbation(0.5, 1.0, 1000 + i + 7)
 
 
+def config_c5(n_per_lap: int = 2_000_000, laps: int = 10, n_scan: int = 100_000, n_scans: int = 10):
+    """C5 stress: multi-lap map (laps x n_per_lap points) and a query batch of
+    n_scans scans (seeds 2000..) at arc lengths spread over the track, each moved
+    into the map frame by its T_true. Returns (map, queries) float32."""
+    mp = multi_lap_map(n_per_lap, laps, 1)
+    qs = []
+    for i in range(n_scans):
+        sc, T = scan(n_scan, (i + 0.5) * TRACK_LEN / n_scans, 2000 + i)
+        qs.append(apply_T(T, sc))
+    return mp, np.ascontiguousarray(np.concatenate(qs).astype(np.float32))
+
+
 def lattice(side: int = 5) -> np.ndarray:
     """Integer lattice {0..side-1}^3 with idx = (x*side + y)*side + z (the kNN tie
     worked example of SURVEY.md §8(c) "What pins each part")."""

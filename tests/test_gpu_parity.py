@@ -337,3 +337,28 @@ def test_c3_fullsize_sampled(orc):
     o29, ab, ocorr = orc.linearize(src, cs, mp, ct, T0, 1.0, pivot=T0[:3, 3])
     assert np.array_equal(H(corr), ocorr)
     assert_lin_parity(H(out), o29, ab)
+
+
+def test_c5_stress_sampled(orc):
+    """C5: 20M-point multi-lap map, 1M external queries (10 scans in the map
+    frame), k=32 kNN + covariance of the neighbour sets; cell 0.2 m (~1.1 r_32 at
+    10x the C3 density). Sampled rows against the oracle (brute force over the
+    full 20M), every row checked for the properties that hold at any size."""
+    mp, q = gen.config_c5()
+    mpd = D(mp)
+    idx = g.build_index(mpd, 0.2)
+    nbr, d2 = g.knn(idx, D(q), 32)
+    cov = g.covariances(mpd, nbr, 1e-3)
+    hn, hd, hc = H(nbr), H(d2), H(cov)
+    # properties, all 1M rows: indices in range, rows ascending by (d2, idx)
+    assert hn.min() >= 0 and hn.max() < len(mp)
+    assert np.all(np.isfinite(hd))
+    dd = np.diff(hd, axis=1)
+    assert np.all((dd > 0) | ((dd == 0) & (np.diff(hn, axis=1) > 0)))
+    rng = np.random.default_rng(78)
+    rows = np.concatenate([[0, len(q) - 1], rng.choice(len(q), 254, replace=False)])
+    on, od = orc.knn(mp, q[rows], 32)
+    assert np.array_equal(hn[rows], on) and np.array_equal(hd[rows], od)
+    oc, gap, _ = orc.covariance(mp, on)
+    assert_cov_parity(hc[rows], oc, gap, masked_frac_max=0.05)
+    idx.free()

@@ -1,0 +1,122 @@
+"""Device-timed numbers for the non-headline configs:
+  C2  scan-to-scan latency: index + kNN/cov of both 30k scans + align
+  C4  batched registration: B scans x 100k vs the 2M map, gicp_align_batched
+      (iterations/s = sum of per-scan iterations / time) vs B single aligns
+  C5  20M multi-lap map, 1M queries, k=32: index build, kNN, covariances
+usage: python tools/workloads.py [c2] [c4 [B]] [c5]"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import gen
+import paper_2308_07173_b200 as g
+
+DEV = torch.device("cuda", 0)
+
+
+def D(a):
+    return torch.from_numpy(np.array(a)).to(DEV)
+
+
+def timed(fn, reps=5, warm=2):
+    ts = []
+    for r in range(reps + warm):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        if r >= warm:
+            ts.append(a.elapsed_time(b))
+    return float(np.median(ts)), out
+
+
+def c2():
+    src, tgt, T_rel, T0 = gen.config_c2()
+    sd, td = D(src), D(tgt)
+
+    def run():
+        it = g.build_index(td, 0.0)
+        _, _, ct = g.knn_cov_self(it, 20, with_nbr=False)
+        isd = g.build_index(sd, 0.0)
+        _, _, cs = g.knn_cov_self(isd, 20, with_nbr=False)
+        T, info = g.align(sd, cs, it, ct, T0)
+        it.free()
+        isd.free()
+        return info
+    ms, info = timed(run)
+    print(json.dumps({"workload": "C2 scan-to-scan 30k vs 30k, k=20", "latency_ms": ms,
+                      "align_iterations": info.iterations}))
+
+
+def c4(B):
+    mp = gen.racetrack_map(2_000_000, 1)
+    im = g.build_index(D(mp), 0.5)
+    _, _, cm = g.knn_cov_self(im, 20, with_nbr=False)
+    g.attach_cov(im, cm)
+    scans, covs, T0s = [], [], []
+    for i in range(B):
+        sc, T, T0 = gen.config_c4_scan(i * (256 // B))
+        sd = D(sc)
+        isc = g.build_index(sd, 0.0)
+        _, _, cs = g.knn_cov_self(isc, 20, with_nbr=False)
+        isc.free()
+        scans.append(sd)
+        covs.append(cs)
+        T0s.append(T0)
+    offs = np.concatenate([[0], np.cumsum([s.shape[0] for s in scans])])
+    src = torch.cat(scans).contiguous()
+    cov = torch.cat(covs).contiguous()
+    T0s = np.array(T0s)
+    ms_b, (Ts, infos) = timed(lambda: g.align_batched(src, cov, offs, im, cm, T0s, allow_degenerate=True), reps=3)
+    its = sum(i.iterations for i in infos)
+
+    def singles():
+        return [g.align(scans[b], covs[b], im, cm, T0s[b])[1] for b in range(B)]
+    ms_s, infos_s = timed(singles, reps=3)
+    same = all(a.iterations == b.iterations and a.error == b.error for a, b in zip(infos, infos_s))
+    print(json.dumps({"workload": f"C4 batched: {B} scans x 100k vs 2M map", "batched_ms": ms_b,
+                      "iterations_total": its, "batched_iters_per_s": 1e3 * its / ms_b,
+                      "batched_source_pts_per_s": 1e3 * its * 100_000 / ms_b, "singles_ms": ms_s,
+                      "singles_iters_per_s": 1e3 * its / ms_s, "identical_to_singles": same}))
+
+
+def c5():
+    t = time.time()
+    mp, q = gen.config_c5()
+    gen_s = time.time() - t
+    mpd, qd = D(mp), D(q)
+    ms_build, idx = timed(lambda: g.build_index(mpd, 0.2), reps=3)
+    nbr = torch.empty((q.shape[0], 32), dtype=torch.int32, device=DEV)
+    d2 = torch.empty((q.shape[0], 32), dtype=torch.float32, device=DEV)
+    cov = torch.empty((q.shape[0], 6), dtype=torch.float32, device=DEV)
+    ms_knn, _ = timed(lambda: g.knn(idx, qd, 32, out=(nbr, d2)))
+    ms_cov, _ = timed(lambda: g.covariances(mpd, nbr, 1e-3, out=cov))
+    m = q.shape[0]
+    print(json.dumps({"workload": "C5 20M multi-lap map, 1M queries, k=32", "index_build_ms": ms_build,
+                      "knn_ms": ms_knn, "cov_ms": ms_cov, "knn_cov_pts_per_s": 1e3 * m / (ms_knn + ms_cov),
+                      "gen_s": gen_s}))
+
+
+if __name__ == "__main__":
+    args = sys.argv[1:] or ["c2", "c4", "c5"]
+    i = 0
+    while i < len(args):
+        a = args[i]
+        if a == "c2":
+            c2()
+        elif a == "c4":
+            B = 16
+            if i + 1 < len(args) and args[i + 1].isdigit():
+                B = int(args[i + 1])
+                i += 1
+            c4(B)
+        elif a == "c5":
+            c5()
+        i += 1
