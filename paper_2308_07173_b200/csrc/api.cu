@@ -220,6 +220,8 @@ GICP_API void gicp_index_free(gicp_index idx) {
     if (idx->cov_sorted) cudaFreeAsync(idx->cov_sorted, s);
     if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
     if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
+    if (idx->adj_oc1) cudaFreeAsync(idx->adj_oc1, s);
+    if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
     cudaGetLastError();
     delete idx;
 }

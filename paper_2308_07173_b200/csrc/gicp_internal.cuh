@@ -161,6 +161,8 @@ struct gicp_index_s {
     gicp::HashEntry* hash_mem = nullptr;  // all levels' tables, one allocation
     int2* adj_oc = nullptr;               // [n] (offset, count) of the level-0 adjacency list, at voxel heads
     int2* adj_rng = nullptr;              // neighbour voxels, nearest-first per voxel: {start, count<<6 | code}
+    int2* adj_oc1 = nullptr;              // the same lists for level 1 (escalated queries)
+    int2* adj_rng1 = nullptr;
     float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
     const float* cov_attached = nullptr;  // the caller's original-order array they were copied from
     int device = 0;

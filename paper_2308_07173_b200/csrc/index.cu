@@ -143,19 +143,38 @@ struct LevelSet {
 // run heads of every level insert their voxel (key >> 3l, start); level-0 heads
 // are also appended to a compact list (for the adjacency kernel)
 __global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, LevelSet ls, int* __restrict__ nheads,
-                        int* __restrict__ heads) {
+                        int* __restrict__ heads, int* __restrict__ nheads1, int* __restrict__ heads1) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool in = i < n;
     const unsigned long long k = in ? keys[i] : 0ull;
     const unsigned long long kp = (in && i > 0) ? keys[i - 1] : ~0ull;
     const bool h0 = in && (i == 0 || kp != k);
+    const bool h1 = in && ls.n > 1 && (i == 0 || (kp >> 3) != (k >> 3));
     {
-        const unsigned mask = __ballot_sync(0xffffffffu, h0);
-        const int lane = threadIdx.x & 31;
-        int base = 0;
-        if (lane == 0 && mask) base = atomicAdd(nheads, __popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (h0) heads[base + __popc(mask & ((1u << lane) - 1))] = (int)i;
+        // compact head lists of levels 0 and 1: warp ballots, one atomic per list
+        // per BLOCK (a counter hit by every warp would serialise at the L2)
+        __shared__ int wc[2][32];
+        __shared__ int bb[2];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+        if (lane == 0) {
+            wc[0][wid] = __popc(m0);
+            wc[1][wid] = __popc(m1);
+        }
+        __syncthreads();
+        if (threadIdx.x < 2) {
+            int t = 0;
+            for (int w = 0; w < nw; ++w) {
+                const int c = wc[threadIdx.x][w];
+                wc[threadIdx.x][w] = t;
+                t += c;
+            }
+            bb[threadIdx.x] = t ? atomicAdd(threadIdx.x == 0 ? nheads : nheads1, t) : 0;
+        }
+        __syncthreads();
+        const unsigned lt = (1u << lane) - 1;
+        if (h0) heads[bb[0] + wc[0][wid] + __popc(m0 & lt)] = (int)i;
+        if (h1) heads1[bb[1] + wc[1][wid] + __popc(m1 & lt)] = (int)i;
     }
     if (!in) return;
     for (int l = 0; l < ls.n; ++l) {
@@ -221,10 +240,10 @@ __global__ void k_scatter(const float* __restrict__ xyz, const int* __restrict__
 // memory is scheduling-dependent, the list of every voxel is not; (offset,
 // count) is stored at the voxel's first point.
 constexpr int kAdjBlock = 256;
-__global__ void __launch_bounds__(kAdjBlock) k_adjacency(Grid g, const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(kAdjBlock) k_adjacency(Grid g, int shift, const unsigned long long* __restrict__ keys,
                                                           const int* __restrict__ heads, const int* __restrict__ nheads,
                                                           int* __restrict__ total, int2* __restrict__ oc,
-                                                          int2* __restrict__ rng_out) {
+                                                          int2* __restrict__ rng_out, int* __restrict__ overflow) {
     __shared__ int wcnt[kAdjBlock / 32];
     __shared__ int bbase;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -242,7 +261,7 @@ __global__ void __launch_bounds__(kAdjBlock) k_adjacency(Grid g, const unsigned 
         head = heads[w];
         // neighbour key by dilated-integer increments of the voxel's Morton key; a
         // step off the grid yields a key no voxel has (empty lookup)
-        const unsigned long long key = keys[head];
+        const unsigned long long key = keys[head] >> shift;
         const unsigned long long MX = 0x1249249249249249ull, MY = MX << 1, MZ = MX << 2;
         auto step = [](unsigned long long k, unsigned long long M, int d) {
             return d < 0 ? ((k - 1ull) & M) : (d > 0 ? (((k | ~M) + 1ull) & M) : k);
@@ -271,7 +290,7 @@ __global__ void __launch_bounds__(kAdjBlock) k_adjacency(Grid g, const unsigned 
     if (ne) {
         const int o = base + __popc(mask & ((1u << lane) - 1));
         const int c = r.y - r.x;
-        if (c > kAdjMaxCount) atomicOr(total + 1, 1);  // count does not fit the packing: no lists
+        if (c > kAdjMaxCount) atomicOr(overflow, 1);  // count does not fit the packing: no lists
         rng_out[o] = make_int2(r.x, (int)adj_pack(c, dx, dy, dz));
     }
     if (valid && lane == 0) oc[head] = make_int2(base, cnt);
@@ -456,6 +475,8 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if (idx->hash_mem) cudaFreeAsync(idx->hash_mem, s);
         if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
         if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
+        if (idx->adj_oc1) cudaFreeAsync(idx->adj_oc1, s);
+        if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
         delete idx;
         return code;
     };
@@ -476,41 +497,48 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         ls.lv[l] = idx->lv[l];
     }
     DevBuf headbuf;
-    if ((rc = alloc_async(headbuf, (n + 4) * sizeof(int), s))) return fail(rc);
-    int* nheads = (int*)headbuf.p;
-    int* heads = nheads + 4;
-    if ((rc = check_cuda(cudaMemsetAsync(nheads, 0, sizeof(int), s), "memset"))) return fail(rc);
-    k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls, nheads, heads);
+    const int64_t n1 = L > 1 ? counts[1] : 0;
+    if ((rc = alloc_async(headbuf, (counts[0] + n1 + 8) * sizeof(int), s))) return fail(rc);
+    int* nheads = (int*)headbuf.p;  // [0] level-0 heads, [1] level-1 heads
+    int* heads = nheads + 8;
+    int* heads1 = heads + counts[0];
+    if ((rc = check_cuda(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), s), "memset"))) return fail(rc);
+    k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls, nheads, heads, nheads + 1, heads1);
     k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls);
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
     int adj_overflow = 0;
     {
-        // level-0 adjacency lists, one pass (upper bound 27 entries per voxel)
-        const int64_t ub = 27 * std::max<int64_t>(counts[0], 1);
-        if (cudaMallocAsync(&idx->adj_oc, n * sizeof(int2), s) != cudaSuccess ||
-            cudaMallocAsync(&idx->adj_rng, ub * sizeof(int2), s) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
-        }
+        // adjacency lists of levels 0 and 1, one pass each (<= 27 entries per voxel)
         DevBuf tot;
-        if ((rc = alloc_async(tot, 16, s))) return fail(rc);
-        if ((rc = check_cuda(cudaMemsetAsync(tot.p, 0, 16, s), "memset"))) return fail(rc);
-        const int64_t threads = (int64_t)std::max(counts[0], 1) * 32;
-        k_adjacency<<<grid_for(threads, kAdjBlock), kAdjBlock, 0, s>>>(idx->lv[0], (unsigned long long*)keys.p, heads, nheads,
-                                                            (int*)tot.p, idx->adj_oc, idx->adj_rng);
-        idx->device_bytes += n * 8 + ub * 8;
-        if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);
+        if ((rc = alloc_async(tot, 32, s))) return fail(rc);
+        if ((rc = check_cuda(cudaMemsetAsync(tot.p, 0, 32, s), "memset"))) return fail(rc);
+        for (int l = 0; l < std::min(L, 2); ++l) {
+            int2*& oc = l == 0 ? idx->adj_oc : idx->adj_oc1;
+            int2*& rng = l == 0 ? idx->adj_rng : idx->adj_rng1;
+            const int64_t nv = std::max(counts[l], 1);
+            if (cudaMallocAsync(&oc, n * sizeof(int2), s) != cudaSuccess ||
+                cudaMallocAsync(&rng, 27 * nv * sizeof(int2), s) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
+            }
+            // per level: [2l] output counter, [1] overflow flag (shared)
+            k_adjacency<<<grid_for(nv * 32, kAdjBlock), kAdjBlock, 0, s>>>(
+                idx->lv[l], 3 * l, (unsigned long long*)keys.p, l == 0 ? heads : heads1, nheads + l,
+                (int*)tot.p + 2 * l, oc, rng, (int*)tot.p + 1);
+            idx->device_bytes += n * 8 + 27 * nv * 8;
+            if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);
+        }
         if ((rc = check_cuda(cudaMemcpyAsync(&adj_overflow, (int*)tot.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s),
                              "adjacency flag")))
             return fail(rc);
     }
     if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
     if (adj_overflow) {  // a voxel too full for the packed entry: queries probe the hash instead
-        cudaFreeAsync(idx->adj_oc, s);
-        cudaFreeAsync(idx->adj_rng, s);
-        idx->adj_oc = nullptr;
-        idx->adj_rng = nullptr;
+        for (int2** p : {&idx->adj_oc, &idx->adj_rng, &idx->adj_oc1, &idx->adj_rng1}) {
+            if (*p) cudaFreeAsync(*p, s);
+            *p = nullptr;
+        }
     }
     *out = idx;
     return GICP_OK;

@@ -37,7 +37,7 @@ constexpr int kBlock = 128;
 #define GICP_KNN_PROF 0  // diagnostics build: per-warp step/replacement counters
 #endif
 #if GICP_KNN_PROF
-__device__ unsigned long long g_kprof[16];
+__device__ unsigned long long g_kprof[64];  // 16 counters per level 0, 1, 2, >= 3
 #define KPROF(x) x
 #else
 #define KPROF(x)
@@ -202,6 +202,8 @@ struct FastShape {
 struct AdjView {
     const int2* oc;
     const int2* rng;  // packed entries (adj_pack)
+    const int2* oc1;  // level 1 (escalated queries)
+    const int2* rng1;
 };
 
 template <int KCAP, bool EXACT = false>
@@ -218,11 +220,13 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     int nr = 0;
     int a0 = 0, a1 = 0;
     bool use_adj = false;
-    if (active && g.level == 0 && adj.oc != nullptr) {
+    const int2* adj_oc = g.level == 0 ? adj.oc : (g.level == 1 ? adj.oc1 : nullptr);
+    const int2* adj_rng = g.level == 0 ? adj.rng : adj.rng1;
+    if (active && adj_oc != nullptr) {
         const int2 own = cell_lookup(g, G.cx, G.cy, G.cz);
         if (own.y > own.x) {
             use_adj = true;
-            const int2 oc = __ldg(adj.oc + own.x);
+            const int2 oc = __ldg(adj_oc + own.x);
             a0 = oc.x;
             a1 = oc.x + oc.y;
         }
@@ -339,7 +343,7 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     // software pipeline: the next adjacency entry and the next candidate point are
     // loaded one advance / one step ahead, so their latency overlaps the heap work
     int2 ne = make_int2(0, 0);
-    if (use_adj && ri < rend) ne = __ldg(adj.rng + ri);
+    if (use_adj && ri < rend) ne = __ldg(adj_rng + ri);
     float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
     while (true) {
         // advance exhausted lanes to their next non-pruned range
@@ -350,7 +354,7 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
             float lb2;
             if (use_adj) {
                 const int2 e = ne;
-                if (ri + 1 < rend) ne = __ldg(adj.rng + ri + 1);
+                if (ri + 1 < rend) ne = __ldg(adj_rng + ri + 1);
                 r = adj_range(e);
                 lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
             } else {
@@ -371,6 +375,20 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
         step(has, pos, p);
         if (has) ++pos;
     }
+#if GICP_KNN_PROF
+    if (!EXACT) {
+        const unsigned full = 0xffffffffu;
+        const unsigned v[9] = {p_steps, p_fill, p_repl, __reduce_add_sync(full, p_lrepl), __reduce_max_sync(full, p_lrepl),
+                               __reduce_add_sync(full, p_cand), __reduce_add_sync(full, p_ent), p_adv,
+                               (unsigned)__popc(__ballot_sync(full, active))};
+        if ((threadIdx.x & 31) == 0) {
+            const int b = 16 * min(g.level, 3);
+            for (int i = 0; i < 8; ++i) atomicAdd(&g_kprof[b + i], (unsigned long long)v[i]);
+            atomicAdd(&g_kprof[b + 8], 1ull);
+            atomicAdd(&g_kprof[b + 9], (unsigned long long)v[8]);
+        }
+    }
+#endif
     if (!active) return 0;
     if (cnt < K) return 1;
     const float m = cube_margin(G, s, slack, 1);
@@ -811,7 +829,7 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     Levels lvs;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
     // level 0 over every query, then one launch that climbs the pyramid for the rest
-    const AdjView adj{idx->adj_oc, idx->adj_rng};
+    const AdjView adj{idx->adj_oc, idx->adj_rng, idx->adj_oc1, idx->adj_rng1};
     k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
                                                          cov, counts + 2, listA, counts + 0, exact, L == 1);
     if (L > 1)
@@ -826,12 +844,17 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
         cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
 #if GICP_KNN_PROF
-        unsigned long long pv[16];
+        unsigned long long pv[64];
         cudaMemcpyFromSymbol(pv, g_kprof, sizeof(pv));
-        const double w = (double)pv[8];
-        fprintf(stderr, "[gicp knn prof] warps=%.0f per warp: steps %.1f fill-steps %.1f repl-steps %.1f lane-repl %.1f "
-                "max-lane-repl %.1f lane-cand %.1f lane-entries %.1f adv-iters %.1f\n", w, pv[0] / w, pv[1] / w,
-                pv[2] / w, pv[3] / w, pv[4] / w, pv[5] / w, pv[6] / w, pv[7] / w);
+        for (int lv = 0; lv < 4; ++lv) {
+            const unsigned long long* q = pv + 16 * lv;
+            const double w = q[8] ? (double)q[8] : 1.0;
+            if (!q[8]) continue;
+            fprintf(stderr, "[gicp knn prof] level %d%s warp calls=%.0f active lanes/call %.1f | per call: steps %.1f "
+                    "fill-steps %.1f repl-steps %.1f lane-repl %.1f max-lane-repl %.1f lane-cand %.1f lane-entries %.1f "
+                    "adv-iters %.1f\n", lv, lv == 3 ? "+" : "", w, q[9] / w, q[0] / w, q[1] / w, q[2] / w, q[3] / w,
+                    q[4] / w, q[5] / w, q[6] / w, q[7] / w);
+        }
         for (auto& x : pv) x = 0;
         cudaMemcpyToSymbol(g_kprof, pv, sizeof(pv));
 #endif
