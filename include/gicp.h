@@ -238,6 +238,27 @@ int gicp_align_batched(const float* src, const float* src_cov, const int64_t* of
                        const gicp_align_params* params /* host */, gicp_align_result* result /* host [B] */,
                        void* stream);
 
+/* gicp_align_batched_ex -- the sharded form: this process holds
+ * E entries (point ranges offsets[E+1] of src), entry e belonging to
+ * registration entry_reg[e] (host int [E], NULL = identity with E == B). After
+ * every evaluation round the library calls
+ *     reduce(entry_rows, E, reg_rows, B, user)
+ * with entry_rows (host) [E][32] -- per entry: out29 (H 21, b 6, e, count), the
+ * trial cost with the previous correspondences and its count, one pad -- and
+ * the callback must fill reg_rows (host) [B][32] with the sum over ALL processes'
+ * entries of each registration (a cross-rank allreduce; summing a fixed global
+ * chunking in chunk order makes the result independent of the process count).
+ * It returns 0 on success. Every process must run the same B registrations with
+ * the same T0 and params: the host LM decisions depend on reg_rows only, so all
+ * processes take the same rounds and their collectives stay matched. reduce =
+ * NULL sums the local entries of each registration in entry order. */
+typedef int (*gicp_reduce_fn)(const double* entry_rows, int E, double* reg_rows, int B, void* user);
+
+int gicp_align_batched_ex(const float* src, const float* src_cov, const int64_t* offsets /* host [E+1] */, int E,
+                          const int* entry_reg /* host [E] or NULL */, int B, gicp_index tgt, const float* tgt_cov,
+                          const double* T0 /* host [B][16] */, const gicp_align_params* params /* host */,
+                          gicp_align_result* result /* host [B] */, gicp_reduce_fn reduce, void* user, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,11 +66,15 @@ _lib.gicp_align.argtypes = [_P, _P, _i64, _P, _P, _P, ctypes.POINTER(AlignParams
                             _P]
 _lib.gicp_linearize_batched.argtypes = [_P, _P, _P, _i32, _P, _P, _P, _P, _f32, _i32, _P, _P, _P]
 _lib.gicp_align_batched.argtypes = [_P, _P, _P, _i32, _P, _P, _P, ctypes.POINTER(AlignParams), _P, _P]
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                             ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_void_p)
+_lib.gicp_align_batched_ex.argtypes = [_P, _P, _P, _i32, _P, _i32, _P, _P, _P, ctypes.POINTER(AlignParams), _P,
+                                       REDUCE_FN, _P, _P]
 
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
-           "gicp_linearize_batched", "gicp_align_batched"]
+           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex"]
 
 
 class GicpError(RuntimeError):
@@ -283,6 +287,44 @@ def align_batched(src: torch.Tensor, src_cov: torch.Tensor, offsets, tgt: Index,
     rc = _lib.gicp_align_batched(_dptr(src), _dptr(src_cov.contiguous()), o.ctypes.data_as(_P), B, tgt.handle,
                                  _dptr(tgt_cov.contiguous()), T0h.ctypes.data_as(_P), ctypes.byref(p),
                                  ctypes.cast(res, _P), _stream())
+    if not (allow_degenerate and rc == EDEGENERATE):
+        _check(rc)
+    Ts = np.array([np.array(r.T[:], dtype=np.float64).reshape(4, 4) for r in res])
+    return Ts, [AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers)) for r in res]
+
+
+def align_batched_ex(src: torch.Tensor, src_cov: torch.Tensor, offsets, entry_reg, B: int, tgt: Index,
+                     tgt_cov: torch.Tensor, T0s, reduce, max_iter=64, lm=True, rot_eps=1e-6, trans_eps=1e-5,
+                     max_corr_dist=1.0, allow_degenerate=False):
+    """Sharded batched align (gicp_align_batched_ex): E local entries (offsets [E+1]),
+    entry e of registration entry_reg[e]; reduce(entry_rows [E,32] float64 numpy) ->
+    registration rows [B,32] (the cross-rank combine, sharding.make_chunk_reducer)."""
+    src = _pts(src, "src")
+    o = _offsets(offsets, src.shape[0])
+    E = o.size - 1
+    er = np.ascontiguousarray(np.asarray(entry_reg, dtype=np.int32).reshape(E))
+    T0h = np.ascontiguousarray(np.asarray(T0s, dtype=np.float64).reshape(B, 16))
+    p = AlignParams(int(max_iter), int(bool(lm)), float(rot_eps), float(trans_eps), float(max_corr_dist))
+    res = (AlignResult * B)()
+    err = []
+
+    def cb(erows, ne, rrows, nb, user):
+        try:
+            rows = np.ctypeslib.as_array(erows, shape=(ne, 32)).copy() if ne > 0 else np.zeros((0, 32))
+            out = np.asarray(reduce(rows), dtype=np.float64).reshape(nb, 32)
+            np.ctypeslib.as_array(rrows, shape=(nb, 32))[:] = out
+            return 0
+        except Exception as e:  # reported after the call returns
+            err.append(e)
+            return 1
+    cfn = REDUCE_FN(cb)
+    rc = _lib.gicp_align_batched_ex(_dptr(src) if src.shape[0] else None,
+                                    _dptr(src_cov.contiguous()) if src.shape[0] else None, o.ctypes.data_as(_P), E,
+                                    er.ctypes.data_as(_P) if E else None, B, tgt.handle, _dptr(tgt_cov.contiguous()),
+                                    T0h.ctypes.data_as(_P), ctypes.byref(p), ctypes.cast(res, _P), cfn, None,
+                                    _stream())
+    if err:
+        raise err[0]
     if not (allow_degenerate and rc == EDEGENERATE):
         _check(rc)
     Ts = np.array([np.array(r.T[:], dtype=np.float64).reshape(4, 4) for r in res])

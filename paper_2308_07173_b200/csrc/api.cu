@@ -632,12 +632,26 @@ GICP_API int gicp_linearize_batched(const float* src, const float* src_cov, cons
 // Lockstep LM over B registrations: the per-registration logic is gicp_align's,
 // step for step; each evaluation round is ONE batched launch over the
 // registrations that need it (the others' blocks exit at once).
-GICP_API int gicp_align_batched(const float* src, const float* src_cov, const int64_t* offsets, int B,
-                                gicp_index tgt, const float* tgt_cov, const double* T0,
-                                const gicp_align_params* prm, gicp_align_result* res, void* stream) {
+// Generalised for sharding: the launch covers E entries (point ranges), entry e
+// belonging to registration entry_reg[e]; after every round the entry rows are
+// turned into registration rows by `reduce` (a cross-rank combine) or, without
+// one, summed in entry order.
+static int align_batched_impl(const float* src, const float* src_cov, const int64_t* offsets, int E,
+                              const int* entry_reg, int B, gicp_index tgt, const float* tgt_cov, const double* T0,
+                              const gicp_align_params* prm, gicp_align_result* res, gicp_reduce_fn reduce,
+                              void* user, void* stream) {
     int rc;
-    if ((rc = check_offsets(offsets, B, "gicp_align_batched"))) return rc;
-    const int64_t ns = offsets[B];
+    if (E == 0 && reduce) {  // a process without entries still takes part in the rounds
+        if (!offsets || offsets[0] != 0) return set_error(GICP_EINVAL, "gicp_align_batched: offsets");
+    } else if ((rc = check_offsets(offsets, E, "gicp_align_batched"))) {
+        return rc;
+    }
+    if (B < 1) return set_error(GICP_EINVAL, "gicp_align_batched: B < 1");
+    if (!entry_reg && E != B) return set_error(GICP_EINVAL, "gicp_align_batched: entry_reg needed when E != B");
+    for (int e = 0; entry_reg && e < E; ++e)
+        if (entry_reg[e] < 0 || entry_reg[e] >= B) return set_error(GICP_EINVAL, "gicp_align_batched: entry_reg");
+    auto reg = [&](int e) { return entry_reg ? entry_reg[e] : e; };
+    const int64_t ns = offsets[E];
     if (!tgt || !tgt_cov || !T0 || !prm || !res || (ns > 0 && (!src || !src_cov)))
         return set_error(GICP_EINVAL, "gicp_align_batched: null pointer");
     if (prm->max_iter < 1) return set_error(GICP_EINVAL, "gicp_align_batched: max_iter < 1");
@@ -649,24 +663,24 @@ GICP_API int gicp_align_batched(const float* src, const float* src_cov, const in
     // device: batch scratch + two correspondence buffers + the sorted source copy
     BatchScratch bs;
     char* ex = nullptr;
-    if ((rc = batch_scratch(offsets, B, 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64, s, bs, &ex)))
+    if ((rc = batch_scratch(offsets, E, 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64, s, bs, &ex)))
         return rc;
     int32_t* corrA = (int32_t*)ex;
     int32_t* corrB = corrA + nsa;
     float* src_p = (float*)(((uintptr_t)(corrB + nsa) + 15) & ~(uintptr_t)15);
     float* cov_p = (float*)(((uintptr_t)(src_p + 3 * nsa) + 15) & ~(uintptr_t)15);  // float2 loads
-    if (ns > 0 && (rc = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s, bs.offs, B))) {
+    if (ns > 0 && (rc = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s, bs.offs, E))) {
         cudaFreeAsync(bs.base, s);
         return rc;
     }
-    // host-mapped: rows [B][32] | flag | pinned pose staging [B]
-    const size_t rows = (size_t)B * 32 * sizeof(double);
-    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)B * sizeof(Pose));
+    // host-mapped: entry rows [E][32] | flag | pinned pose staging [E]
+    const size_t rows = (size_t)E * 32 * sizeof(double);
+    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)E * sizeof(Pose));
     if (!mb) {
         cudaFreeAsync(bs.base, s);
         return set_error(GICP_ENOMEM, "gicp_align_batched: host-mapped buffer");
     }
-    const double* H = (const double*)mb->h;
+    double* He = (double*)mb->h;
     double* Hd = (double*)mb->d;
     volatile unsigned* hflag = (volatile unsigned*)(mb->h + rows);
     Pose* pst = (Pose*)(mb->h + rows + 256);
@@ -674,6 +688,8 @@ GICP_API int gicp_align_batched(const float* src, const float* src_cov, const in
     MappedOut mo;  // wait_mapped view of the flag
     mo.flag = hflag;
     bs.ls.flag = (volatile unsigned*)(mb->d + rows);
+    std::vector<double> Hr((size_t)B * 32, 0.0);  // registration rows of the last round
+    const double* H = Hr.data();
 
     struct St {
         double T[16], piv[3], lin29[29], Tn[16], pn[3], delta[6], Hm[36], b[6];
@@ -687,39 +703,56 @@ GICP_API int gicp_align_batched(const float* src, const float* src_cov, const in
         st[b].piv[0] = st[b].T[3];
         st[b].piv[1] = st[b].T[7];
         st[b].piv[2] = st[b].T[11];
-        if (offsets[b + 1] == offsets[b]) {  // no points: no correspondences
+        if (!reduce && !entry_reg && offsets[b + 1] == offsets[b]) {  // no points: no correspondences
             st[b].done = 1;
             st[b].rc = GICP_EDEGENERATE;
         }
     }
     // one evaluation round: `who` selects the registrations, pose(b) their pose;
-    // DUAL reads the current buffer as corr_old and writes the other one
+    // DUAL reads the current buffer as corr_old and writes the other one. Every
+    // rank calls `reduce` on every round (collectives stay matched) even when it
+    // launches nothing.
     auto round = [&](auto who, auto pose, int flags) -> int {
         int n_active = 0;
-        for (int b = 0; b < B; ++b) {
-            const bool a = who(b);
+        for (int e = 0; e < E; ++e) {
+            const int b = reg(e);
+            const bool a = who(b) && offsets[e + 1] > offsets[e];  // an empty entry has no block
             const double* Tp;
             const double* pp;
             pose(b, Tp, pp);
-            pst[b] = make_pose(Tp, pp);
-            pst[b].active = a;
-            pst[b].cur = st[b].cur;
+            pst[e] = make_pose(Tp, pp);
+            pst[e].active = a;
+            pst[e].cur = st[b].cur;
             n_active += a;
         }
-        if (n_active == 0) return GICP_OK;
-        int r = check_cuda(cudaMemcpyAsync(bs.poses, pst, B * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
-        if (r) return r;
-        BatchView bv;
-        bv.btab = bs.btab;
-        bv.offs = bs.offs;
-        bv.poses = bs.poses;
-        bv.n_scans = B;
-        bv.n_active = n_active;
-        bv.out_stride = 32;
-        bs.ls.seq = ++seq;
-        r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags, Hd, corrA, s,
-                                  bs.ls, corrB, bv, bs.nb);
-        return r ? r : wait_mapped(&mo, bs.ls.seq, s);
+        int r = GICP_OK;
+        if (n_active > 0) {
+            r = check_cuda(cudaMemcpyAsync(bs.poses, pst, E * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
+            if (r) return r;
+            BatchView bv;
+            bv.btab = bs.btab;
+            bv.offs = bs.offs;
+            bv.poses = bs.poses;
+            bv.n_scans = E;
+            bv.n_active = n_active;
+            bv.out_stride = 32;
+            bs.ls.seq = ++seq;
+            r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags, Hd, corrA, s,
+                                      bs.ls, corrB, bv, bs.nb);
+            if (!r) r = wait_mapped(&mo, bs.ls.seq, s);
+            if (r) return r;
+        }
+        for (int e = 0; e < E; ++e)  // rows of entries not launched this round are zero
+            if (!pst[e].active) std::memset(He + 32 * e, 0, 32 * sizeof(double));
+        if (reduce) {
+            if (reduce(He, E, Hr.data(), B, user) != 0)
+                return set_error(GICP_ECUDA, "gicp_align_batched: the reduce callback failed");
+        } else {
+            std::fill(Hr.begin(), Hr.end(), 0.0);
+            for (int e = 0; e < E; ++e)
+                for (int c = 0; c < 32; ++c) Hr[32 * reg(e) + c] += He[32 * e + c];
+        }
+        return GICP_OK;
     };
     auto at_T = [&](int b, const double*& Tp, const double*& pp) {
         Tp = st[b].T;
@@ -885,4 +918,19 @@ GICP_API int gicp_align_batched(const float* src, const float* src_cov, const in
     if (rc) return rc;
     return any_degenerate ? set_error(GICP_EDEGENERATE, "gicp_align_batched: a registration has < 6 correspondences")
                           : GICP_OK;
+}
+
+GICP_API int gicp_align_batched(const float* src, const float* src_cov, const int64_t* offsets, int B,
+                                gicp_index tgt, const float* tgt_cov, const double* T0,
+                                const gicp_align_params* prm, gicp_align_result* res, void* stream) {
+    return align_batched_impl(src, src_cov, offsets, B, nullptr, B, tgt, tgt_cov, T0, prm, res, nullptr, nullptr,
+                              stream);
+}
+
+GICP_API int gicp_align_batched_ex(const float* src, const float* src_cov, const int64_t* offsets, int E,
+                                   const int* entry_reg, int B, gicp_index tgt, const float* tgt_cov,
+                                   const double* T0, const gicp_align_params* prm, gicp_align_result* res,
+                                   gicp_reduce_fn reduce, void* user, void* stream) {
+    return align_batched_impl(src, src_cov, offsets, E, entry_reg, B, tgt, tgt_cov, T0, prm, res, reduce, user,
+                              stream);
 }

@@ -1,0 +1,101 @@
+"""Point-sharded batched registration (C4 across processes) on the
+GPU: each process linearises its chunks of every registration through
+gicp_align_batched_ex and one all_reduce per round combines them (gloo here:
+there is one GPU, both processes use it; the host-side collective never makes
+kernels wait on each other). World size 2 must reproduce world size 1 BITWISE
+(fixed chunking, chunk-ordered combine), and both must agree with the unsharded
+gicp_align_batched to rounding (different summation order)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.multiprocessing as mp  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCANS = [(0, 20000), (64, 7777), (200, 3000)]
+
+
+def _problem():
+    sys.path.insert(0, ROOT)
+    import gen
+    import paper_2308_07173_b200 as g
+    dev = torch.device("cuda:0")
+    D = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    mp_ = gen.racetrack_map(2_000_000, 1)
+    im = g.build_index(D(mp_), 0.5)
+    _, _, cm = g.knn_cov_self(im, 20, 1e-3, with_nbr=False)
+    g.attach_cov(im, cm)
+    srcs, covs, T0 = [], [], []
+    for i, n in SCANS:
+        sc, T, Tp = gen.config_c4_scan(i, n)
+        sd = D(sc)
+        isc = g.build_index(sd, 0.0)
+        _, _, cs = g.knn_cov_self(isc, 20, 1e-3, with_nbr=False)
+        isc.free()
+        srcs.append(sd)
+        covs.append(cs)
+        T0.append(Tp)
+    offs = np.concatenate([[0], np.cumsum([s.shape[0] for s in srcs])]).astype(np.int64)
+    return g, im, cm, torch.cat(srcs).contiguous(), torch.cat(covs).contiguous(), offs, np.array(T0)
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    from paper_2308_07173_b200 import sharding
+    g, im, cm, src, cov, offs, T0 = _problem()
+    Ts, infos = sharding.align_batched_sharded(g, src, cov, offs, im, cm, T0)
+    q.put((rank, Ts, [(i.iterations, i.converged, i.error, i.inliers) for i in infos]))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (T, inf)) for r, T, inf in (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_sharded_align_world2_is_bitwise_world1():
+    r1 = _run(1)
+    r2 = _run(2)
+    T1, i1 = r1[0]
+    for r in (0, 1):
+        T2, i2 = r2[r]
+        assert np.array_equal(T2, T1)
+        assert i2 == i1
+    # against the unsharded batched align (registration-wide summation order)
+    g, im, cm, src, cov, offs, T0 = _problem()
+    Tu, iu = g.align_batched(src, cov, offs, im, cm, T0)
+    for b in range(len(SCANS)):
+        assert np.linalg.norm(T1[b][:3, 3] - Tu[b][:3, 3]) <= 1e-3
+        c = (np.trace(T1[b][:3, :3] @ Tu[b][:3, :3].T) - 1) / 2
+        assert np.arccos(min(1.0, c)) <= 1e-4
+        assert i1[b][3] > 0 and abs(i1[b][3] - iu[b].inliers) <= 0.001 * iu[b].inliers

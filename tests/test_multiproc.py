@@ -91,3 +91,61 @@ def test_gloo_world2_matches_single_process_bitwise():
     whole, ab, _ = oracle.linearize(src, cs, tgt, ct, T0, 1.0, pivot=T0[:3, 3])
     assert single[28] == whole[28]
     assert np.all(np.abs(single[:28] - whole[:28]) <= 1e-12 * ab[:28] + 1e-300)
+
+
+# --- point-sharded batched registration (C4): the reduce callback's host logic ---
+
+SIZES = [20000, 0, 7777, 300, 256]
+
+
+def _chunk_rows(b, c):
+    """Deterministic stand-in for one chunk's 32-value row (what one GPU launch
+    would produce for chunk c of registration b): wide dynamic range so any
+    change of summation order shows in the bits."""
+    rng = np.random.default_rng(1000 * b + c)
+    return rng.standard_normal(32) * 10.0 ** rng.integers(-8, 8, 32)
+
+
+def _reduce_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sh = _load_sharding()
+    entries = sh.registration_chunks(SIZES, rank, world)
+    rows = np.stack([_chunk_rows(b, c) for (b, c, _, _) in entries]) if entries else np.zeros((0, 32))
+    out = sh.make_chunk_reducer(entries, len(SIZES))(rows)
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_chunk_reducer_is_world_size_independent(world):
+    """Every rank gets the chunk-ordered sum of every registration's chunk rows,
+    bitwise equal to the single-process combine, for world sizes 2 and 3."""
+    sh = _load_sharding()
+    B = len(SIZES)
+    table = np.zeros((B * sh.NUM_CHUNKS, 32))
+    for (b, c, _, _) in sh.registration_chunks(SIZES, 0, 1):
+        table[b * sh.NUM_CHUNKS + c] = _chunk_rows(b, c)
+    single = sh.combine_chunk_table(table, B)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert np.array_equal(res[r], single)
+    # chunks cover every point once; empty registrations have no entries
+    for w in (1, 2, 4, 8):
+        cov = {b: 0 for b in range(B)}
+        for r in range(w):
+            for (b, c, lo, hi) in sh.registration_chunks(SIZES, r, w):
+                assert c % w == r and hi > lo
+                cov[b] += hi - lo
+        assert [cov[b] for b in range(B)] == SIZES
