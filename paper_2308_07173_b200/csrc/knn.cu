@@ -42,6 +42,9 @@ __device__ unsigned long long g_kprof[64];  // 16 counters per level 0, 1, 2, >=
 #else
 #define KPROF(x)
 #endif
+#ifndef GICP_KNN_REGSORT
+#define GICP_KNN_REGSORT 1  // sort the final K keys in registers
+#endif
 #ifndef GICP_KNN_MINB
 #define GICP_KNN_MINB 6
 #endif
@@ -85,11 +88,18 @@ constexpr SortNet make_sortnet(int N) {
     return r;
 }
 
-template <int N>
+template <int N, bool FULL = false>
 __device__ __forceinline__ void sort_network(unsigned long long (&v)[N]) {
     constexpr SortNet net = make_sortnet(N);
 #pragma unroll
-    for (int c = 0; c < net.n; ++c) cas_hi(v[net.a[c]], v[net.b[c]]);
+    for (int c = 0; c < net.n; ++c) {
+        unsigned long long& a = v[net.a[c]];
+        unsigned long long& b = v[net.b[c]];
+        const bool sw = FULL ? b < a : hi32(b) < hi32(a);
+        const unsigned long long t = a;
+        a = sw ? b : a;
+        b = sw ? t : b;
+    }
 }
 
 // the same network on a shared-memory column (stride kBlock) -- keeps the K keys
@@ -396,8 +406,21 @@ __device__ __forceinline__ int knn_fast(const float4* __restrict__ pts, const Gr
     if (!EXACT && tie == hi32(top)) return 2;
     // sort the K keys in place (slots K..KCAP-1 temporarily +inf; the caller
     // restores the 0-key padding after emitting the row)
+#if GICP_KNN_REGSORT
+    {
+        // the K keys through registers: the network's compare-exchanges are ALU
+        // selects instead of dependent shared-memory round trips
+        unsigned long long kk[KCAP];
+#pragma unroll
+        for (int r = 0; r < KCAP; ++r) kk[r] = r < K ? HSLOT(r) : kEmptyKey;
+        sort_network<KCAP, EXACT>(kk);
+#pragma unroll
+        for (int r = 0; r < KCAP; ++r) HSLOT(r) = kk[r];
+    }
+#else
     for (int r = K; r < KCAP; ++r) HSLOT(r) = kEmptyKey;
     sort_network_smem<KCAP, kBlock, EXACT>(Hl);
+#endif
     if (EXACT) return 0;
     bool dup = false;
     unsigned prev = hi32(HSLOT(0));
