@@ -63,6 +63,9 @@ def lib():
         L.oracle_se3_exp.argtypes = [P, P]
         L.oracle_se3_exp.restype = None
         L.oracle_ldlt_solve6.argtypes = [P, P, P]
+        L.oracle_kernel_eval.argtypes = [i32, f64, f64, f64, i32, P, P]
+        L.oracle_kernel_eval.restype = f64
+        L.oracle_covariance_kd.argtypes = [P, i64, P, P, i64, i32, i32, f64, f64, f64, i32, P, i32, f64, P, P, i32]
         L.oracle_align.argtypes = [P, P, i64, P, P, i64, P, ctypes.POINTER(AlignParams),
                                    ctypes.POINTER(AlignResult), i32]
         _lib = L
@@ -144,6 +147,35 @@ def linearize(src, src_cov, tgt, tgt_cov, T, max_corr_dist=1.0, corr=None, nthre
     if rc != OK:
         raise OracleError(rc, "oracle_linearize")
     return out, ab, corr
+
+
+KD_UNIFORM, KD_RBF, KD_GAUSSIAN, KD_POLYNOMIAL, KD_HI, KD_LAPLACIAN = range(6)
+REG_PLANE, REG_MIN_EIG, REG_NORMALIZED_MIN_EIG = range(3)
+
+
+def kernel_eval(kind, x, y, sigma=1.0, alpha=1.0, c=0.0, d=2):
+    """O5: one Table I kernel value K(x, y) (x = query, y = neighbour)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return float(lib().oracle_kernel_eval(int(kind), float(sigma), float(alpha), float(c), int(d), _ptr(x), _ptr(y)))
+
+
+def covariance_kd(xyz, nbr, kind, q=None, sigma=1.0, alpha=1.0, c=0.0, d=2, origin=(0.0, 0.0, 0.0),
+                  reg=REG_PLANE, eps=1e-3, nthreads=0):
+    """O6: kernel-weighted covariance, (cov fp64 [m,6], gap [m])."""
+    xyz = _f32(xyz)
+    nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+    m, k = nbr.shape
+    qq = None if q is None else _f32(q)
+    o = np.ascontiguousarray(origin, dtype=np.float64)
+    cov = np.empty((m, 6))
+    gap = np.empty(m)
+    rc = lib().oracle_covariance_kd(_ptr(xyz), xyz.shape[0], None if qq is None else _ptr(qq), _ptr(nbr), m, k,
+                                    int(kind), float(sigma), float(alpha), float(c), int(d), _ptr(o), int(reg),
+                                    float(eps), _ptr(cov), _ptr(gap), nthreads)
+    if rc != OK:
+        raise OracleError(rc, "oracle_covariance_kd")
+    return cov, gap
 
 
 def se3_exp(delta):

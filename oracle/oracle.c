@@ -21,6 +21,10 @@
  *                          and the inverse -- DESIGN.md readings R1/R2), J for the
  *                          left perturbation T <- Exp(delta) T, Neumaier sums.
  *   O4 oracle_align        host Levenberg-Marquardt on O3 (T = argmin ..., l.396-402).
+ *   O5 oracle_kernel_eval  Table I kernel descriptors (l.420-435), written out.
+ *   O6 oracle_covariance_kd  kernel-weighted mean / scatter + PLANE / MIN_EIG /
+ *                          NORMALIZED_MIN_EIG regularisation (SURVEY §8(f) #1,
+ *                          "covariance computation using the kernel descriptors" l.413).
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py against
  * closed forms, LAPACK, an fp32-FMA emulation, finite differences and known
@@ -275,6 +279,143 @@ int oracle_covariance(const float* xyz, int64_t n, const int32_t* nbr, int64_t m
             s6[4] = S[5];
             s6[5] = S[8];
         }
+    }
+    return bad ? ORACLE_EINVAL : ORACLE_OK;
+}
+
+/* -------------------------------------------------------------------------- */
+/* O5: kernel descriptors (Table I, l.420-435)     */
+/* -------------------------------------------------------------------------- */
+
+/* Table I, written out (readings R19-R21):
+ *   RBF         exp(-||x - y||^2 * sigma)       (verbatim: times sigma)
+ *   Gaussian    exp(-||x - y||^2 / (2 sigma^2))
+ *   Polynomial  (alpha <x, y> + c)^d
+ *   HI          sum_i min(x_i, y_i) / sum_i x_i  (x, y non-negative)
+ *   Laplacian   exp(-||x - y|| / sigma)
+ * kind 0 = uniform (weight 1). x is the query point, y the neighbour. */
+enum { KD_UNIFORM = 0, KD_RBF = 1, KD_GAUSSIAN = 2, KD_POLYNOMIAL = 3, KD_HI = 4, KD_LAPLACIAN = 5 };
+
+double oracle_kernel_eval(int kind, double sigma, double alpha, double c, int d, const double* x, const double* y) {
+    double d2 = 0.0, dot = 0.0, smin = 0.0, sx = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        d2 += (x[a] - y[a]) * (x[a] - y[a]);
+        dot += x[a] * y[a];
+        smin += x[a] < y[a] ? x[a] : y[a];
+        sx += x[a];
+    }
+    switch (kind) {
+        case KD_UNIFORM: return 1.0;
+        case KD_RBF: return exp(-d2 * sigma);
+        case KD_GAUSSIAN: return exp(-d2 / (2.0 * sigma * sigma));
+        case KD_POLYNOMIAL: return pow(alpha * dot + c, (double)d);
+        case KD_HI: return sx > 0.0 ? smin / sx : 1.0;
+        case KD_LAPLACIAN: return exp(-sqrt(d2) / sigma);
+        default: return NAN;
+    }
+}
+
+/* O6: kernel-weighted covariance with a choice of regularisation.
+ *   w_j = max(0, K(q_i - o, x_j - o)), HI on max(0, .) components (R20);
+ *   all w_j == 0 -> uniform weights (R19);
+ *   mu = sum w x / sum w, S = sum w (x - mu)(x - mu)^T / sum w   (R19);
+ *   reg 0 PLANE: V diag(eps,1,1) V^T (lam3 == 0 -> n = +z, R11)
+ *   reg 1 MIN_EIG: V diag(max(lam_i, eps)) V^T
+ *   reg 2 NORMALIZED_MIN_EIG: V diag(max(lam_i / lam3, eps)) V^T (lam3 == 0 -> eps I)  (R21)
+ * q = NULL uses xyz[i] as the query of row i (m <= n). */
+int oracle_covariance_kd(const float* xyz, int64_t n, const float* q, const int32_t* nbr, int64_t m, int k, int kind,
+                         double sigma, double alpha, double c, int degree, const double* origin, int reg, double eps,
+                         double* cov, double* gap, int nthreads) {
+    if (!xyz || !nbr || !cov || n <= 0 || m < 0 || (!q && m > n)) return ORACLE_EINVAL;
+    if (k < 1 || k > 32 || k > n) return ORACLE_EK;
+    if (kind < 0 || kind > 5 || reg < 0 || reg > 2) return ORACLE_EINVAL;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    const double o[3] = {origin ? origin[0] : 0.0, origin ? origin[1] : 0.0, origin ? origin[2] : 0.0};
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t i = 0; i < m; ++i) {
+        double X[32][3], w[32];
+        const float* qi = q ? q + 3 * i : xyz + 3 * i;
+        double Q[3];
+        for (int a = 0; a < 3; ++a) {
+            Q[a] = (double)qi[a] - o[a];
+            if (kind == KD_HI && Q[a] < 0.0) Q[a] = 0.0;
+        }
+        double W = 0.0;
+        for (int j = 0; j < k; ++j) {
+            int32_t id = nbr[i * k + j];
+            if (id < 0 || id >= n) {
+                bad = 1;
+                id = 0;
+            }
+            double Y[3];
+            for (int a = 0; a < 3; ++a) {
+                X[j][a] = (double)xyz[3 * (int64_t)id + a];
+                Y[a] = X[j][a] - o[a];
+                if (kind == KD_HI && Y[a] < 0.0) Y[a] = 0.0;
+            }
+            double wj = oracle_kernel_eval(kind, sigma, alpha, c, degree, Q, Y);
+            if (!(wj > 0.0)) wj = 0.0; /* also NaN */
+            w[j] = wj;
+            W += wj;
+        }
+        if (!(W > 0.0)) {
+            for (int j = 0; j < k; ++j) w[j] = 1.0;
+            W = (double)k;
+        }
+        double mu[3] = {0, 0, 0};
+        for (int j = 0; j < k; ++j)
+            for (int a = 0; a < 3; ++a) mu[a] += w[j] * X[j][a];
+        for (int a = 0; a < 3; ++a) mu[a] /= W;
+        double S[9] = {0};
+        for (int j = 0; j < k; ++j)
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) S[3 * a + b] += w[j] * (X[j][a] - mu[a]) * (X[j][b] - mu[b]);
+        for (int a = 0; a < 9; ++a) S[a] /= W;
+        double lam[3], V[9];
+        oracle_jacobi3(S, lam, V);
+        double lw[3];
+        int eye = 0;
+        if (reg == 0) {
+            if (lam[2] == 0.0) { /* S = 0: n = +z (R11); columns (0,0,1), (0,1,0), (1,0,0) */
+                const double P[9] = {0, 0, 1, 0, 1, 0, 1, 0, 0};
+                for (int a = 0; a < 9; ++a) V[a] = P[a];
+            }
+            lw[0] = eps;
+            lw[1] = 1.0;
+            lw[2] = 1.0;
+        } else if (reg == 1) {
+            for (int a = 0; a < 3; ++a) lw[a] = lam[a] > eps ? lam[a] : eps;
+        } else {
+            if (lam[2] > 0.0) {
+                for (int a = 0; a < 3; ++a) lw[a] = lam[a] / lam[2] > eps ? lam[a] / lam[2] : eps;
+            } else {
+                eye = 1;
+            }
+        }
+        double C[9];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                double s = 0.0;
+                if (eye) {
+                    s = (a == b) ? eps : 0.0;
+                } else {
+                    for (int cc = 0; cc < 3; ++cc) s += V[3 * a + cc] * lw[cc] * V[3 * b + cc];
+                }
+                C[3 * a + b] = s;
+            }
+        double* out = cov + 6 * i;
+        out[0] = C[0];
+        out[1] = C[1];
+        out[2] = C[2];
+        out[3] = C[4];
+        out[4] = C[5];
+        out[5] = C[8];
+        if (gap) gap[i] = (lam[2] == 0.0) ? 0.0 : (lam[1] - lam[0]) / lam[2];
     }
     return bad ? ORACLE_EINVAL : ORACLE_OK;
 }
