@@ -141,6 +141,38 @@ int gicp_covariances(const float* xyz, int64_t n, const int32_t* nbr, int64_t m,
 int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, float* d2, float* cov, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * gicp_covariances_kd -- kernel-descriptor weighted covariances (PAPER.md l.413
+ * "covariance computation using the kernel descriptors", Table I l.420-435;
+ * SURVEY.md §8(f) #1; readings R19-R21):
+ *   w_j = max(0, K(q_i - o, x_j - o)) for the K of Table I (x = the query):
+ *     RBF exp(-||x-y||^2 * sigma) (verbatim), Gaussian exp(-||x-y||^2/(2 sigma^2)),
+ *     Polynomial (alpha <x,y> + c)^degree, HI sum min(x_i,y_i) / sum x_i on the
+ *     non-negative parts, Laplacian exp(-||x-y||/sigma), or uniform;
+ *   all weights 0 -> uniform; mu = sum w x / sum w; S = sum w (x-mu)(x-mu)^T / sum w;
+ *   reg PLANE: V diag(eps,1,1) V^T (as gicp_covariances), MIN_EIG:
+ *   V diag(max(lam, eps)) V^T, NORMALIZED_MIN_EIG: V diag(max(lam/lam_max, eps)) V^T.
+ *   xyz [n][3] cloud the neighbours index, q [m][3] queries or NULL (row i's query
+ *   is xyz[i], m <= n), nbr [m][k], cov [m][6] out (device). params (host).
+ * Errors: EINVAL (null, n <= 0, m < 0, sigma <= 0 for the distance kernels,
+ * degree < 1 or > 16 for Polynomial, eps out of (0, 1], unknown kind / reg), EK.
+ * ------------------------------------------------------------------------- */
+enum { GICP_KD_UNIFORM = 0, GICP_KD_RBF = 1, GICP_KD_GAUSSIAN = 2, GICP_KD_POLYNOMIAL = 3, GICP_KD_HI = 4,
+       GICP_KD_LAPLACIAN = 5 };
+enum { GICP_REG_PLANE = 0, GICP_REG_MIN_EIG = 1, GICP_REG_NORMALIZED_MIN_EIG = 2 };
+typedef struct {
+    int kernel;        /* GICP_KD_* */
+    float sigma;       /* RBF / Gaussian / Laplacian */
+    float alpha, c;    /* Polynomial */
+    int degree;        /* Polynomial, 1..16 */
+    float origin[3];   /* o: Polynomial / HI coordinates are x - o */
+    int reg;           /* GICP_REG_* */
+    float eps;         /* 1e-3 */
+} gicp_cov_params;
+
+int gicp_covariances_kd(const float* xyz, int64_t n, const float* q, const int32_t* nbr, int64_t m, int k,
+                        const gicp_cov_params* params /* host */, float* cov, void* stream);
+
+/* ---------------------------------------------------------------------------
  * gicp_linearize -- one GICP linearisation at pose T (PAPER.md eq_trans_err
  * l.382-387, eq_trans_likelihood l.396-402; readings R1-R4, R12):
  *   p'  = R p + t in fp64 (a-th row: fma(R_a2, p_z, fma(R_a1, p_y, fma(R_a0, p_x, t_a))))

@@ -61,6 +61,17 @@ _lib.gicp_knn.argtypes = [_P, _P, _i64, _i32, _P, _P, _P]
 _lib.gicp_knn_self.argtypes = [_P, _i32, _P, _P, _P]
 _lib.gicp_covariances.argtypes = [_P, _i64, _P, _i64, _i32, _f32, _P, _P]
 _lib.gicp_knn_cov_self.argtypes = [_P, _i32, _f32, _P, _P, _P, _P]
+
+
+class CovParams(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int), ("sigma", ctypes.c_float), ("alpha", ctypes.c_float),
+                ("c", ctypes.c_float), ("degree", ctypes.c_int), ("origin", ctypes.c_float * 3),
+                ("reg", ctypes.c_int), ("eps", ctypes.c_float)]
+
+
+_lib.gicp_covariances_kd.argtypes = [_P, _i64, _P, _P, _i64, _i32, ctypes.POINTER(CovParams), _P, _P]
+KERNELS = {"uniform": 0, "rbf": 1, "gaussian": 2, "polynomial": 3, "hi": 4, "laplacian": 5}
+REGS = {"plane": 0, "min_eig": 1, "normalized_min_eig": 2}
 _lib.gicp_linearize.argtypes = [_P, _P, _i64, _P, _P, _P, _P, _f32, _i32, _P, _P, _P]
 _lib.gicp_align.argtypes = [_P, _P, _i64, _P, _P, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
                             _P]
@@ -74,7 +85,7 @@ _lib.gicp_align_batched_ex.argtypes = [_P, _P, _P, _i32, _P, _i32, _P, _P, _P, c
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
-           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex"]
+           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd"]
 
 
 class GicpError(RuntimeError):
@@ -180,6 +191,25 @@ def covariances(xyz: torch.Tensor, nbr: torch.Tensor, eps: float = 1e-3, out=Non
     m, k = nbr.shape
     cov = out if out is not None else torch.empty((m, 6), dtype=torch.float32, device=xyz.device)
     _check(_lib.gicp_covariances(_dptr(xyz), xyz.shape[0], _dptr(nbr), m, k, float(eps), _dptr(cov), _stream()))
+    return cov
+
+
+def covariances_kd(xyz: torch.Tensor, nbr: torch.Tensor, kernel="laplacian", sigma=1.0, q=None, alpha=1.0, c=0.0,
+                   degree=2, origin=(0.0, 0.0, 0.0), reg="plane", eps: float = 1e-3, out=None):
+    """Kernel-descriptor weighted covariances (gicp_covariances_kd, Table I).
+    q: queries [m,3] (default: row i's query is xyz[i]). Returns cov float32 [m,6]."""
+    xyz = _pts(xyz, "xyz")
+    if nbr.dtype != torch.int32 or nbr.dim() != 2:
+        raise ValueError("nbr must be int32 [m, k]")
+    nbr = nbr.contiguous()
+    m, k = nbr.shape
+    qq = None if q is None else _pts(q, "q")
+    p = CovParams(KERNELS[kernel] if isinstance(kernel, str) else int(kernel), float(sigma), float(alpha), float(c),
+                  int(degree), (ctypes.c_float * 3)(*[float(v) for v in origin]),
+                  REGS[reg] if isinstance(reg, str) else int(reg), float(eps))
+    cov = out if out is not None else torch.empty((m, 6), dtype=torch.float32, device=xyz.device)
+    _check(_lib.gicp_covariances_kd(_dptr(xyz), xyz.shape[0], None if qq is None else _dptr(qq), _dptr(nbr), m, k,
+                                    ctypes.byref(p), _dptr(cov), _stream()))
     return cov
 
 

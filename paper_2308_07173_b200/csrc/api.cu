@@ -284,6 +284,33 @@ GICP_API int gicp_covariances(const float* xyz, int64_t n, const int32_t* nbr, i
     return launch_covariances(xyz, n, nbr, m, k, eps, cov, (cudaStream_t)stream);
 }
 
+GICP_API int gicp_covariances_kd(const float* xyz, int64_t n, const float* q, const int32_t* nbr, int64_t m, int k,
+                                 const gicp_cov_params* p, float* cov, void* stream) {
+    if (!p) return set_error(GICP_EINVAL, "gicp_covariances_kd: null params");
+    if (n <= 0 || m < 0) return set_error(GICP_EINVAL, "gicp_covariances_kd: n must be > 0 and m >= 0");
+    if (!q && m > n) return set_error(GICP_EINVAL, "gicp_covariances_kd: m > n without queries");
+    int rc = check_k(k, n, "gicp_covariances_kd");
+    if (rc) return rc;
+    if (p->kernel < GICP_KD_UNIFORM || p->kernel > GICP_KD_LAPLACIAN)
+        return set_error(GICP_EINVAL, "gicp_covariances_kd: unknown kernel");
+    if (p->reg < GICP_REG_PLANE || p->reg > GICP_REG_NORMALIZED_MIN_EIG)
+        return set_error(GICP_EINVAL, "gicp_covariances_kd: unknown regularisation");
+    if (!(p->eps > 0.0f && p->eps <= 1.0f)) return set_error(GICP_EINVAL, "gicp_covariances_kd: eps must be in (0, 1]");
+    const bool dist = p->kernel == GICP_KD_RBF || p->kernel == GICP_KD_GAUSSIAN || p->kernel == GICP_KD_LAPLACIAN;
+    if (dist && !(p->sigma > 0.0f && std::isfinite(p->sigma)))
+        return set_error(GICP_EINVAL, "gicp_covariances_kd: sigma must be finite and > 0");
+    if (p->kernel == GICP_KD_POLYNOMIAL && (p->degree < 1 || p->degree > 16 || !std::isfinite(p->alpha) ||
+                                            !std::isfinite(p->c)))
+        return set_error(GICP_EINVAL, "gicp_covariances_kd: polynomial degree 1..16, finite alpha / c");
+    if (!(std::isfinite(p->origin[0]) && std::isfinite(p->origin[1]) && std::isfinite(p->origin[2])))
+        return set_error(GICP_EINVAL, "gicp_covariances_kd: non-finite origin");
+    if (m == 0) return GICP_OK;
+    if (!xyz || !nbr || !cov) return set_error(GICP_EINVAL, "gicp_covariances_kd: null pointer");
+    const CovKD kd{p->kernel, p->sigma, p->alpha, p->c, p->degree, p->origin[0], p->origin[1], p->origin[2], p->reg,
+                   p->eps};
+    return launch_covariances_kd(xyz, n, q, nbr, m, k, kd, cov, (cudaStream_t)stream);
+}
+
 GICP_API int gicp_knn_cov_self(gicp_index idx, int k, float eps, int32_t* nbr, float* d2, float* cov, void* stream) {
     if (!idx || !cov) return set_error(GICP_EINVAL, "gicp_knn_cov_self: null pointer");
     int rc = check_k(k, idx->n, "gicp_knn_cov_self");

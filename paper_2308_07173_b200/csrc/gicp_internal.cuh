@@ -180,6 +180,17 @@ int check_cuda(cudaError_t e, const char* what);
 int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gicp_index* out);
 int launch_knn_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, cudaStream_t s);
 int launch_knn(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, cudaStream_t s);
+// kernel-descriptor weighted covariance parameters (gicp_cov_params, device copy)
+struct CovKD {
+    int kind;
+    float sigma, alpha, c;
+    int degree;
+    float ox, oy, oz;
+    int reg;
+    float eps;
+};
+int launch_covariances_kd(const float* xyz, int64_t n, const float* q, const int32_t* nbr, int64_t m, int k,
+                          const CovKD& p, float* cov, cudaStream_t s);
 int launch_covariances(const float* xyz, int64_t n, const int32_t* nbr, int64_t m, int k, float eps, float* cov,
                        cudaStream_t s);
 // preallocated linearize scratch (gicp_align): block partials + done counter

@@ -362,3 +362,41 @@ def test_c5_stress_sampled(orc):
     oc, gap, _ = orc.covariance(mp, on)
     assert_cov_parity(hc[rows], oc, gap, masked_frac_max=0.05)
     idx.free()
+
+
+# ---------------------------------------------------------------------------
+# kernel-descriptor covariances: every Table I kernel x every
+# regularisation against the oracle on a racetrack section (oracle neighbours)
+@pytest.mark.parametrize("kernel,sigma", [("uniform", 1.0), ("rbf", 4.0), ("gaussian", 0.3), ("polynomial", 1.0),
+                                          ("hi", 1.0), ("laplacian", 0.5)])
+@pytest.mark.parametrize("reg", ["plane", "min_eig", "normalized_min_eig"])
+def test_covariances_kd_vs_oracle(orc, kernel, sigma, reg):
+    mp = gen.racetrack_map(2_000_000, 1)
+    sel = np.nonzero((np.abs(mp[:, 0] - 150.0) < 25.0) & (mp[:, 1] > 0))[0][:20000]
+    xyz = np.ascontiguousarray(mp[sel])
+    nbr, _ = orc.knn(xyz, xyz, 20)
+    o = xyz.min(axis=0).astype(np.float64)
+    kinds = dict(uniform=0, rbf=1, gaussian=2, polynomial=3, hi=4, laplacian=5)
+    regs = dict(plane=0, min_eig=1, normalized_min_eig=2)
+    ref, gap = orc.covariance_kd(xyz, nbr, kinds[kernel], sigma=sigma, alpha=0.01, c=1.0, d=2, origin=o,
+                                 reg=regs[reg])
+    got = H(g.covariances_kd(D(xyz), D(nbr), kernel, sigma=sigma, alpha=0.01, c=1.0, degree=2, origin=o, reg=reg))
+    assert np.all(np.isfinite(got))
+    m = gap >= 1e-2
+    assert m.mean() > 0.95
+    scale = np.abs(ref[m]).max(axis=1, keepdims=True)
+    assert (np.abs(got[m] - ref[m]) / np.maximum(scale, 1e-12)).max() <= 1e-4
+
+
+def test_covariances_kd_external_queries_and_errors(orc):
+    xyz = gen.uniform_cloud(5000, 11, lo=-3.0, hi=3.0)
+    q = gen.uniform_cloud(700, 12, lo=-3.0, hi=3.0)
+    nbr, _ = orc.knn(xyz, q, 16)
+    ref, gap = orc.covariance_kd(xyz, nbr, 5, q=q, sigma=0.7)
+    got = H(g.covariances_kd(D(xyz), D(nbr), "laplacian", sigma=0.7, q=D(q)))
+    m = gap >= 1e-2
+    assert np.abs(got[m] - ref[m]).max() <= 1e-4
+    with pytest.raises(g.GicpError):
+        g.covariances_kd(D(xyz), D(nbr), "laplacian", sigma=0.0, q=D(q))
+    with pytest.raises(g.GicpError):
+        g.covariances_kd(D(xyz), D(nbr), "polynomial", degree=0, q=D(q))
