@@ -104,6 +104,27 @@ def c5():
                       "gen_s": gen_s}))
 
 
+
+
+def kd():
+    """kernel-descriptor covariances on the C3 map (2M, k=20), per kernel x reg."""
+    mp = gen.racetrack_map(2_000_000, 1)
+    md = D(mp)
+    im = g.build_index(md, 0.5)
+    nbr, _, _ = g.knn_cov_self(im, 20)
+    o = tuple(float(v) for v in mp.min(axis=0))
+    cov = torch.empty((mp.shape[0], 6), dtype=torch.float32, device=DEV)
+    res = {}
+    ms0, _ = timed(lambda: g.covariances(md, nbr, 1e-3, out=cov))
+    res["unweighted_plane"] = ms0
+    for kern, sig in (("laplacian", 0.5), ("rbf", 4.0), ("gaussian", 0.3), ("polynomial", 1.0), ("hi", 1.0)):
+        for reg in ("plane", "min_eig"):
+            ms, _ = timed(lambda: g.covariances_kd(md, nbr, kern, sigma=sig, alpha=0.01, c=1.0, origin=o, reg=reg,
+                                                   out=cov))
+            res[f"{kern}_{reg}"] = ms
+    print(json.dumps({"workload": "kernel-descriptor covariances, C3 map 2M x k=20 (ms per call)", **res}))
+
+
 if __name__ == "__main__":
     args = sys.argv[1:] or ["c2", "c4", "c5"]
     i = 0
@@ -119,4 +140,6 @@ if __name__ == "__main__":
             c4(B)
         elif a == "c5":
             c5()
+        elif a == "kd":
+            kd()
         i += 1
