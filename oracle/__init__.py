@@ -66,6 +66,9 @@ def lib():
         L.oracle_kernel_eval.argtypes = [i32, f64, f64, f64, i32, P, P]
         L.oracle_kernel_eval.restype = f64
         L.oracle_covariance_kd.argtypes = [P, i64, P, P, i64, i32, i32, f64, f64, f64, i32, P, i32, f64, P, P, i32]
+        L.oracle_linearize_vgicp.argtypes = [P, P, i64, P, P, i64, f32, P, P, i32, P, P]
+        L.oracle_align_vgicp.argtypes = [P, P, i64, P, P, i64, f32, i32, P, ctypes.POINTER(AlignParams),
+                                         ctypes.POINTER(AlignResult)]
         L.oracle_align.argtypes = [P, P, i64, P, P, i64, P, ctypes.POINTER(AlignParams),
                                    ctypes.POINTER(AlignResult), i32]
         _lib = L
@@ -176,6 +179,37 @@ def covariance_kd(xyz, nbr, kind, q=None, sigma=1.0, alpha=1.0, c=0.0, d=2, orig
     if rc != OK:
         raise OracleError(rc, "oracle_covariance_kd")
     return cov, gap
+
+
+def linearize_vgicp(src, src_cov, tgt, tgt_cov, T, res=1.0, mode=7, pivot=None):
+    """O7: voxelized GICP linearisation -> (out29, absum29)."""
+    src, tgt = _f32(src), _f32(tgt)
+    src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    piv = None if pivot is None else np.ascontiguousarray(pivot, dtype=np.float64)
+    out = np.empty(29)
+    ab = np.empty(29)
+    rc = lib().oracle_linearize_vgicp(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
+                                      float(res), _ptr(T), None if piv is None else _ptr(piv), int(mode), _ptr(out),
+                                      _ptr(ab))
+    if rc != OK:
+        raise OracleError(rc, "oracle_linearize_vgicp")
+    return out, ab
+
+
+def align_vgicp(src, src_cov, tgt, tgt_cov, T0, res=1.0, mode=7, max_iter=64, rot_eps=1e-6, trans_eps=1e-5):
+    """O8: LM on O7 -> dict(T, iterations, converged, error, inliers)."""
+    src, tgt = _f32(src), _f32(tgt)
+    src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
+    T0 = np.ascontiguousarray(T0, dtype=np.float64)
+    p = AlignParams(max_iter, 1, rot_eps, trans_eps, 1.0)
+    r = AlignResult()
+    rc = lib().oracle_align_vgicp(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
+                                  float(res), int(mode), _ptr(T0), ctypes.byref(p), ctypes.byref(r))
+    if rc != OK:
+        raise OracleError(rc, "oracle_align_vgicp")
+    return dict(T=np.array(r.T[:]).reshape(4, 4), iterations=r.iterations, converged=bool(r.converged),
+                error=r.error, inliers=r.inliers)
 
 
 def se3_exp(delta):

@@ -22,6 +22,9 @@
  *                          left perturbation T <- Exp(delta) T, Neumaier sums.
  *   O4 oracle_align        host Levenberg-Marquardt on O3 (T = argmin ..., l.396-402).
  *   O5 oracle_kernel_eval  Table I kernel descriptors (l.420-435), written out.
+ *   O7 oracle_linearize_vgicp / O8 oracle_align_vgicp  voxelized GICP (l.419):
+ *                          voxel N, mean, mean covariance; pairs with the voxels
+ *                          around fl32(T p); N-weighted Mahalanobis terms.
  *   O6 oracle_covariance_kd  kernel-weighted mean / scatter + PLANE / MIN_EIG /
  *                          NORMALIZED_MIN_EIG regularisation (SURVEY §8(f) #1,
  *                          "covariance computation using the kernel descriptors" l.413).
@@ -864,5 +867,277 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
     res->converged = converged;
     res->error = err;
     res->inliers = inl;
+    return rc;
+}
+
+/* -------------------------------------------------------------------------- */
+/* O7/O8: voxelized GICP ("extends and optimizes the Voxelized-  */
+/* GICP"; readings R22-R23)                       */
+/* -------------------------------------------------------------------------- */
+
+/* voxel of a point: c_a = floor(fl32(fl32(x_a - o_a) * fl32(1/res))), o = the
+ * target's per-axis minimum (the index's grid). */
+static void vox_coord(const float* x, const float o[3], float inv, int64_t c[3]) {
+    for (int a = 0; a < 3; ++a) {
+        volatile float d = x[a] - o[a];
+        volatile float t = d * inv;
+        c[a] = (int64_t)floor((double)t);
+    }
+}
+
+typedef struct {
+    int64_t c[3];
+    int64_t idx; /* target point */
+} vox_item;
+
+static int vox_cmp(const void* pa, const void* pb) {
+    const vox_item* a = (const vox_item*)pa;
+    const vox_item* b = (const vox_item*)pb;
+    for (int k = 0; k < 3; ++k) {
+        if (a->c[k] < b->c[k]) return -1;
+        if (a->c[k] > b->c[k]) return 1;
+    }
+    return (a->idx < b->idx) ? -1 : (a->idx > b->idx);
+}
+
+typedef struct {
+    int64_t c[3];
+    int64_t n;
+    double mu[3];
+    double S[9]; /* mean of the points' covariances */
+} voxel;
+
+static int vcmp_key(const int64_t c[3], const voxel* v) {
+    for (int k = 0; k < 3; ++k) {
+        if (c[k] < v->c[k]) return -1;
+        if (c[k] > v->c[k]) return 1;
+    }
+    return 0;
+}
+
+/* voxel statistics of the target (R22): N, mu = sum x / N, Sigma = sum C_j / N */
+static voxel* build_voxels(const float* tgt, const float* tgt_cov, int64_t nt, float res, float o[3], float* inv,
+                           int64_t* nv) {
+    for (int a = 0; a < 3; ++a) {
+        o[a] = tgt[a];
+        for (int64_t j = 1; j < nt; ++j)
+            if (tgt[3 * j + a] < o[a]) o[a] = tgt[3 * j + a];
+    }
+    volatile float iv = 1.0f / res;
+    *inv = iv;
+    vox_item* it = (vox_item*)malloc(sizeof(vox_item) * nt);
+    voxel* vs = (voxel*)malloc(sizeof(voxel) * nt);
+    if (!it || !vs) {
+        free(it);
+        free(vs);
+        return NULL;
+    }
+    for (int64_t j = 0; j < nt; ++j) {
+        vox_coord(tgt + 3 * j, o, *inv, it[j].c);
+        it[j].idx = j;
+    }
+    qsort(it, nt, sizeof(vox_item), vox_cmp);
+    int64_t m = 0;
+    for (int64_t s = 0; s < nt;) {
+        int64_t e = s;
+        while (e < nt && it[e].c[0] == it[s].c[0] && it[e].c[1] == it[s].c[1] && it[e].c[2] == it[s].c[2]) ++e;
+        voxel* v = &vs[m++];
+        for (int a = 0; a < 3; ++a) v->c[a] = it[s].c[a];
+        v->n = e - s;
+        double mu[3] = {0, 0, 0}, S[9] = {0};
+        for (int64_t r = s; r < e; ++r) {
+            const int64_t j = it[r].idx;
+            double C[9];
+            cov6_to_full(tgt_cov + 6 * j, C);
+            for (int a = 0; a < 3; ++a) mu[a] += (double)tgt[3 * j + a];
+            for (int a = 0; a < 9; ++a) S[a] += C[a];
+        }
+        for (int a = 0; a < 3; ++a) v->mu[a] = mu[a] / (double)v->n;
+        for (int a = 0; a < 9; ++a) v->S[a] = S[a] / (double)v->n;
+        s = e;
+    }
+    free(it);
+    *nv = m;
+    return vs;
+}
+
+static const voxel* find_voxel(const voxel* vs, int64_t nv, const int64_t c[3]) {
+    int64_t lo = 0, hi = nv - 1;
+    while (lo <= hi) {
+        const int64_t mid = (lo + hi) / 2;
+        const int r = vcmp_key(c, &vs[mid]);
+        if (r == 0) return &vs[mid];
+        if (r < 0)
+            hi = mid - 1;
+        else
+            lo = mid + 1;
+    }
+    return NULL;
+}
+
+/* neighbour sets: own voxel, + 6 faces, + 12 edges + 8 corners (nearest-first) */
+static const int vg_off[27][3] = {{0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},
+                                  {0, 0, 1},   {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1},
+                                  {1, 0, -1},  {-1, 0, 1},  {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},
+                                  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1}, {-1, 1, -1}, {1, 1, -1}, {-1, -1, 1},
+                                  {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+
+/* O7: out29 = sum over (source i, voxel v in the neighbour set of fl32(T p_i)) of
+ * N_v * (J^T M J, J^T M d, d^T M d) with d = mu_v - T p_i, M = (Sigma_v + R C_i
+ * R^T)^-1, J about the pivot; out29[28] = number of pairs. Neumaier sums in
+ * (i, offset) order; absum29 = sum |term|. mode = 1, 7 or 27. */
+int oracle_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, const float* tgt,
+                           const float* tgt_cov, int64_t nt, float res, const double T[16], const double* pivot,
+                           int mode, double* out29, double* absum29) {
+    if (!src || !src_cov || !tgt || !tgt_cov || !T || !out29 || ns < 0 || nt <= 0 || !(res > 0.0f)) return ORACLE_EINVAL;
+    if (mode != 1 && mode != 7 && mode != 27) return ORACLE_EINVAL;
+    const double c0[3] = {pivot ? pivot[0] : 0.0, pivot ? pivot[1] : 0.0, pivot ? pivot[2] : 0.0};
+    float o[3], inv;
+    int64_t nv = 0;
+    voxel* vs = build_voxels(tgt, tgt_cov, nt, res, o, &inv, &nv);
+    if (!vs) return ORACLE_EINVAL;
+    const double R[9] = {T[0], T[1], T[2], T[4], T[5], T[6], T[8], T[9], T[10]};
+    const double t[3] = {T[3], T[7], T[11]};
+    neumaier acc[28];
+    double ab[28];
+    memset(acc, 0, sizeof(acc));
+    memset(ab, 0, sizeof(ab));
+    int64_t pairs = 0;
+    int bad = 0;
+    for (int64_t i = 0; i < ns; ++i) {
+        const double p[3] = {src[3 * i], src[3 * i + 1], src[3 * i + 2]};
+        double pp[3];
+        for (int a = 0; a < 3; ++a) pp[a] = fma(R[3 * a + 2], p[2], fma(R[3 * a + 1], p[1], fma(R[3 * a + 0], p[0], t[a])));
+        const float s[3] = {(float)pp[0], (float)pp[1], (float)pp[2]};
+        int64_t c[3];
+        vox_coord(s, o, inv, c);
+        double Cp[9], RC[9], RCR[9];
+        cov6_to_full(src_cov + 6 * i, Cp);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                double v = 0.0;
+                for (int k = 0; k < 3; ++k) v += R[3 * a + k] * Cp[3 * k + b];
+                RC[3 * a + b] = v;
+            }
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                double v = 0.0;
+                for (int k = 0; k < 3; ++k) v += RC[3 * a + k] * R[3 * b + k];
+                RCR[3 * a + b] = v;
+            }
+        for (int u = 0; u < mode; ++u) {
+            const int64_t cn[3] = {c[0] + vg_off[u][0], c[1] + vg_off[u][1], c[2] + vg_off[u][2]};
+            const voxel* v = find_voxel(vs, nv, cn);
+            if (!v) continue;
+            double A[9], M[9];
+            for (int a = 0; a < 9; ++a) A[a] = v->S[a] + RCR[a];
+            if (spd_inverse3(A, M) != 0) {
+                bad = 1;
+                continue;
+            }
+            const double d[3] = {v->mu[0] - pp[0], v->mu[1] - pp[1], v->mu[2] - pp[2]};
+            double term[28];
+            point_terms(pp, c0, d, M, term);
+            for (int k = 0; k < 28; ++k) {
+                const double w = (double)v->n * term[k];
+                nm_add(&acc[k], w);
+                ab[k] += fabs(w);
+            }
+            ++pairs;
+        }
+    }
+    for (int k = 0; k < 28; ++k) out29[k] = acc[k].s + acc[k].c;
+    out29[28] = (double)pairs;
+    if (absum29) {
+        for (int k = 0; k < 28; ++k) absum29[k] = ab[k];
+        absum29[28] = (double)pairs;
+    }
+    free(vs);
+    return bad ? ORACLE_EINVAL : ORACLE_OK;
+}
+
+/* O8: LM on O7 (R13's schedule; the trial cost e' is a full O7 evaluation at the
+ * trial pose -- voxel pairs follow the pose, R23). */
+int oracle_align_vgicp(const float* src, const float* src_cov, int64_t ns, const float* tgt, const float* tgt_cov,
+                       int64_t nt, float res, int mode, const double T0[16], const oracle_align_params* prm,
+                       oracle_align_result* out) {
+    if (!prm || !out || !T0) return ORACLE_EINVAL;
+    double T[16];
+    memcpy(T, T0, sizeof(T));
+    double lambda = -1.0, nu = 2.0, err = 0.0;
+    int converged = 0, it = 0, rc = ORACLE_OK;
+    int64_t inl = 0;
+    for (it = 1; it <= prm->max_iter; ++it) {
+        double o29[29];
+        const double piv[3] = {T[3], T[7], T[11]};
+        rc = oracle_linearize_vgicp(src, src_cov, ns, tgt, tgt_cov, nt, res, T, piv, mode, o29, NULL);
+        if (rc != ORACLE_OK) break;
+        inl = (int64_t)o29[28];
+        if (inl < 6) {
+            rc = ORACLE_EDEGENERATE;
+            break;
+        }
+        double H[36], b[6], delta[6] = {0};
+        unpack_H(o29, H, b);
+        const double e = o29[27];
+        err = e;
+        if (lambda < 0) {
+            double mx = 0;
+            for (int a = 0; a < 6; ++a)
+                if (H[7 * a] > mx) mx = H[7 * a];
+            lambda = 1e-9 * mx;
+        }
+        int accepted = 0;
+        for (int inner = 0; inner < 10; ++inner) {
+            double Hl[36], nb[6];
+            memcpy(Hl, H, sizeof(Hl));
+            for (int a = 0; a < 6; ++a) {
+                Hl[7 * a] += lambda;
+                nb[a] = -b[a];
+            }
+            if (oracle_ldlt_solve6(Hl, nb, delta) != 0) {
+                lambda *= nu;
+                nu *= 2.0;
+                continue;
+            }
+            double dT[16], Tn[16], o2[29];
+            oracle_pivoted_exp(delta, piv, dT);
+            mat4_mul(dT, T, Tn);
+            const double pn[3] = {Tn[3], Tn[7], Tn[11]};
+            rc = oracle_linearize_vgicp(src, src_cov, ns, tgt, tgt_cov, nt, res, Tn, pn, mode, o2, NULL);
+            if (rc != ORACLE_OK) break;
+            const double en = o2[27];
+            double den = 0.0;
+            for (int a = 0; a < 6; ++a) den += delta[a] * (lambda * delta[a] - b[a]);
+            const double rho = (e - en) / den;
+            if (rho > 0) {
+                memcpy(T, Tn, sizeof(T));
+                const double f = 1.0 - pow(2.0 * rho - 1.0, 3);
+                lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
+                nu = 2.0;
+                err = en;
+                accepted = 1;
+                break;
+            }
+            lambda *= nu;
+            nu *= 2.0;
+        }
+        if (rc != ORACLE_OK) break;
+        if (!accepted) {
+            converged = 1;
+            break;
+        }
+        const double mw = fmax(fabs(delta[0]), fmax(fabs(delta[1]), fabs(delta[2])));
+        const double mv = fmax(fabs(delta[3]), fmax(fabs(delta[4]), fabs(delta[5])));
+        if (mw < prm->rot_eps && mv < prm->trans_eps) {
+            converged = 1;
+            break;
+        }
+    }
+    memcpy(out->T, T, sizeof(T));
+    out->iterations = (it > prm->max_iter) ? prm->max_iter : it;
+    out->converged = converged;
+    out->error = err;
+    out->inliers = inl;
     return rc;
 }
