@@ -291,6 +291,36 @@ int gicp_align_batched_ex(const float* src, const float* src_cov, const int64_t*
                           const double* T0 /* host [B][16] */, const gicp_align_params* params /* host */,
                           gicp_align_result* result /* host [B] */, gicp_reduce_fn reduce, void* user, void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * Voxelized GICP ("extends and optimizes the Voxelized-GICP";
+ * SURVEY.md §8(f) #2; readings R22-R23). Build the target index with
+ * cell_size = the VGICP resolution, then attach the voxel Gaussians:
+ *
+ * gicp_index_attach_voxels -- per level-0 voxel v: N_v, mean mu_v (fp64 sums,
+ *   stored as an fp32 offset from the voxel's first point) and Sigma_v = the
+ *   mean of its points' covariances cov [n][6] (original order, device).
+ *   Asynchronous. Errors: EINVAL, ENOMEM.
+ * gicp_linearize_vgicp -- out29 = sum over pairs (source i, voxel v among the
+ *   voxel of fl32(T p_i) and its 6 faces (mode 7) / 26 neighbours (mode 27) / none
+ *   (mode 1)) of N_v (J^T M J, J^T M d, d^T M d), d = mu_v - T p_i (fp64),
+ *   M = (Sigma_v + R C_i R^T)^-1, J about the pivot (as gicp_linearize);
+ *   out29[28] = the number of pairs. base: each source point's base voxel
+ *   (cx, cy, cz), written unless GICP_LIN_REUSE_CORR, which reuses it (the pairs
+ *   of a previous linearisation); GICP_LIN_ERROR_ONLY as gicp_linearize. Async.
+ * gicp_align_vgicp -- gicp_align's LM on gicp_linearize_vgicp; the trial cost
+ *   keeps the pairs of the linearisation. Synchronous.
+ *   EDEGENERATE: < 6 pairs.
+ * ------------------------------------------------------------------------- */
+int gicp_index_attach_voxels(gicp_index idx, const float* cov, void* stream);
+int gicp_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, gicp_index tgt,
+                         const double T[16] /* host */, const double* pivot /* host [3] or NULL */, int mode,
+                         int flags, int32_t* base /* device [ns][3], nullable unless REUSE_CORR */,
+                         double* out29 /* device [29] */, void* stream);
+int gicp_align_vgicp(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, int mode,
+                     const double T0[16] /* host */, const gicp_align_params* params /* host */,
+                     gicp_align_result* result /* host */, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

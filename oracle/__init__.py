@@ -66,7 +66,7 @@ def lib():
         L.oracle_kernel_eval.argtypes = [i32, f64, f64, f64, i32, P, P]
         L.oracle_kernel_eval.restype = f64
         L.oracle_covariance_kd.argtypes = [P, i64, P, P, i64, i32, i32, f64, f64, f64, i32, P, i32, f64, P, P, i32]
-        L.oracle_linearize_vgicp.argtypes = [P, P, i64, P, P, i64, f32, P, P, i32, P, P]
+        L.oracle_linearize_vgicp.argtypes = [P, P, i64, P, P, i64, f32, P, P, i32, i32, P, P, P]
         L.oracle_align_vgicp.argtypes = [P, P, i64, P, P, i64, f32, i32, P, ctypes.POINTER(AlignParams),
                                          ctypes.POINTER(AlignResult)]
         L.oracle_align.argtypes = [P, P, i64, P, P, i64, P, ctypes.POINTER(AlignParams),
@@ -181,20 +181,28 @@ def covariance_kd(xyz, nbr, kind, q=None, sigma=1.0, alpha=1.0, c=0.0, d=2, orig
     return cov, gap
 
 
-def linearize_vgicp(src, src_cov, tgt, tgt_cov, T, res=1.0, mode=7, pivot=None):
-    """O7: voxelized GICP linearisation -> (out29, absum29)."""
+def linearize_vgicp(src, src_cov, tgt, tgt_cov, T, res=1.0, mode=7, pivot=None, base=None):
+    """O7: voxelized GICP linearisation -> (out29, absum29, base). With base given
+    (int32 [ns,3]) the pairs are those base voxels (REUSE); otherwise they are
+    computed at T and returned."""
     src, tgt = _f32(src), _f32(tgt)
     src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
     T = np.ascontiguousarray(T, dtype=np.float64)
     piv = None if pivot is None else np.ascontiguousarray(pivot, dtype=np.float64)
     out = np.empty(29)
     ab = np.empty(29)
+    flags = 0
+    if base is not None:
+        base = np.ascontiguousarray(base, dtype=np.int32).copy()
+        flags = LIN_REUSE_CORR
+    else:
+        base = np.empty((src.shape[0], 3), np.int32)
     rc = lib().oracle_linearize_vgicp(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
-                                      float(res), _ptr(T), None if piv is None else _ptr(piv), int(mode), _ptr(out),
-                                      _ptr(ab))
+                                      float(res), _ptr(T), None if piv is None else _ptr(piv), int(mode), flags,
+                                      _ptr(base), _ptr(out), _ptr(ab))
     if rc != OK:
         raise OracleError(rc, "oracle_linearize_vgicp")
-    return out, ab
+    return out, ab, base
 
 
 def align_vgicp(src, src_cov, tgt, tgt_cov, T0, res=1.0, mode=7, max_iter=64, rot_eps=1e-6, trans_eps=1e-5):

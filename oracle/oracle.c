@@ -983,13 +983,16 @@ static const int vg_off[27][3] = {{0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1,
                                   {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
 
 /* O7: out29 = sum over (source i, voxel v in the neighbour set of fl32(T p_i)) of
+ * (with LIN_REUSE_CORR the base voxel of each i is taken from base[3i..] -- the
+ * previous linearisation's -- instead of fl32(T p_i); otherwise it is written there) 
  * N_v * (J^T M J, J^T M d, d^T M d) with d = mu_v - T p_i, M = (Sigma_v + R C_i
  * R^T)^-1, J about the pivot; out29[28] = number of pairs. Neumaier sums in
  * (i, offset) order; absum29 = sum |term|. mode = 1, 7 or 27. */
 int oracle_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, const float* tgt,
                            const float* tgt_cov, int64_t nt, float res, const double T[16], const double* pivot,
-                           int mode, double* out29, double* absum29) {
+                           int mode, int flags, int32_t* base, double* out29, double* absum29) {
     if (!src || !src_cov || !tgt || !tgt_cov || !T || !out29 || ns < 0 || nt <= 0 || !(res > 0.0f)) return ORACLE_EINVAL;
+    if ((flags & LIN_REUSE_CORR) && !base) return ORACLE_EINVAL;
     if (mode != 1 && mode != 7 && mode != 27) return ORACLE_EINVAL;
     const double c0[3] = {pivot ? pivot[0] : 0.0, pivot ? pivot[1] : 0.0, pivot ? pivot[2] : 0.0};
     float o[3], inv;
@@ -1010,7 +1013,13 @@ int oracle_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, c
         for (int a = 0; a < 3; ++a) pp[a] = fma(R[3 * a + 2], p[2], fma(R[3 * a + 1], p[1], fma(R[3 * a + 0], p[0], t[a])));
         const float s[3] = {(float)pp[0], (float)pp[1], (float)pp[2]};
         int64_t c[3];
-        vox_coord(s, o, inv, c);
+        if (flags & LIN_REUSE_CORR) { /* the pairs of the previous linearisation (R23) */
+            for (int a = 0; a < 3; ++a) c[a] = base[3 * i + a];
+        } else {
+            vox_coord(s, o, inv, c);
+            if (base)
+                for (int a = 0; a < 3; ++a) base[3 * i + a] = (int32_t)c[a];
+        }
         double Cp[9], RC[9], RCR[9];
         cov6_to_full(src_cov + 6 * i, Cp);
         for (int a = 0; a < 3; ++a)
@@ -1056,8 +1065,8 @@ int oracle_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, c
     return bad ? ORACLE_EINVAL : ORACLE_OK;
 }
 
-/* O8: LM on O7 (R13's schedule; the trial cost e' is a full O7 evaluation at the
- * trial pose -- voxel pairs follow the pose, R23). */
+/* O8: LM on O7 with R13's schedule; the trial cost e' keeps the pairs of the
+ * linearisation (the base voxels, R23), as gicp_align keeps its correspondences. */
 int oracle_align_vgicp(const float* src, const float* src_cov, int64_t ns, const float* tgt, const float* tgt_cov,
                        int64_t nt, float res, int mode, const double T0[16], const oracle_align_params* prm,
                        oracle_align_result* out) {
@@ -1067,10 +1076,12 @@ int oracle_align_vgicp(const float* src, const float* src_cov, int64_t ns, const
     double lambda = -1.0, nu = 2.0, err = 0.0;
     int converged = 0, it = 0, rc = ORACLE_OK;
     int64_t inl = 0;
+    int32_t* base = (int32_t*)malloc(sizeof(int32_t) * 3 * (ns > 0 ? ns : 1));
+    if (!base) return ORACLE_EINVAL;
     for (it = 1; it <= prm->max_iter; ++it) {
         double o29[29];
         const double piv[3] = {T[3], T[7], T[11]};
-        rc = oracle_linearize_vgicp(src, src_cov, ns, tgt, tgt_cov, nt, res, T, piv, mode, o29, NULL);
+        rc = oracle_linearize_vgicp(src, src_cov, ns, tgt, tgt_cov, nt, res, T, piv, mode, 0, base, o29, NULL);
         if (rc != ORACLE_OK) break;
         inl = (int64_t)o29[28];
         if (inl < 6) {
@@ -1104,7 +1115,8 @@ int oracle_align_vgicp(const float* src, const float* src_cov, int64_t ns, const
             oracle_pivoted_exp(delta, piv, dT);
             mat4_mul(dT, T, Tn);
             const double pn[3] = {Tn[3], Tn[7], Tn[11]};
-            rc = oracle_linearize_vgicp(src, src_cov, ns, tgt, tgt_cov, nt, res, Tn, pn, mode, o2, NULL);
+            rc = oracle_linearize_vgicp(src, src_cov, ns, tgt, tgt_cov, nt, res, Tn, pn, mode, LIN_REUSE_CORR, base, o2,
+                                        NULL);
             if (rc != ORACLE_OK) break;
             const double en = o2[27];
             double den = 0.0;
@@ -1134,6 +1146,7 @@ int oracle_align_vgicp(const float* src, const float* src_cov, int64_t ns, const
             break;
         }
     }
+    free(base);
     memcpy(out->T, T, sizeof(T));
     out->iterations = (it > prm->max_iter) ? prm->max_iter : it;
     out->converged = converged;

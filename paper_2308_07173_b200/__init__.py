@@ -69,6 +69,10 @@ class CovParams(ctypes.Structure):
                 ("reg", ctypes.c_int), ("eps", ctypes.c_float)]
 
 
+_lib.gicp_index_attach_voxels.argtypes = [_P, _P, _P]
+_lib.gicp_linearize_vgicp.argtypes = [_P, _P, _i64, _P, _P, _P, _i32, _i32, _P, _P, _P]
+_lib.gicp_align_vgicp.argtypes = [_P, _P, _i64, _P, _i32, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
+                                  _P]
 _lib.gicp_covariances_kd.argtypes = [_P, _i64, _P, _P, _i64, _i32, ctypes.POINTER(CovParams), _P, _P]
 KERNELS = {"uniform": 0, "rbf": 1, "gaussian": 2, "polynomial": 3, "hi": 4, "laplacian": 5}
 REGS = {"plane": 0, "min_eig": 1, "normalized_min_eig": 2}
@@ -85,7 +89,8 @@ _lib.gicp_align_batched_ex.argtypes = [_P, _P, _P, _i32, _P, _i32, _P, _P, _P, c
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
-           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd"]
+           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd",
+           "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp"]
 
 
 class GicpError(RuntimeError):
@@ -359,6 +364,44 @@ def align_batched_ex(src: torch.Tensor, src_cov: torch.Tensor, offsets, entry_re
         _check(rc)
     Ts = np.array([np.array(r.T[:], dtype=np.float64).reshape(4, 4) for r in res])
     return Ts, [AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers)) for r in res]
+
+
+def attach_voxels(index: Index, cov: torch.Tensor):
+    """VGICP voxel Gaussians (N, mean, mean covariance) of the index's level-0 voxels;
+    the index must be built with cell_size = the VGICP resolution."""
+    index._voxcov = cov.contiguous()
+    _check(_lib.gicp_index_attach_voxels(index.handle, _dptr(index._voxcov), _stream()))
+
+
+def linearize_vgicp(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, T, mode: int = 7, pivot=None,
+                    error_only: bool = False, base: torch.Tensor | None = None, reuse: bool = False, out=None):
+    """Voxelized GICP linearisation -> (out29 float64 device [29] (28 = number of
+    pairs), base int32 device [ns, 3] (each point's base voxel; reused when reuse))."""
+    src = _pts(src, "src")
+    Th = _T(T)
+    out29 = out if out is not None else torch.empty(29, dtype=torch.float64, device=src.device)
+    if base is None:
+        if reuse:
+            raise ValueError("reuse needs base")
+        base = torch.empty((src.shape[0], 3), dtype=torch.int32, device=src.device)
+    piv = None if pivot is None else np.ascontiguousarray(np.asarray(pivot, dtype=np.float64).reshape(3))
+    flags = (LIN_ERROR_ONLY if error_only else 0) | (LIN_REUSE_CORR if reuse else 0)
+    _check(_lib.gicp_linearize_vgicp(_dptr(src), _dptr(src_cov.contiguous()), src.shape[0], tgt.handle,
+                                     Th.ctypes.data_as(_P), None if piv is None else piv.ctypes.data_as(_P), int(mode),
+                                     flags, _dptr(base), _dptr(out29), _stream()))
+    return out29, base
+
+
+def align_vgicp(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, T0, mode: int = 7, max_iter=64,
+                rot_eps=1e-6, trans_eps=1e-5):
+    src = _pts(src, "src")
+    T0h = _T(T0)
+    p = AlignParams(int(max_iter), 1, float(rot_eps), float(trans_eps), 1.0)
+    r = AlignResult()
+    _check(_lib.gicp_align_vgicp(_dptr(src), _dptr(src_cov.contiguous()), src.shape[0], tgt.handle, int(mode),
+                                 T0h.ctypes.data_as(_P), ctypes.byref(p), ctypes.byref(r), _stream()))
+    T = np.array(r.T[:], dtype=np.float64).reshape(4, 4)
+    return T, AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers))
 
 
 def version() -> int:

@@ -221,6 +221,8 @@ GICP_API void gicp_index_free(gicp_index idx) {
     if (idx->adj_oc) cudaFreeAsync(idx->adj_oc, s);
     if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
     if (idx->adj_oc1) cudaFreeAsync(idx->adj_oc1, s);
+    if (idx->vox_mu) cudaFreeAsync(idx->vox_mu, s);
+    if (idx->vox_cov) cudaFreeAsync(idx->vox_cov, s);
     if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
     cudaGetLastError();
     delete idx;
@@ -960,4 +962,142 @@ GICP_API int gicp_align_batched_ex(const float* src, const float* src_cov, const
                                    gicp_reduce_fn reduce, void* user, void* stream) {
     return align_batched_impl(src, src_cov, offsets, E, entry_reg, B, tgt, tgt_cov, T0, prm, res, reduce, user,
                               stream);
+}
+
+// ---- voxelized GICP ---------------------------------------
+
+GICP_API int gicp_index_attach_voxels(gicp_index idx, const float* cov, void* stream) {
+    if (!idx || !cov) return set_error(GICP_EINVAL, "gicp_index_attach_voxels: null pointer");
+    init_pool_once();
+    return attach_voxels(idx, cov, (cudaStream_t)stream);
+}
+
+GICP_API int gicp_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, gicp_index tgt,
+                                  const double T[16], const double* pivot, int mode, int flags, int32_t* base,
+                                  double* out29, void* stream) {
+    if (!tgt || !T || !out29) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: null pointer");
+    if (!tgt->vox_mu) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: call gicp_index_attach_voxels first");
+    if (ns < 0 || ns >= (1ll << 31) - 1) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: ns out of range");
+    if (ns > 0 && (!src || !src_cov)) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: null source");
+    if (mode != 1 && mode != 7 && mode != 27) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: mode 1, 7 or 27");
+    if (flags & ~(GICP_LIN_ERROR_ONLY | GICP_LIN_REUSE_CORR)) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: flags");
+    if ((flags & GICP_LIN_REUSE_CORR) && !base && ns > 0)
+        return set_error(GICP_EINVAL, "gicp_linearize_vgicp: REUSE_CORR needs base");
+    if (!finite_T(T)) return set_error(GICP_EINVAL, "gicp_linearize_vgicp: non-finite T");
+    init_pool_once();
+    return launch_linearize_vgicp(src, src_cov, ns, tgt, T, pivot, mode, flags, base, out29, (cudaStream_t)stream);
+}
+
+// LM on the voxelized linearisation with gicp_align's schedule (R13); the trial
+// cost keeps the pairs (base voxels) of the linearisation (reading R23).
+GICP_API int gicp_align_vgicp(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, int mode,
+                              const double T0[16], const gicp_align_params* prm, gicp_align_result* res,
+                              void* stream) {
+    if (!tgt || !T0 || !prm || !res || (ns > 0 && (!src || !src_cov)))
+        return set_error(GICP_EINVAL, "gicp_align_vgicp: null pointer");
+    if (!tgt->vox_mu) return set_error(GICP_EINVAL, "gicp_align_vgicp: call gicp_index_attach_voxels first");
+    if (mode != 1 && mode != 7 && mode != 27) return set_error(GICP_EINVAL, "gicp_align_vgicp: mode 1, 7 or 27");
+    if (prm->max_iter < 1) return set_error(GICP_EINVAL, "gicp_align_vgicp: max_iter < 1");
+    if (!finite_T(T0)) return set_error(GICP_EINVAL, "gicp_align_vgicp: non-finite T0");
+    init_pool_once();
+    cudaStream_t s = (cudaStream_t)stream;
+    MappedOut* mo = mapped_out();
+    if (!mo) return set_error(GICP_ENOMEM, "gicp_align_vgicp: host-mapped buffer");
+    const size_t bytes = 512 + vgicp_scratch_bytes(ns > 0 ? ns : 1) + 3 * sizeof(int) * (ns > 0 ? ns : 1) + 16;
+    char* scratch = nullptr;
+    if (cudaMallocAsync((void**)&scratch, bytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(GICP_ENOMEM, "gicp_align_vgicp: scratch allocation failed");
+    }
+    LinScratch ls;
+    ls.done = (unsigned*)(scratch + 256);
+    ls.partials = (double*)(scratch + 512);
+    double* d_out = (double*)scratch;
+    int* base = (int*)(((uintptr_t)(scratch + 512 + vgicp_scratch_bytes(ns > 0 ? ns : 1)) + 15) & ~(uintptr_t)15);
+    int rc = check_cuda(cudaMemsetAsync(ls.done, 0, sizeof(unsigned), s), "memset");
+    double h[29];
+    auto lin = [&](const double* T, const double* piv, int flags) -> int {
+        int r = launch_linearize_vgicp(src, src_cov, ns, tgt, T, piv, mode, flags, base, d_out, s, &ls);
+        if (!r) r = check_cuda(cudaMemcpyAsync(mo->h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+        if (!r) r = check_cuda(cudaStreamSynchronize(s), "vgicp sync");
+        if (!r) std::memcpy(h, mo->h, sizeof(h));
+        return r;
+    };
+    double T[16];
+    std::memcpy(T, T0, sizeof(T));
+    double lambda = -1.0, nu = 2.0, err = 0.0;
+    int converged = 0, it = 0;
+    int64_t inl = 0;
+    for (it = 1; !rc && it <= prm->max_iter; ++it) {
+        const double piv[3] = {T[3], T[7], T[11]};
+        if ((rc = lin(T, piv, 0))) break;
+        inl = (int64_t)h[28];
+        if (inl < 6) {
+            rc = set_error(GICP_EDEGENERATE, "gicp_align_vgicp: fewer than 6 voxel pairs");
+            break;
+        }
+        double Hm[36], b[6], delta[6] = {0, 0, 0, 0, 0, 0};
+        for (int a = 0, o = 0; a < 6; ++a)
+            for (int c = a; c < 6; ++c, ++o) Hm[6 * a + c] = Hm[6 * c + a] = h[o];
+        for (int a = 0; a < 6; ++a) b[a] = h[21 + a];
+        const double e = h[27];
+        err = e;
+        if (lambda < 0) {
+            double mx = 0.0;
+            for (int a = 0; a < 6; ++a) mx = std::fmax(mx, Hm[7 * a]);
+            lambda = 1e-9 * mx;
+        }
+        bool accepted = false;
+        for (int inner = 0; inner < 10; ++inner) {
+            double Hl[36], nb[6];
+            std::memcpy(Hl, Hm, sizeof(Hl));
+            for (int a = 0; a < 6; ++a) {
+                Hl[7 * a] += lambda;
+                nb[a] = -b[a];
+            }
+            if (!ldlt6(Hl, nb, delta)) {
+                lambda *= nu;
+                nu *= 2.0;
+                continue;
+            }
+            double E[16], Tn[16];
+            pivoted_exp(delta, piv, E);
+            mul44(E, T, Tn);
+            const double pn[3] = {Tn[3], Tn[7], Tn[11]};
+            if ((rc = lin(Tn, pn, GICP_LIN_ERROR_ONLY | GICP_LIN_REUSE_CORR))) break;
+            const double en = h[27];
+            double den = 0.0;
+            for (int a = 0; a < 6; ++a) den += delta[a] * (lambda * delta[a] - b[a]);
+            const double rho = (e - en) / den;
+            if (rho > 0) {
+                std::memcpy(T, Tn, sizeof(T));
+                const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);
+                lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
+                nu = 2.0;
+                err = en;
+                accepted = true;
+                break;
+            }
+            lambda *= nu;
+            nu *= 2.0;
+        }
+        if (rc) break;
+        if (!accepted) {
+            converged = 1;
+            break;
+        }
+        const double mw = std::fmax(std::fabs(delta[0]), std::fmax(std::fabs(delta[1]), std::fabs(delta[2])));
+        const double mv = std::fmax(std::fabs(delta[3]), std::fmax(std::fabs(delta[4]), std::fabs(delta[5])));
+        if (mw < prm->rot_eps && mv < prm->trans_eps) {
+            converged = 1;
+            break;
+        }
+    }
+    cudaFreeAsync(scratch, s);
+    std::memcpy(res->T, T, sizeof(T));
+    res->iterations = it > prm->max_iter ? prm->max_iter : it;
+    res->converged = converged;
+    res->error = err;
+    res->inliers = inl;
+    return rc;
 }

@@ -164,6 +164,9 @@ struct gicp_index_s {
     int2* adj_oc1 = nullptr;              // the same lists for level 1 (escalated queries)
     int2* adj_rng1 = nullptr;
     float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
+    float4* vox_mu = nullptr;             // VGICP: per level-0 voxel, at its head: mean - first point (xyz), N (w)
+    float4* vox_cov = nullptr;            // VGICP: mean covariance of the voxel's points (2 x float4 at the head)
+    const float* vox_attached = nullptr;  // the covariance array the voxel statistics came from
     const float* cov_attached = nullptr;  // the caller's original-order array they were copied from
     int device = 0;
     cudaStream_t stream = nullptr;  // build stream: device memory is pool-allocated on it
@@ -261,6 +264,11 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
                           int32_t* corr, cudaStream_t s, const LinScratch& scr, const int32_t* corr_old,
                           const BatchView& bv, int64_t nb);
 int attach_covariances(gicp_index_s* idx, const float* cov, cudaStream_t s);
+int attach_voxels(gicp_index_s* idx, const float* cov, cudaStream_t s);
+size_t vgicp_scratch_bytes(int64_t ns);
+int launch_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
+                           const double T[16], const double* pivot, int mode, int flags, int* base, double* out29,
+                           cudaStream_t s, const LinScratch* pre = nullptr);
 int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
                 cudaStream_t s, const int64_t* offs = nullptr, int nseg = 1);
 

@@ -18,7 +18,7 @@ def test_single_voxel_closed_form():
     src = np.array([[2.6, 3.5, 4.3]], np.float32)
     cs = gen.random_covariances(1, 6)
     T = np.eye(4)
-    out, _ = orc.linearize_vgicp(src, cs, tgt, ct, T, res=1.0, mode=1)
+    out, _, _ = orc.linearize_vgicp(src, cs, tgt, ct, T, res=1.0, mode=1)
     full = lambda c: np.array([[c[0], c[1], c[2]], [c[1], c[3], c[4]], [c[2], c[4], c[5]]], np.float64)  # noqa: E731
     mu = tgt.astype(np.float64).mean(axis=0)
     S = np.mean([full(c.astype(np.float64)) for c in ct.astype(np.float32)], axis=0)
@@ -42,7 +42,7 @@ def test_one_point_per_voxel_reduces_to_gicp():
     src = (tgt[rng.choice(len(tgt), 150, replace=False)] + rng.uniform(0.15, 0.6, (150, 3))).astype(np.float32)
     cs = gen.random_covariances(150, 9)
     T = gen.make_T(gen.euler_to_R(0.001, -0.002, 0.002), [0.05, -0.04, 0.02])
-    out, _ = orc.linearize_vgicp(src, cs, tgt, ct, T, res=1.0, mode=1, pivot=[1.0, 2.0, 3.0])
+    out, _, _ = orc.linearize_vgicp(src, cs, tgt, ct, T, res=1.0, mode=1, pivot=[1.0, 2.0, 3.0])
     # the correspondence: the lattice point whose voxel holds fl32(T p)
     o = tgt.min(axis=0)
     pp = src.astype(np.float64) @ T[:3, :3].T + T[:3, 3]
@@ -61,6 +61,10 @@ def test_pair_counts_by_mode():
     ct = gen.random_covariances(len(tgt), 2)
     n = [orc.linearize_vgicp(src, cs, tgt, ct, T_true, res=1.0, mode=m)[0][28] for m in (1, 7, 27)]
     assert 0 < n[0] <= len(src) and n[0] < n[1] < n[2] <= 27 * len(src)
+    # REUSE with the returned base voxels reproduces the evaluation exactly
+    o1, _, base = orc.linearize_vgicp(src, cs, tgt, ct, T0, res=1.0, mode=7)
+    o2, _, _ = orc.linearize_vgicp(src, cs, tgt, ct, T0, res=1.0, mode=7, base=base)
+    assert np.array_equal(o1, o2)
 
 
 def test_align_vgicp_recovers_the_corner():
@@ -69,6 +73,6 @@ def test_align_vgicp_recovers_the_corner():
     nt, _ = orc.knn(tgt, tgt, 10)
     cs = orc.covariance(src, ns)[0]
     ct = orc.covariance(tgt, nt)[0]
-    r = orc.align_vgicp(src, cs, tgt, ct, T0, res=0.5, mode=7)
+    r = orc.align_vgicp(src, cs, tgt, ct, T0, res=0.5, mode=27)
     assert r["converged"]
     assert np.linalg.norm(r["T"][:3, 3] - T_true[:3, 3]) < 0.02
