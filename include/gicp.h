@@ -321,6 +321,22 @@ int gicp_align_vgicp(const float* src, const float* src_cov, int64_t ns, gicp_in
                      const double T0[16] /* host */, const gicp_align_params* params /* host */,
                      gicp_align_result* result /* host */, void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * gicp_ground_filter -- the z-vote vertical-feature extractor (PAPER.md l.500-520,
+ * "vote the points corresponding to the grid-cell ... hashing ... filter out
+ * ground points without matrix computation"; R24):
+ *   cell (u, v) = (floor(fl32(x * fl32(1/cell))), floor(fl32(y * fl32(1/cell))))
+ *   in the points' (vehicle body) frame, |u|, |v| clamped below 2^31 - 1;
+ *   keep[i] = 1 iff i's cell holds >= min_count points (a vertical feature:
+ *   walls, posts), 0 for ground; count[i] (nullable) = that number.
+ *   The input is expected voxel-filtered (leaf <= cell, SPEC pre).
+ *   xyz [n][3] fp32, keep [n] uint8, count [n] int32 (device). Asynchronous.
+ * Errors: EINVAL (n < 0, cell <= 0, null), ENOMEM.
+ * ------------------------------------------------------------------------- */
+int gicp_ground_filter(const float* xyz, int64_t n, float cell, int min_count, uint8_t* keep, int32_t* count,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,7 @@ def lib():
         L.oracle_kernel_eval.argtypes = [i32, f64, f64, f64, i32, P, P]
         L.oracle_kernel_eval.restype = f64
         L.oracle_covariance_kd.argtypes = [P, i64, P, P, i64, i32, i32, f64, f64, f64, i32, P, i32, f64, P, P, i32]
+        L.oracle_ground_filter.argtypes = [P, i64, f32, i32, P, P]
         L.oracle_linearize_vgicp.argtypes = [P, P, i64, P, P, i64, f32, P, P, i32, i32, P, P, P]
         L.oracle_align_vgicp.argtypes = [P, P, i64, P, P, i64, f32, i32, P, ctypes.POINTER(AlignParams),
                                          ctypes.POINTER(AlignResult)]
@@ -218,6 +219,18 @@ def align_vgicp(src, src_cov, tgt, tgt_cov, T0, res=1.0, mode=7, max_iter=64, ro
         raise OracleError(rc, "oracle_align_vgicp")
     return dict(T=np.array(r.T[:]).reshape(4, 4), iterations=r.iterations, converged=bool(r.converged),
                 error=r.error, inliers=r.inliers)
+
+
+def ground_filter(xyz, cell, min_count):
+    """O9: (keep bool [n], count int32 [n]) of the z-vote filter."""
+    xyz = _f32(xyz).reshape(-1, 3)
+    n = xyz.shape[0]
+    keep = np.zeros(n, np.uint8)
+    count = np.zeros(n, np.int32)
+    rc = lib().oracle_ground_filter(_ptr(xyz), n, float(cell), int(min_count), _ptr(count), _ptr(keep))
+    if rc != OK:
+        raise OracleError(rc, "oracle_ground_filter")
+    return keep.astype(bool), count
 
 
 def se3_exp(delta):

@@ -25,6 +25,8 @@
  *   O7 oracle_linearize_vgicp / O8 oracle_align_vgicp  voxelized GICP (l.419):
  *                          voxel N, mean, mean covariance; pairs with the voxels
  *                          around fl32(T p); N-weighted Mahalanobis terms.
+ *   O9 oracle_ground_filter  z-vote ground filter: 2-D cell counts, keep cells
+ *                          with >= min_count points (l.500-520).
  *   O6 oracle_covariance_kd  kernel-weighted mean / scatter + PLANE / MIN_EIG /
  *                          NORMALIZED_MIN_EIG regularisation (SURVEY §8(f) #1,
  *                          "covariance computation using the kernel descriptors" l.413).
@@ -1153,4 +1155,52 @@ int oracle_align_vgicp(const float* src, const float* src_cov, int64_t ns, const
     out->error = err;
     out->inliers = inl;
     return rc;
+}
+
+/* -------------------------------------------------------------------------- */
+/* O9: z-vote ground filter ("vote the points corresponding  */
+/* to the grid-cell ... filter out ground points ... without matrix computation"; */
+/* SURVEY.md §8(f) #4; reading R24)                   */
+/* -------------------------------------------------------------------------- */
+
+/* cell (u, v) = (floor(fl32(x * fl32(1/cell))), floor(fl32(y * fl32(1/cell)))) in
+ * the points' (vehicle body) frame; count[i] = the number of points in i's cell;
+ * keep[i] = count[i] >= min_count (a vertical feature). */
+typedef struct {
+    int64_t u, v, i;
+} uv_item;
+
+static int uv_cmp(const void* pa, const void* pb) {
+    const uv_item* a = (const uv_item*)pa;
+    const uv_item* b = (const uv_item*)pb;
+    if (a->u != b->u) return a->u < b->u ? -1 : 1;
+    if (a->v != b->v) return a->v < b->v ? -1 : 1;
+    return (a->i < b->i) ? -1 : (a->i > b->i);
+}
+
+int oracle_ground_filter(const float* xyz, int64_t n, float cell, int min_count, int32_t* count, uint8_t* keep) {
+    if (!xyz || n < 0 || !(cell > 0.0f) || !keep) return ORACLE_EINVAL;
+    if (n == 0) return ORACLE_OK;
+    volatile float iv = 1.0f / cell;
+    const float inv = iv;
+    uv_item* it = (uv_item*)malloc(sizeof(uv_item) * n);
+    if (!it) return ORACLE_EINVAL;
+    for (int64_t i = 0; i < n; ++i) {
+        volatile float tu = xyz[3 * i] * inv, tv = xyz[3 * i + 1] * inv;
+        it[i].u = (int64_t)floor((double)tu);
+        it[i].v = (int64_t)floor((double)tv);
+        it[i].i = i;
+    }
+    qsort(it, n, sizeof(uv_item), uv_cmp);
+    for (int64_t s = 0; s < n;) {
+        int64_t e = s;
+        while (e < n && it[e].u == it[s].u && it[e].v == it[s].v) ++e;
+        for (int64_t r = s; r < e; ++r) {
+            if (count) count[it[r].i] = (int32_t)(e - s);
+            keep[it[r].i] = (e - s) >= min_count;
+        }
+        s = e;
+    }
+    free(it);
+    return ORACLE_OK;
 }

@@ -73,6 +73,7 @@ _lib.gicp_index_attach_voxels.argtypes = [_P, _P, _P]
 _lib.gicp_linearize_vgicp.argtypes = [_P, _P, _i64, _P, _P, _P, _i32, _i32, _P, _P, _P]
 _lib.gicp_align_vgicp.argtypes = [_P, _P, _i64, _P, _i32, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
                                   _P]
+_lib.gicp_ground_filter.argtypes = [_P, _i64, _f32, _i32, _P, _P, _P]
 _lib.gicp_covariances_kd.argtypes = [_P, _i64, _P, _P, _i64, _i32, ctypes.POINTER(CovParams), _P, _P]
 KERNELS = {"uniform": 0, "rbf": 1, "gaussian": 2, "polynomial": 3, "hi": 4, "laplacian": 5}
 REGS = {"plane": 0, "min_eig": 1, "normalized_min_eig": 2}
@@ -90,7 +91,7 @@ EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_fr
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
            "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd",
-           "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp"]
+           "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter"]
 
 
 class GicpError(RuntimeError):
@@ -402,6 +403,19 @@ def align_vgicp(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, T0, mode: 
                                  T0h.ctypes.data_as(_P), ctypes.byref(p), ctypes.byref(r), _stream()))
     T = np.array(r.T[:], dtype=np.float64).reshape(4, 4)
     return T, AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers))
+
+
+def ground_filter(xyz: torch.Tensor, cell: float, min_count: int, with_count: bool = False):
+    """z-vote ground filter: keep (bool device [n]) = the point's 2-D cell holds
+    >= min_count points (vertical features); optionally the counts (int32 [n])."""
+    xyz = _pts(xyz, "xyz")
+    n = xyz.shape[0]
+    keep = torch.empty(n, dtype=torch.uint8, device=xyz.device)
+    count = torch.empty(n, dtype=torch.int32, device=xyz.device) if with_count else None
+    _check(_lib.gicp_ground_filter(_dptr(xyz) if n else None, n, float(cell), int(min_count),
+                                   _dptr(keep) if n else None, None if count is None or not n else _dptr(count),
+                                   _stream()))
+    return (keep.bool(), count) if with_count else keep.bool()
 
 
 def version() -> int:

@@ -1101,3 +1101,13 @@ GICP_API int gicp_align_vgicp(const float* src, const float* src_cov, int64_t ns
     res->inliers = inl;
     return rc;
 }
+
+// ---- z-vote ground filter -----------------------------------
+GICP_API int gicp_ground_filter(const float* xyz, int64_t n, float cell, int min_count, uint8_t* keep, int32_t* count,
+                                void* stream) {
+    if (n < 0) return set_error(GICP_EINVAL, "gicp_ground_filter: n < 0");
+    if (!(cell > 0.0f) || !std::isfinite(cell)) return set_error(GICP_EINVAL, "gicp_ground_filter: cell must be > 0");
+    if (n > 0 && (!xyz || !keep)) return set_error(GICP_EINVAL, "gicp_ground_filter: null pointer");
+    init_pool_once();
+    return launch_ground_filter(xyz, n, cell, min_count, keep, count, (cudaStream_t)stream);
+}
