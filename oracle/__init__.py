@@ -67,6 +67,8 @@ def lib():
         L.oracle_kernel_eval.restype = f64
         L.oracle_covariance_kd.argtypes = [P, i64, P, P, i64, i32, i32, f64, f64, f64, i32, P, i32, f64, P, P, i32]
         L.oracle_ground_filter.argtypes = [P, i64, f32, i32, P, P]
+        L.oracle_cluster.argtypes = [P, i64, f32, i32, P]
+        L.oracle_cluster.restype = i64
         L.oracle_linearize_vgicp.argtypes = [P, P, i64, P, P, i64, f32, P, P, i32, i32, P, P, P]
         L.oracle_align_vgicp.argtypes = [P, P, i64, P, P, i64, f32, i32, P, ctypes.POINTER(AlignParams),
                                          ctypes.POINTER(AlignResult)]
@@ -231,6 +233,16 @@ def ground_filter(xyz, cell, min_count):
     if rc != OK:
         raise OracleError(rc, "oracle_ground_filter")
     return keep.astype(bool), count
+
+
+def cluster(xyz, tol, min_size=1):
+    """O10: (labels int32 [n] -- rank by descending size, -1 if dropped --, count)."""
+    xyz = _f32(xyz).reshape(-1, 3)
+    lab = np.empty(xyz.shape[0], np.int32)
+    nc = lib().oracle_cluster(_ptr(xyz), xyz.shape[0], float(tol), int(min_size), _ptr(lab))
+    if nc < 0:
+        raise OracleError(int(nc), "oracle_cluster")
+    return lab, int(nc)
 
 
 def se3_exp(delta):

@@ -25,6 +25,8 @@
  *   O7 oracle_linearize_vgicp / O8 oracle_align_vgicp  voxelized GICP (l.419):
  *                          voxel N, mean, mean covariance; pairs with the voxels
  *                          around fl32(T p); N-weighted Mahalanobis terms.
+ *   O10 oracle_cluster     Euclidean cluster extraction (l.549-559): connected
+ *                          components under d2 <= tol^2, brute-force union-find.
  *   O9 oracle_ground_filter  z-vote ground filter: 2-D cell counts, keep cells
  *                          with >= min_count points (l.500-520).
  *   O6 oracle_covariance_kd  kernel-weighted mean / scatter + PLANE / MIN_EIG /
@@ -1203,4 +1205,74 @@ int oracle_ground_filter(const float* xyz, int64_t n, float cell, int min_count,
     }
     free(it);
     return ORACLE_OK;
+}
+
+/* -------------------------------------------------------------------------- */
+/* O10: Euclidean cluster extraction ("CUDA-based Euclidean   */
+/* distance clustering ... to find cluster C_j" citing Rusu 2010       */
+/* §8(f) #4; reading R25)                              */
+/* -------------------------------------------------------------------------- */
+
+static int64_t uf_find(int64_t* p, int64_t x) {
+    while (p[x] != x) {
+        p[x] = p[p[x]];
+        x = p[x];
+    }
+    return x;
+}
+
+/* i ~ j iff d2(p_i, p_j) <= fl32(tol * tol) with the R9 fp32 d2; clusters = the
+ * connected components; those with fewer than min_size points get label -1;
+ * the rest are numbered 0, 1, ... by descending size, ties by the smallest
+ * member index. O(n^2) pairs (brute force). Returns the number of clusters. */
+int64_t oracle_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t* label) {
+    if (!xyz || n < 0 || !(tol > 0.0f) || !label) return -1;
+    if (n == 0) return 0;
+    const int hw = have_fma();
+    const float t2 = tol * tol;
+    int64_t* par = (int64_t*)malloc(sizeof(int64_t) * n);
+    if (!par) return -1;
+    for (int64_t i = 0; i < n; ++i) par[i] = i;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = i + 1; j < n; ++j) {
+            const float d2 = hw ? d2_fma_hw(xyz + 3 * i, xyz + 3 * j) : d2_fma_sw(xyz + 3 * i, xyz + 3 * j);
+            if (d2 <= t2) {
+                const int64_t a = uf_find(par, i), b = uf_find(par, j);
+                if (a != b) par[a > b ? a : b] = a < b ? a : b;
+            }
+        }
+    /* component of each point = its root (the smallest member index) */
+    int64_t* size = (int64_t*)calloc(n, sizeof(int64_t));
+    if (!size) {
+        free(par);
+        return -1;
+    }
+    for (int64_t i = 0; i < n; ++i) size[uf_find(par, i)]++;
+    int64_t nc = 0;
+    for (int64_t r = 0; r < n; ++r)
+        if (size[r] >= min_size && size[r] > 0) ++nc;
+    int64_t* roots = (int64_t*)malloc(sizeof(int64_t) * (nc > 0 ? nc : 1));
+    int64_t* rank = (int64_t*)malloc(sizeof(int64_t) * n);
+    if (!roots || !rank) {
+        free(par); free(size); free(roots); free(rank);
+        return -1;
+    }
+    int64_t k = 0;
+    for (int64_t r = 0; r < n; ++r)
+        if (size[r] >= min_size && size[r] > 0) roots[k++] = r;
+    /* insertion sort by (size desc, root asc) -- roots ascending already */
+    for (int64_t a = 1; a < nc; ++a) {
+        const int64_t x = roots[a];
+        int64_t b = a - 1;
+        while (b >= 0 && size[roots[b]] < size[x]) {
+            roots[b + 1] = roots[b];
+            --b;
+        }
+        roots[b + 1] = x;
+    }
+    for (int64_t r = 0; r < n; ++r) rank[r] = -1;
+    for (int64_t a = 0; a < nc; ++a) rank[roots[a]] = a;
+    for (int64_t i = 0; i < n; ++i) label[i] = (int32_t)rank[uf_find(par, i)];
+    free(par); free(size); free(roots); free(rank);
+    return nc;
 }
