@@ -337,6 +337,19 @@ int gicp_align_vgicp(const float* src, const float* src_cov, int64_t ns, gicp_in
 int gicp_ground_filter(const float* xyz, int64_t n, float cell, int min_count, uint8_t* keep, int32_t* count,
                        void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * gicp_cluster -- Euclidean cluster extraction (the
+ * "CUDA-based Euclidean distance clustering" of Rusu 2010; SPEC S:549-556;
+ * DESIGN.md R25): i ~ j iff d2(p_i, p_j) <= fl32(tol*tol) (fp32 d2 as gicp_knn);
+ * clusters = connected components, numbered 0, 1, ... by descending size, ties
+ * by the smallest member index; components with fewer than min_size points get
+ * label -1. xyz [n][3], label [n] int32 (device); *n_clusters (host) = the
+ * number of numbered clusters. Synchronous. Errors: EINVAL, ENOMEM, ERANGE.
+ * ------------------------------------------------------------------------- */
+int gicp_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t* label, int64_t* n_clusters,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

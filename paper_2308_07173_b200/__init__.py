@@ -74,6 +74,7 @@ _lib.gicp_linearize_vgicp.argtypes = [_P, _P, _i64, _P, _P, _P, _i32, _i32, _P, 
 _lib.gicp_align_vgicp.argtypes = [_P, _P, _i64, _P, _i32, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
                                   _P]
 _lib.gicp_ground_filter.argtypes = [_P, _i64, _f32, _i32, _P, _P, _P]
+_lib.gicp_cluster.argtypes = [_P, _i64, _f32, _i32, _P, ctypes.POINTER(ctypes.c_int64), _P]
 _lib.gicp_covariances_kd.argtypes = [_P, _i64, _P, _P, _i64, _i32, ctypes.POINTER(CovParams), _P, _P]
 KERNELS = {"uniform": 0, "rbf": 1, "gaussian": 2, "polynomial": 3, "hi": 4, "laplacian": 5}
 REGS = {"plane": 0, "min_eig": 1, "normalized_min_eig": 2}
@@ -91,7 +92,8 @@ EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_fr
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
            "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd",
-           "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter"]
+           "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter",
+           "gicp_cluster"]
 
 
 class GicpError(RuntimeError):
@@ -416,6 +418,18 @@ def ground_filter(xyz: torch.Tensor, cell: float, min_count: int, with_count: bo
                                    _dptr(keep) if n else None, None if count is None or not n else _dptr(count),
                                    _stream()))
     return (keep.bool(), count) if with_count else keep.bool()
+
+
+def cluster(xyz: torch.Tensor, tol: float, min_size: int = 1):
+    """Euclidean clusters: (labels int32 device [n] -- 0.. by descending size, -1
+    below min_size --, number of clusters)."""
+    xyz = _pts(xyz, "xyz")
+    n = xyz.shape[0]
+    lab = torch.empty(n, dtype=torch.int32, device=xyz.device)
+    nc = ctypes.c_int64(0)
+    _check(_lib.gicp_cluster(_dptr(xyz) if n else None, n, float(tol), int(min_size), _dptr(lab) if n else None,
+                             ctypes.byref(nc), _stream()))
+    return lab, int(nc.value)
 
 
 def version() -> int:

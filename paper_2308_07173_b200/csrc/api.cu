@@ -1111,3 +1111,13 @@ GICP_API int gicp_ground_filter(const float* xyz, int64_t n, float cell, int min
     init_pool_once();
     return launch_ground_filter(xyz, n, cell, min_count, keep, count, (cudaStream_t)stream);
 }
+
+// ---- Euclidean cluster extraction ----------------------------
+GICP_API int gicp_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t* label, int64_t* n_clusters,
+                          void* stream) {
+    if (!n_clusters || n < 0 || (n > 0 && (!xyz || !label))) return set_error(GICP_EINVAL, "gicp_cluster: null / n");
+    if (!(tol > 0.0f) || !std::isfinite(tol)) return set_error(GICP_EINVAL, "gicp_cluster: tol must be > 0");
+    if (n >= (1ll << 31) - 1) return set_error(GICP_EINVAL, "gicp_cluster: n too large");
+    init_pool_once();
+    return launch_cluster(xyz, n, tol, min_size, label, n_clusters, (cudaStream_t)stream);
+}

@@ -265,6 +265,8 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
                           const BatchView& bv, int64_t nb);
 int attach_covariances(gicp_index_s* idx, const float* cov, cudaStream_t s);
 int attach_voxels(gicp_index_s* idx, const float* cov, cudaStream_t s);
+int launch_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t* label, int64_t* n_clusters,
+                   cudaStream_t s);
 int launch_ground_filter(const float* xyz, int64_t n, float cell, int min_count, uint8_t* keep, int32_t* count,
                          cudaStream_t s);
 size_t vgicp_scratch_bytes(int64_t ns);

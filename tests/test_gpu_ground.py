@@ -40,3 +40,37 @@ def test_ground_filter_edges(orc):
     assert g.ground_filter(torch.zeros((0, 3), dtype=torch.float32, device=DEV), 0.5, 3).numel() == 0
     with pytest.raises(g.GicpError):
         g.ground_filter(D(p), 0.0, 3)
+
+
+# --- Euclidean clustering (O10) ---------------------------------------------
+def test_cluster_random_sets(orc):
+    rng = np.random.default_rng(21)
+    for t in range(20):
+        p = rng.uniform(0, 10, (200, 3)).astype(np.float32)
+        lab, nc = g.cluster(D(p), 1.0, 1 + t % 3)
+        ol, onc = orc.cluster(p, 1.0, 1 + t % 3)
+        assert nc == onc and np.array_equal(lab.cpu().numpy(), ol)
+
+
+def test_cluster_ground_filtered_scan(orc):
+    """The paper's pipeline on a scan: ground filter, then clusters of the
+    vertical features (walls, posts, boxes); labels bit-exact vs the oracle."""
+    sc, _ = gen.scan(60_000, 300.0, 78)
+    _, first = np.unique(np.floor(sc / 0.25).astype(np.int64), axis=0, return_index=True)  # voxel filter (SPEC pre)
+    sc = np.ascontiguousarray(sc[np.sort(first)])
+    keep = g.ground_filter(D(sc), 0.5, 6).cpu().numpy()
+    feat = np.ascontiguousarray(sc[keep])
+    assert 500 < len(feat) < 0.8 * len(sc)
+    lab, nc = g.cluster(D(feat), 0.5, 10)
+    ol, onc = orc.cluster(feat, 0.5, 10)
+    assert nc == onc > 1 and np.array_equal(lab.cpu().numpy(), ol)
+
+
+def test_cluster_edges():
+    lab, nc = g.cluster(torch.zeros((0, 3), dtype=torch.float32, device=DEV), 1.0)
+    assert nc == 0 and lab.numel() == 0
+    same = torch.zeros((50, 3), dtype=torch.float32, device=DEV)  # coincident points: one cluster
+    lab, nc = g.cluster(same, 0.1)
+    assert nc == 1 and (lab == 0).all()
+    with pytest.raises(g.GicpError):
+        g.cluster(same, 0.0)
