@@ -149,6 +149,20 @@ def vg():
     print(json.dumps({"workload": "VGICP vs GICP, C3 100k scan vs 2M map (voxel 1.0 m)", **res}))
 
 
+def gc():
+    """z-vote ground filter + Euclidean clustering on the C3 scan (vehicle frame)."""
+    sc, _ = gen.scan(100_000, gen.C3_U, 1000)
+    _, first = np.unique(np.floor(sc / 0.25).astype(np.int64), axis=0, return_index=True)
+    vf = np.ascontiguousarray(sc[np.sort(first)])
+    sd = D(vf)
+    ms_g, keep = timed(lambda: g.ground_filter(sd, 0.5, 6))
+    feat = sd[keep].contiguous()
+    ms_c, (lab, nc) = timed(lambda: g.cluster(feat, 0.5, 10))
+    print(json.dumps({"workload": "ground filter + clustering, C3 scan voxel-filtered at 0.25 m",
+                      "points": int(sd.shape[0]), "kept": int(feat.shape[0]), "ground_filter_ms": ms_g,
+                      "cluster_ms": ms_c, "clusters": nc}))
+
+
 if __name__ == "__main__":
     args = sys.argv[1:] or ["c2", "c4", "c5"]
     i = 0
@@ -168,4 +182,6 @@ if __name__ == "__main__":
             kd()
         elif a == "vg":
             vg()
+        elif a == "gc":
+            gc()
         i += 1
