@@ -350,6 +350,25 @@ int gicp_ground_filter(const float* xyz, int64_t n, float cell, int min_count, u
 int gicp_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t* label, int64_t* n_clusters,
                  void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * Sliding-window submap (a GPU hash associating each pose on
+ * the race line with its map points; "points from M_i^psi instead of the entire
+ * unified map"; R26).
+ * gicp_submap_build -- bucket (device int32 [n]): each map point's arc-length
+ *   bucket in [0, n_buckets) (the caller's race-line parametrisation; the track
+ *   is closed). One stable sort by bucket + the bucket start table (a perfect
+ *   hash: bucket ids are dense). Synchronous. EINVAL on an id out of range.
+ * gicp_submap_query -- the map point indices of the buckets center - radius ..
+ *   center + radius (mod n_buckets, each bucket once: radius >= n_buckets / 2 is
+ *   the whole map), in that order, original order inside a bucket, into out
+ *   (device int32, capacity >= the count); *count (host). Stream-ordered.
+ * ------------------------------------------------------------------------- */
+typedef struct gicp_submap_s* gicp_submap;
+int gicp_submap_build(const int32_t* bucket, int64_t n, int n_buckets, gicp_submap* out, void* stream);
+int gicp_submap_query(gicp_submap sm, int center, int radius, int32_t* out, int64_t* count, void* stream);
+void gicp_submap_free(gicp_submap sm);
+
 #ifdef __cplusplus
 }
 #endif

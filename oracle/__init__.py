@@ -68,6 +68,8 @@ def lib():
         L.oracle_covariance_kd.argtypes = [P, i64, P, P, i64, i32, i32, f64, f64, f64, i32, P, i32, f64, P, P, i32]
         L.oracle_ground_filter.argtypes = [P, i64, f32, i32, P, P]
         L.oracle_cluster.argtypes = [P, i64, f32, i32, P]
+        L.oracle_submap_query.argtypes = [P, i64, i32, i32, i32, P]
+        L.oracle_submap_query.restype = i64
         L.oracle_cluster.restype = i64
         L.oracle_linearize_vgicp.argtypes = [P, P, i64, P, P, i64, f32, P, P, i32, i32, P, P, P]
         L.oracle_align_vgicp.argtypes = [P, P, i64, P, P, i64, f32, i32, P, ctypes.POINTER(AlignParams),
@@ -243,6 +245,16 @@ def cluster(xyz, tol, min_size=1):
     if nc < 0:
         raise OracleError(int(nc), "oracle_cluster")
     return lab, int(nc)
+
+
+def submap_query(bucket, n_buckets, center, radius):
+    """O11: point indices of the window of buckets around `center` (int32 [m])."""
+    b = np.ascontiguousarray(bucket, dtype=np.int32)
+    out = np.empty(max(1, b.size), np.int32)
+    m = lib().oracle_submap_query(_ptr(b), b.size, int(n_buckets), int(center), int(radius), _ptr(out))
+    if m < 0:
+        raise OracleError(int(m), "oracle_submap_query")
+    return out[:m].copy()
 
 
 def se3_exp(delta):

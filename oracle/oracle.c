@@ -25,6 +25,8 @@
  *   O7 oracle_linearize_vgicp / O8 oracle_align_vgicp  voxelized GICP (l.419):
  *                          voxel N, mean, mean covariance; pairs with the voxels
  *                          around fl32(T p); N-weighted Mahalanobis terms.
+ *   O11 oracle_submap_query  sliding-window submap: the points of the arc-length
+ *                          buckets around a pose (l.477-481).
  *   O10 oracle_cluster     Euclidean cluster extraction (l.549-559): connected
  *                          components under d2 <= tol^2, brute-force union-find.
  *   O9 oracle_ground_filter  z-vote ground filter: 2-D cell counts, keep cells
@@ -1275,4 +1277,26 @@ int64_t oracle_cluster(const float* xyz, int64_t n, float tol, int min_size, int
     for (int64_t i = 0; i < n; ++i) label[i] = (int32_t)rank[uf_find(par, i)];
     free(par); free(size); free(roots); free(rank);
     return nc;
+}
+
+/* -------------------------------------------------------------------------- */
+/* O11: sliding-window submap query ("associate each pose on  */
+/* the race line with its corresponding point cloud map" via a GPU hash; "points  */
+/* from M_i^psi instead of the entire unified map"; DESIGN R26)   */
+/* -------------------------------------------------------------------------- */
+
+/* points of the buckets center - radius .. center + radius (mod n_buckets, each
+ * bucket once; radius >= n_buckets / 2 covers the whole track), in window order
+ * (center - radius first), original order inside a bucket. Returns the count. */
+int64_t oracle_submap_query(const int32_t* bucket, int64_t n, int n_buckets, int center, int radius, int32_t* out) {
+    if (!bucket || n < 0 || n_buckets < 1 || radius < 0 || center < 0 || center >= n_buckets) return -1;
+    int64_t span = 2 * (int64_t)radius + 1;
+    if (span > n_buckets) span = n_buckets;
+    int64_t m = 0;
+    for (int64_t w = 0; w < span; ++w) {
+        const int b = (int)((((int64_t)center - radius + w) % n_buckets + n_buckets) % n_buckets);
+        for (int64_t i = 0; i < n; ++i)
+            if (bucket[i] == b) out[m++] = (int32_t)i;
+    }
+    return m;
 }

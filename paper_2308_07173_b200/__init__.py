@@ -74,6 +74,10 @@ _lib.gicp_linearize_vgicp.argtypes = [_P, _P, _i64, _P, _P, _P, _i32, _i32, _P, 
 _lib.gicp_align_vgicp.argtypes = [_P, _P, _i64, _P, _i32, _P, ctypes.POINTER(AlignParams), ctypes.POINTER(AlignResult),
                                   _P]
 _lib.gicp_ground_filter.argtypes = [_P, _i64, _f32, _i32, _P, _P, _P]
+_lib.gicp_submap_build.argtypes = [_P, _i64, _i32, ctypes.POINTER(_P), _P]
+_lib.gicp_submap_query.argtypes = [_P, _i32, _i32, _P, ctypes.POINTER(ctypes.c_int64), _P]
+_lib.gicp_submap_free.argtypes = [_P]
+_lib.gicp_submap_free.restype = None
 _lib.gicp_cluster.argtypes = [_P, _i64, _f32, _i32, _P, ctypes.POINTER(ctypes.c_int64), _P]
 _lib.gicp_covariances_kd.argtypes = [_P, _i64, _P, _P, _i64, _i32, ctypes.POINTER(CovParams), _P, _P]
 KERNELS = {"uniform": 0, "rbf": 1, "gaussian": 2, "polynomial": 3, "hi": 4, "laplacian": 5}
@@ -93,7 +97,7 @@ EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_fr
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
            "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd",
            "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter",
-           "gicp_cluster"]
+           "gicp_cluster", "gicp_submap_build", "gicp_submap_query", "gicp_submap_free"]
 
 
 class GicpError(RuntimeError):
@@ -430,6 +434,40 @@ def cluster(xyz: torch.Tensor, tol: float, min_size: int = 1):
     _check(_lib.gicp_cluster(_dptr(xyz) if n else None, n, float(tol), int(min_size), _dptr(lab) if n else None,
                              ctypes.byref(nc), _stream()))
     return lab, int(nc.value)
+
+
+class Submap:
+    """Arc-length bucketed map (gicp_submap_*): query(center, radius) -> the point
+    indices (int32 device) of the window of buckets around a race-line position."""
+
+    def __init__(self, bucket: torch.Tensor, n_buckets: int):
+        if bucket.dtype != torch.int32 or bucket.dim() != 1:
+            raise ValueError("bucket must be int32 [n]")
+        self._bucket = bucket.contiguous()
+        self.n = bucket.shape[0]
+        self.n_buckets = int(n_buckets)
+        self.device = bucket.device
+        h = _P()
+        _check(_lib.gicp_submap_build(_dptr(self._bucket) if self.n else None, self.n, self.n_buckets,
+                                      ctypes.byref(h), _stream()))
+        self._h = h
+
+    def query(self, center: int, radius: int) -> torch.Tensor:
+        out = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.device)
+        cnt = ctypes.c_int64(0)
+        _check(_lib.gicp_submap_query(self._h, int(center), int(radius), _dptr(out), ctypes.byref(cnt), _stream()))
+        return out[:cnt.value]
+
+    def free(self):
+        if self._h:
+            _lib.gicp_submap_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def version() -> int:

@@ -13,7 +13,6 @@
 
 #include "gicp_internal.cuh"
 
-#define GICP_API extern "C" __attribute__((visibility("default")))
 
 namespace gicp {
 

@@ -19,6 +19,7 @@
 #include "../../include/gicp.h"
 
 #define GICP_HD __host__ __device__ __forceinline__
+#define GICP_API extern "C" __attribute__((visibility("default")))
 
 namespace gicp {
 

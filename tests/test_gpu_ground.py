@@ -74,3 +74,17 @@ def test_cluster_edges():
     assert nc == 1 and (lab == 0).all()
     with pytest.raises(g.GicpError):
         g.cluster(same, 0.0)
+
+
+# --- sliding-window submap (O11) ----------------------------------------------
+def test_submap_queries_match_the_oracle(orc):
+    mp = gen.racetrack_map(2_000_000, 1)
+    nb = 240  # ~10 m buckets of the 2408 m oval: bucket = the angle around the oval centre (a race-line proxy)
+    b = (np.floor((np.arctan2(mp[:, 1], mp[:, 0]) + np.pi) / (2 * np.pi) * nb).astype(np.int64) % nb).astype(np.int32)
+    sm = g.Submap(D(b), nb)
+    for center, radius in ((0, 0), (0, 3), (17, 1), (239, 5), (120, 500)):
+        got = sm.query(center, radius).cpu().numpy()
+        assert np.array_equal(got, orc.submap_query(b, nb, center, radius)), (center, radius)
+    sm.free()
+    with pytest.raises(g.GicpError):
+        g.Submap(D(np.array([0, 5, 240], np.int32)), 240)
