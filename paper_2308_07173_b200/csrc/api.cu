@@ -185,7 +185,57 @@ int wait_mapped(MappedOut* m, unsigned seq, cudaStream_t s) {
     }
 }
 
+struct Bytes256 {
+    unsigned char b[256];
+};
+
+__global__ void k_export_bytes(const unsigned char* __restrict__ src, unsigned char* dst, size_t n) {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+}
+
+__global__ void k_import_bytes(Bytes256 v, unsigned char* __restrict__ dst, size_t n) {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = v.b[i];
+}
+
 }  // namespace
+
+int read_small(void* dst, const void* src_dev, size_t bytes, cudaStream_t s) {
+    constexpr size_t kCap = 1 << 16;
+    static thread_local unsigned char* h = nullptr;
+    static thread_local unsigned char* d = nullptr;
+    if (bytes > kCap) {  // large: a plain copy
+        int rc = check_cuda(cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+        return rc ? rc : check_cuda(cudaStreamSynchronize(s), "D2H sync");
+    }
+    if (!h) {
+        void* p = nullptr;
+        void* dp = nullptr;
+        if (cudaHostAlloc(&p, kCap, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+            cudaHostGetDevicePointer(&dp, p, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (p) cudaFreeHost(p);
+            return set_error(GICP_ENOMEM, "host-mapped staging buffer");
+        }
+        h = (unsigned char*)p;
+        d = (unsigned char*)dp;
+    }
+    if (bytes == 0) return GICP_OK;
+    k_export_bytes<<<1, 256, 0, s>>>((const unsigned char*)src_dev, d, bytes);
+    int rc = check_cuda(cudaGetLastError(), "small read");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(s), "small read");
+    if (!rc) std::memcpy(dst, h, bytes);
+    return rc;
+}
+
+int write_small(void* dst_dev, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes > sizeof(Bytes256)) return check_cuda(cudaMemcpyAsync(dst_dev, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+    Bytes256 v;
+    std::memcpy(v.b, src, bytes);
+    k_import_bytes<<<1, 256, 0, s>>>(v, (unsigned char*)dst_dev, bytes);
+    return check_cuda(cudaGetLastError(), "small write");
+}
+
 }  // namespace gicp
 
 using namespace gicp;
@@ -1017,9 +1067,7 @@ GICP_API int gicp_align_vgicp(const float* src, const float* src_cov, int64_t ns
     double h[29];
     auto lin = [&](const double* T, const double* piv, int flags) -> int {
         int r = launch_linearize_vgicp(src, src_cov, ns, tgt, T, piv, mode, flags, base, d_out, s, &ls);
-        if (!r) r = check_cuda(cudaMemcpyAsync(mo->h, d_out, 29 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-        if (!r) r = check_cuda(cudaStreamSynchronize(s), "vgicp sync");
-        if (!r) std::memcpy(h, mo->h, sizeof(h));
+        if (!r) r = read_small(h, d_out, sizeof(h), s);
         return r;
     };
     double T[16];

@@ -153,8 +153,7 @@ int launch_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t
     k_label<<<G, 256, 0, s>>>(idx->pts, n, par, size, rank, min_size, label);
     int h = 0;
     rc = check_cuda(cudaGetLastError(), "cluster kernels");
-    if (!rc) rc = check_cuda(cudaMemcpyAsync(&h, ncl, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
-    if (!rc) rc = check_cuda(cudaStreamSynchronize(s), "cluster");
+    if (!rc) rc = read_small(&h, ncl, sizeof(int), s);
     cudaFreeAsync(buf, s);
     gicp_index_free(idx);
     *n_clusters = h;

@@ -401,11 +401,10 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     DevBuf bb;
     if ((rc = alloc_async(bb, 16 * sizeof(int), s))) return rc;
     int init[8] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN, 0, 0};
-    if ((rc = check_cuda(cudaMemcpyAsync(bb.p, init, sizeof(init), cudaMemcpyHostToDevice, s), "H2D"))) return rc;
+    if ((rc = write_small(bb.p, init, sizeof(init), s))) return rc;
     k_bbox<<<(unsigned)std::min<int64_t>(grid_for(n, 256), 148 * 8), 256, 0, s>>>(xyz, n, (int*)bb.p);
     int res[8];
-    if ((rc = check_cuda(cudaMemcpyAsync(res, bb.p, sizeof(res), cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
-    if ((rc = check_cuda(cudaStreamSynchronize(s), "bbox"))) return rc;
+    if ((rc = read_small(res, bb.p, sizeof(res), s))) return rc;
     if (res[6] != 0) return set_error(GICP_EINVAL, "non-finite coordinate in the target cloud");
     float mn[3], mx[3];
     for (int a = 0; a < 3; ++a) {
@@ -427,8 +426,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if ((rc = check_cuda(cudaMemsetAsync(acc.p, 0, 16, s), "memset"))) return rc;
         k_runlen2<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)k1.p, n, (unsigned long long*)acc.p);
         unsigned long long sum2 = 0;
-        if ((rc = check_cuda(cudaMemcpyAsync(&sum2, acc.p, 8, cudaMemcpyDeviceToHost, s), "D2H"))) return rc;
-        if ((rc = check_cuda(cudaStreamSynchronize(s), "auto cell"))) return rc;
+        if ((rc = read_small(&sum2, acc.p, 8, s))) return rc;
         // point-weighted mean voxel occupancy at the trial cell; aim at ~12
         const double med = std::max(1.0, (double)sum2 / (double)n) / 1.5;
         cell_size = (float)(trial * std::sqrt(GICP_AUTO_OCC / med));
@@ -449,9 +447,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     if ((rc = check_cuda(cudaMemsetAsync(cnt.p, 0, kMaxLevels * sizeof(int), s), "memset"))) return rc;
     k_level_count<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, L, (int*)cnt.p);
     int counts[kMaxLevels] = {0};
-    if ((rc = check_cuda(cudaMemcpyAsync(counts, cnt.p, sizeof(counts), cudaMemcpyDeviceToHost, s), "D2H")))
-        return rc;
-    if ((rc = check_cuda(cudaStreamSynchronize(s), "level counts"))) return rc;
+    if ((rc = read_small(counts, cnt.p, sizeof(counts), s))) return rc;
 
     gicp_index_s* idx = new gicp_index_s();
     idx->n = n;
@@ -529,9 +525,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
             idx->device_bytes += n * 8 + 27 * nv * 8;
             if ((rc = check_cuda(cudaGetLastError(), "adjacency kernel"))) return fail(rc);
         }
-        if ((rc = check_cuda(cudaMemcpyAsync(&adj_overflow, (int*)tot.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s),
-                             "adjacency flag")))
-            return fail(rc);
+        if ((rc = read_small(&adj_overflow, (int*)tot.p + 1, sizeof(int), s))) return fail(rc);
     }
     if ((rc = check_cuda(cudaStreamSynchronize(s), "build"))) return fail(rc);
     if (adj_overflow) {  // a voxel too full for the packed entry: queries probe the hash instead

@@ -87,10 +87,7 @@ GICP_API int gicp_submap_build(const int32_t* bucket, int64_t n, int n_buckets, 
         rc = check_cuda(cudaGetLastError(), "submap build");
     }
     std::vector<int> hc((size_t)n_buckets + 1, 0);
-    if (!rc)
-        rc = check_cuda(cudaMemcpyAsync(hc.data(), cnt, (n_buckets + 1) * sizeof(int), cudaMemcpyDeviceToHost, s),
-                        "D2H");
-    if (!rc) rc = check_cuda(cudaStreamSynchronize(s), "submap build");
+    if (!rc) rc = read_small(hc.data(), cnt, (n_buckets + 1) * sizeof(int), s);
     cudaFreeAsync(buf, s);
     if (!rc && hc[n_buckets]) rc = set_error(GICP_EINVAL, "gicp_submap_build: bucket id outside [0, n_buckets)");
     if (rc) {
