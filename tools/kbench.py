@@ -14,7 +14,7 @@ reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 sc, mp, T, T0 = gen.config_c3()
 md = torch.from_numpy(np.array(mp)).cuda()
 sd = torch.from_numpy(np.array(sc)).cuda()
-im = g.build_index(md, 0.5)
+im = g.build_index(md, float(os.environ.get("KB_CELL", "0.5")))
 isc = g.build_index(sd, 0.0)
 out = (torch.empty((mp.shape[0], 20), dtype=torch.int32, device="cuda"),
        torch.empty((mp.shape[0], 20), dtype=torch.float32, device="cuda"),
