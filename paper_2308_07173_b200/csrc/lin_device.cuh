@@ -15,7 +15,7 @@ constexpr int kLinAcc = 28;  // H(21) b(6) e(1)
 // per-pair terms for the residual d (fp32) at the transformed point pp, added
 // to the fp64 acc (times w when WEIGHTED: the voxel size N of VGICP)
 template <bool ERROR_ONLY, bool WEIGHTED = false>
-__device__ __forceinline__ void accumulate_terms(const Pose& P, const double pp[3], const float dx, const float dy,
+__device__ __forceinline__ double accumulate_terms(const Pose& P, const double pp[3], const float dx, const float dy,
                                                  const float dz, const float cp[6], const float cq[6],
                                                  double acc[kLinAcc], const double w = 1.0) {
     // A = C^q + R C^p R^T
@@ -46,8 +46,10 @@ __device__ __forceinline__ void accumulate_terms(const Pose& P, const double pp[
     const float mdx = M00 * dx + M01 * dy + M02 * dz;
     const float mdy = M01 * dx + M11 * dy + M12 * dz;
     const float mdz = M02 * dx + M12 * dy + M22 * dz;
-    acc[27] += WEIGHTED ? w * (double)(dx * mdx + dy * mdy + dz * mdz) : (double)(dx * mdx + dy * mdy + dz * mdz);
-    if (ERROR_ONLY) return;
+    const double et =
+        WEIGHTED ? w * (double)(dx * mdx + dy * mdy + dz * mdz) : (double)(dx * mdx + dy * mdy + dz * mdz);
+    acc[27] += et;
+    if (ERROR_ONLY) return et;
     // lever arm about the pivot (fp64 difference, then fp32)
     const float px = (float)(pp[0] - P.c[0]), py = (float)(pp[1] - P.c[1]), pz = (float)(pp[2] - P.c[2]);
     // P = skew(p') = [[0,-z,y],[z,0,-x],[-y,x,0]];  MP = M P
@@ -74,6 +76,7 @@ __device__ __forceinline__ void accumulate_terms(const Pose& P, const double pp[
                          H25, M00, M01, M02, M11, M12, M22, b0,  b1,  b2,  -mdx, -mdy, -mdz};
 #pragma unroll
     for (int c = 0; c < 27; ++c) acc[c] += WEIGHTED ? w * (double)v[c] : (double)v[c];
+    return et;  // the cost term this pair added
 }
 
 

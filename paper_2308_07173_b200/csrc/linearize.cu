@@ -286,12 +286,12 @@ __device__ __forceinline__ void load_cov6(const float* __restrict__ c, int64_t r
 
 // per-point terms of one inlier, accumulated into fp64 acc[28]
 template <bool ERROR_ONLY>
-__device__ __forceinline__ void accumulate_point(const Pose& P, const double pp[3], float qx, float qy, float qz,
-                                                 const float cp[6], const float cq[6], double acc[kNumAcc]) {
+__device__ __forceinline__ double accumulate_point(const Pose& P, const double pp[3], float qx, float qy, float qz,
+                                                   const float cp[6], const float cq[6], double acc[kNumAcc]) {
     const float dx = (float)((double)qx - pp[0]);
     const float dy = (float)((double)qy - pp[1]);
     const float dz = (float)((double)qz - pp[2]);
-    accumulate_terms<ERROR_ONLY>(P, pp, dx, dy, dz, cp, cq, acc);
+    return accumulate_terms<ERROR_ONLY>(P, pp, dx, dy, dz, cp, cq, acc);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -407,27 +407,33 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         if (!active) continue;
         float cp[6], cq[6];
         if (DUAL || orig >= 0) load_cov6(src_cov, i, cp);
+        double e_new = 0.0;
+        if (orig >= 0) {
+            if (SORTED)
+                load_cov_sorted(tgt_cov_sorted, spos, cq);
+            else
+                load_cov6(tgt_cov, orig, cq);
+            e_new = accumulate_point<ERROR_ONLY>(sP, pp, qx, qy, qz, cp, cq, acc);
+            cnt += 1.0;
+        }
         if (DUAL) {  // the trial cost with the previous correspondences
             const int c = corr_old[i];
             if (c >= 0 && c < nt) {
-                const float4 q = SPOS ? __ldg(pts + c) : __ldg(pts_orig + c);
-                const int so = SPOS ? c : __float_as_int(q.w);
-                const int oo = SPOS ? __float_as_int(q.w) : c;
-                if (SORTED)
-                    load_cov_sorted(tgt_cov_sorted, so, cq);
-                else
-                    load_cov6(tgt_cov, oo, cq);
-                accumulate_point<true>(sP, pp, q.x, q.y, q.z, cp, cq, eold);
+                if (orig >= 0 && c == (SPOS ? spos : orig)) {
+                    eold[27] += e_new;  // the same pair at the same pose: the same term, bitwise
+                } else {
+                    const float4 q = SPOS ? __ldg(pts + c) : __ldg(pts_orig + c);
+                    const int so = SPOS ? c : __float_as_int(q.w);
+                    const int oo = SPOS ? __float_as_int(q.w) : c;
+                    if (SORTED)
+                        load_cov_sorted(tgt_cov_sorted, so, cq);
+                    else
+                        load_cov6(tgt_cov, oo, cq);
+                    accumulate_point<true>(sP, pp, q.x, q.y, q.z, cp, cq, eold);
+                }
                 cnt_old += 1.0;
             }
         }
-        if (orig < 0) continue;
-        if (SORTED)
-            load_cov_sorted(tgt_cov_sorted, spos, cq);
-        else
-            load_cov6(tgt_cov, orig, cq);
-        accumulate_point<ERROR_ONLY>(sP, pp, qx, qy, qz, cp, cq, acc);
-        cnt += 1.0;
     }
     LPROF({
         const unsigned dt = (unsigned)min(clock64() - tk0, 0xffffffffll);
