@@ -36,6 +36,7 @@ import numpy as np  # noqa: E402
 
 K = 20
 EPS = 1e-3
+LIN_BYTES_PER_PT = 80   # linearize, per source point per iteration
 MAP_CELL = 0.5          # m, ~1.15 x the 20-NN radius at 31 pts/m^2
 METRIC = "kNN+covariance points/sec (k=20) and GICP iters/sec; % HBM roofline"
 WORKLOAD = "C3 scan-to-map: 100k-point scan vs 2M-point racetrack map, k=20, GICP to convergence"
@@ -226,7 +227,10 @@ def main():
         rec = []
         step_ms = []
         t_start = time.time()
-        for _ in range(args.steps):
+        for si in range(args.steps):
+            # per-launch CUDA events around gicp_align's linearisations during the last
+            # timed step only (the event records would otherwise add ~4 % to every step)
+            g.align_timing(si == args.steps - 1)
             flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the timed region
             if world > 1:
                 dist.barrier()
@@ -238,6 +242,7 @@ def main():
             t1.record(stream)
             torch.cuda.synchronize()
             step_ms.append(t0.elapsed_time(t1))
+        lin_ms, lin_n, lin_pts = g.align_timing(False)
         t_end = time.time()
         time.sleep(0.15)
     clocks = clk.summary(t_start, t_end + 0.1)
@@ -257,9 +262,22 @@ def main():
 
     value = world * n_pts / (ms * 1e-3)
     peak, peak_kind = peaks()
-    achieved = mp.shape[0] * BYTES_PER_PT / (knncov_ms * 1e-3) / 1e9
-    traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
+    achieved = mp.shape[0] * BYTES_PER_PT / (knncov_ms * 1e-3) / 1e9
+    # the linearisation (the step's largest kernel share: 26 launches per step):
+    # algorithmic bytes per source point per launch = 12 xyz + 24 cov
+    # + 40 target float4 + cov + 4 corr = 80 B; average launch time from the events
+    lin_bytes = LIN_BYTES_PER_PT * lin_pts
+    lin_launch_ms = lin_ms[0] / max(lin_n[0], 1)
+    lin_achieved = lin_bytes / (lin_launch_ms * 1e-3) / 1e9 if lin_n[0] else None
+    lin_step_ms = sum(lin_ms)  # one step's worth (the last timed step)
+    lin_traffic = None
+    if os.path.exists(tp):
+        try:
+            lin_traffic = json.load(open(tp)).get("k_linearize_dual_bytes_per_launch")
+        except Exception:
+            lin_traffic = None
+    traffic = None
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("k_knn_self_map_bytes_per_launch")
@@ -340,6 +358,17 @@ def main():
                "sample": f"{args.cpu_queries} seeded map points, kNN(k=20)+covariance vs the full 2M map "
                          f"(brute force), {dt:.1f} s"}
 
+    roof_knn = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_kind": peak_kind, "kernel": "k_knn_self (fused kNN+cov, map: level, escalate, exact)",
+                "bytes_per_point": BYTES_PER_PT, "ms_per_step": knncov_ms}
+    roof_lin = None
+    if lin_achieved is not None:
+        roof_lin = {"bound": "hbm", "achieved": lin_achieved, "peak": peak, "unit": "GB/s",
+                    "frac": lin_achieved / peak, "traffic": lin_traffic, "peak_kind": peak_kind,
+                    "kernel": "k_linearize (speculative dual launch inside gicp_align)",
+                    "bytes_per_point": LIN_BYTES_PER_PT, "points": lin_pts, "launch_ms": lin_launch_ms,
+                    "launches_per_step": sum(lin_n), "ms_per_step": lin_step_ms,
+                    "timed": "CUDA events around every linearisation launch of the last timed step"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
@@ -354,10 +383,10 @@ def main():
                              "scan_index_knn_cov": scan_ms, "align": align_ms, "align_iterations": iters},
             "knn_cov_kernel_pts_per_s": mp.shape[0] / (knncov_ms * 1e-3),
             "align_translation_error_m": dt_err,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_knn_self (fused kNN+cov, map)",
-                         "bytes_per_point": BYTES_PER_PT},
+            # the kernel with the largest share of the step (per-step device time)
+            "roofline": (roof_knn if knncov_ms >= lin_step_ms or lin_achieved is None else roof_lin),
+            "roofline_knn_cov": roof_knn,
+            "roofline_linearize": roof_lin,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,

@@ -369,6 +369,15 @@ int gicp_submap_build(const int32_t* bucket, int64_t n, int n_buckets, gicp_subm
 int gicp_submap_query(gicp_submap sm, int center, int radius, int32_t* out, int64_t* count, void* stream);
 void gicp_submap_free(gicp_submap sm);
 
+
+/* gicp_align_timing -- opt-in diagnostics (bench.py's roofline): while enabled,
+ * gicp_align records CUDA events on its stream around every linearisation launch
+ * of the calling thread. The call returns the accumulated device milliseconds and
+ * launch counts per kind ([0] speculative dual launches, [1] full linearisations,
+ * [2] trial costs) and the source size of the last one, resets them, and sets the
+ * enable flag. Host pointers, nullable. */
+int gicp_align_timing(int enable, double* ms, int64_t* launches, int64_t* points);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ _lib.gicp_submap_build.argtypes = [_P, _i64, _i32, ctypes.POINTER(_P), _P]
 _lib.gicp_submap_query.argtypes = [_P, _i32, _i32, _P, ctypes.POINTER(ctypes.c_int64), _P]
 _lib.gicp_submap_free.argtypes = [_P]
 _lib.gicp_submap_free.restype = None
+_lib.gicp_align_timing.argtypes = [_i32, _P, _P, _P]
 _lib.gicp_cluster.argtypes = [_P, _i64, _f32, _i32, _P, ctypes.POINTER(ctypes.c_int64), _P]
 _lib.gicp_covariances_kd.argtypes = [_P, _i64, _P, _P, _i64, _i32, ctypes.POINTER(CovParams), _P, _P]
 KERNELS = {"uniform": 0, "rbf": 1, "gaussian": 2, "polynomial": 3, "hi": 4, "laplacian": 5}
@@ -97,7 +98,7 @@ EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_fr
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
            "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd",
            "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter",
-           "gicp_cluster", "gicp_submap_build", "gicp_submap_query", "gicp_submap_free"]
+           "gicp_cluster", "gicp_submap_build", "gicp_submap_query", "gicp_submap_free", "gicp_align_timing"]
 
 
 class GicpError(RuntimeError):
@@ -468,6 +469,17 @@ class Submap:
             self.free()
         except Exception:
             pass
+
+
+def align_timing(enable: bool = True):
+    """Per-launch device timing of gicp_align's linearisations on this thread:
+    returns (ms [dual, full, trial], launches [dual, full, trial], points) accumulated
+    since the previous call, resets them and sets the enable flag."""
+    ms = (ctypes.c_double * 3)()
+    n = (ctypes.c_int64 * 3)()
+    pts = ctypes.c_int64(0)
+    _check(_lib.gicp_align_timing(int(bool(enable)), ctypes.cast(ms, _P), ctypes.cast(n, _P), ctypes.byref(pts)))
+    return list(ms), list(n), int(pts.value)
 
 
 def version() -> int:

@@ -185,6 +185,36 @@ int wait_mapped(MappedOut* m, unsigned seq, cudaStream_t s) {
     }
 }
 
+// opt-in per-launch device timing of gicp_align's linearisations (CUDA events on
+// the launching stream): [0] speculative dual launches, [1] full linearisations,
+// [2] trial costs. gicp_align_timing() enables / reads / resets it.
+struct KernelTiming {
+    static constexpr int kCap = 256;  // launches timed per gicp_align call
+    int on = 0;
+    cudaEvent_t e[2 * kCap] = {};
+    int kind[kCap] = {};
+    int used = 0;  // event pairs recorded by the current call
+    double ms[3] = {0, 0, 0};
+    int64_t n[3] = {0, 0, 0};
+    int64_t points = 0;
+};
+KernelTiming& kernel_timing() {
+    static thread_local KernelTiming t;
+    return t;
+}
+// read the recorded pairs (their stream has been synchronised) into the totals
+void kernel_timing_collect(KernelTiming& t) {
+    for (int i = 0; i < t.used; ++i) {
+        float m = 0.f;
+        if (cudaEventElapsedTime(&m, t.e[2 * i], t.e[2 * i + 1]) == cudaSuccess) {
+            t.ms[t.kind[i]] += m;
+            t.n[t.kind[i]] += 1;
+        }
+    }
+    cudaGetLastError();
+    t.used = 0;
+}
+
 struct Bytes256 {
     unsigned char b[256];
 };
@@ -429,10 +459,20 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     // one launch + one sync per evaluation: `old` != nullptr also evaluates the
     // trial cost with the previous correspondences (values 29, 30)
     ls.flag = mo->dflag;
+    KernelTiming& kt = kernel_timing();
     auto go = [&](const double* T, const double* piv, int flags, int32_t* corr, const int32_t* old) -> int {
         ls.seq = ++mo->seq;
-        const int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, flags, mo->d,
-                                        corr, s, &ls, old);
+        // per-launch device time of the linearisations (bench.py's roofline): event
+        // pairs on the stream, read once the alignment has finished
+        const bool timed = kt.on && kt.used < KernelTiming::kCap;
+        if (timed) cudaEventRecord(kt.e[2 * kt.used], s);
+        int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, flags, mo->d,
+                                  corr, s, &ls, old);
+        if (timed) {
+            cudaEventRecord(kt.e[2 * kt.used + 1], s);
+            kt.kind[kt.used++] = (old != nullptr) ? 0 : ((flags & GICP_LIN_ERROR_ONLY) ? 2 : 1);
+            kt.points = ns;
+        }
         return rc ? rc : wait_mapped(mo, ls.seq, s);
     };
     auto lin = [&](const double* T, const double* piv, int32_t* corr, const int32_t* old) -> int {
@@ -549,6 +589,10 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
             piv[2] = T[11];
             if ((rc = lin(T, piv, corr_a, nullptr)) == GICP_OK) std::memcpy(lin29, h, sizeof(lin29));
         }
+    }
+    if (kt.used) {
+        cudaStreamSynchronize(s);
+        kernel_timing_collect(kt);
     }
     cudaFreeAsync(scratch, s);
     std::memcpy(res->T, T, sizeof(T));
@@ -1167,4 +1211,28 @@ GICP_API int gicp_cluster(const float* xyz, int64_t n, float tol, int min_size, 
     if (n >= (1ll << 31) - 1) return set_error(GICP_EINVAL, "gicp_cluster: n too large");
     init_pool_once();
     return launch_cluster(xyz, n, tol, min_size, label, n_clusters, (cudaStream_t)stream);
+}
+
+// ---- diagnostics ----------------------------------------------------------------
+GICP_API int gicp_align_timing(int enable, double* ms /* host [3] or NULL */, int64_t* launches /* host [3] */,
+                               int64_t* points) {
+    KernelTiming& t = kernel_timing();
+    if (ms)
+        for (int k = 0; k < 3; ++k) ms[k] = t.ms[k];
+    if (launches)
+        for (int k = 0; k < 3; ++k) launches[k] = t.n[k];
+    if (points) *points = t.points;
+    for (int k = 0; k < 3; ++k) {
+        t.ms[k] = 0.0;
+        t.n[k] = 0;
+    }
+    if (enable && !t.e[0]) {
+        for (auto& ev : t.e)
+            if (cudaEventCreate(&ev) != cudaSuccess) {
+                cudaGetLastError();
+                return set_error(GICP_ECUDA, "gicp_align_timing: event creation failed");
+            }
+    }
+    t.on = enable ? 1 : 0;
+    return GICP_OK;
 }

@@ -23,9 +23,10 @@ def main():
 
     def step():
         imap = g.build_index(map_d, bench.MAP_CELL)
-        _, _, cov_map = g.knn_cov_self(imap, bench.K, bench.EPS)
+        _, _, cov_map = g.knn_cov_self(imap, bench.K, bench.EPS, with_nbr=True)
+        g.attach_cov(imap, cov_map)
         iscan = g.build_index(scan_d, 0.0)
-        _, _, cov_scan = g.knn_cov_self(iscan, bench.K, bench.EPS)
+        _, _, cov_scan = g.knn_cov_self(iscan, bench.K, bench.EPS, with_nbr=True)
         if only != "knn":
             T, info = g.align(scan_d, cov_scan, imap, cov_map, T0)
         torch.cuda.synchronize()
