@@ -257,8 +257,13 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
                      const int32_t* corr_old = nullptr);
 // the pose block of a launch: R, t (fp64 and fp32 R) and the perturbation pivot
 Pose make_pose(const double T[16], const double* pivot);
+// lanes per source point in the linearisation (the candidate scan is split
+// between them: more warps in flight for the latency-bound 1-NN search)
+#ifndef GICP_LIN_TEAM
+#define GICP_LIN_TEAM 1  // measured: 2 lanes +15 %, 4 lanes +48 % (the per-warp reductions double)
+#endif
 // points per linearize block (the fixed partition of every registration)
-constexpr int kLinPPB = 256;
+constexpr int kLinPPB = 256 / GICP_LIN_TEAM;
 // one launch over nb blocks: single (bv.btab == nullptr, P) or batched (bv)
 int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                           const float* tgt_cov, const Pose& P, float max_corr_dist, int flags, double* out29,

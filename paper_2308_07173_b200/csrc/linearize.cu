@@ -25,8 +25,9 @@ namespace gicp {
 namespace {
 
 constexpr int kLinBlock = 256;
-constexpr int kPPT = 1;                       // points per thread
-constexpr int kPPB = kLinBlock * kPPT;        // points per block (fixed: defines the partition)
+constexpr int kPPT = 1;                       // points per team
+constexpr int kTeam = GICP_LIN_TEAM;          // lanes per point (adjacent lanes of a warp)
+constexpr int kPPB = kLinBlock / kTeam * kPPT;  // points per block (fixed: defines the partition)
 static_assert(kPPB == kLinPPB, "kLinPPB (gicp_internal.cuh) is the partition");
 constexpr int kNumAcc = 28;                   // H(21) b(6) e(1); count kept separately
 constexpr int kNV = 31;                       // reduced values: 28 + count + (DUAL) e_old + count_old
@@ -65,7 +66,7 @@ struct Levels {
 // coarser levels up to `ring_level`, then ring expansion there.
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
                                           float qy, float qz, float r2, unsigned long long& best, int& bj,
-                                          int& overflow) {
+                                          int& overflow, const int t) {
     // the key (d2 bits << 32 | original index) is kept as two words: the common
     // case (d2 larger) is one 32-bit compare, and only the sorted position of the
     // winner is tracked (its coordinates are loaded once, by the caller)
@@ -83,6 +84,19 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     };
     auto consider = [&](int j) { consider_p(j, __ldg(pts + j)); };
     auto finish = [&]() { best = ((unsigned long long)bh << 32) | bo; };
+    // the team's lanes split the level-0 candidates; their bests combine by a
+    // butterfly min of the (d2 bits, original index) keys after every voxel
+    auto team_min = [&]() {
+#pragma unroll
+        for (int o = 1; o < kTeam; o <<= 1) {
+            const unsigned ph = __shfl_xor_sync(0xffffffffu, bh, o), po = __shfl_xor_sync(0xffffffffu, bo, o);
+            const int pj = __shfl_xor_sync(0xffffffffu, bj, o);
+            const bool better = ph < bh || (ph == bh && po < bo);
+            bh = better ? ph : bh;
+            bo = better ? po : bo;
+            bj = better ? pj : bj;
+        }
+    };
     auto scan = [&](int2 rng) {
         for (int j = rng.x; j < rng.y; ++j) consider(j);
     };
@@ -161,15 +175,20 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             }
             const int len = r.y - r.x;
             const int lmax = __reduce_max_sync(0xffffffffu, len);
-            for (int j = 0; j < lmax; j += kUnroll) {
+            for (int j = 0; j < lmax; j += kUnroll * kTeam) {
                 float4 pv[kUnroll];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-                    if (j + u < len) pv[u] = __ldg(pts + r.x + j + u);
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int c = j + u * kTeam + t;
+                    if (c < len) pv[u] = __ldg(pts + r.x + c);
+                }
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-                    if (j + u < len) consider_p(r.x + j + u, pv[u]);
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int c = j + u * kTeam + t;
+                    if (c < len) consider_p(r.x + c, pv[u]);
+                }
             }
+            if (kTeam > 1) team_min();
         }
         if (!active) { finish(); return; }
         const float m = cube_margin(G, s, slack, 1);
@@ -347,10 +366,11 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     double cnt = 0.0, cnt_old = 0.0;
     double eold[kNumAcc];
     eold[27] = 0.0;
-    const int64_t base = p0 + (int64_t)blk * kPPB + threadIdx.x;
+    const int tl = (int)(threadIdx.x % kTeam);  // lane within the point's team
+    const int64_t base = p0 + (int64_t)blk * kPPB + threadIdx.x / kTeam;
 #pragma unroll 1
     for (int k = 0; k < kPPT; ++k) {
-        const int64_t i = base + (int64_t)k * kLinBlock;
+        const int64_t i = base + (int64_t)k * (kLinBlock / kTeam);
         const bool active = i < pend;  // warp-uniform loop: every lane reaches the search
         double pp[3] = {0.0, 0.0, 0.0};
         if (active) {
@@ -378,7 +398,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             unsigned long long best;
             int bj, ovf;
             LPROF(const long long t0 = clock64();)
-            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bj, ovf);
+            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bj, ovf, tl);
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
@@ -395,7 +415,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                 const bool inl = best != kEmptyKey && bd2 < r2;
                 orig = inl ? (int)(best & 0xffffffffu) : -1;
                 spos = inl ? bj : -1;
-                if (corr) corr[i] = SPOS ? spos : orig;
+                if (corr && tl == 0) corr[i] = SPOS ? spos : orig;
                 if (inl) {
                     const float4 q = __ldg(pts + bj);
                     qx = q.x;
@@ -406,9 +426,11 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         }
         if (!active) continue;
         float cp[6], cq[6];
-        if (DUAL || orig >= 0) load_cov6(src_cov, i, cp);
+        // lane 0 of the team adds the new pair, the last lane the DUAL trial term
+        const bool do_new = tl == 0, do_old = DUAL && tl == kTeam - 1;
+        if ((do_new && orig >= 0) || do_old) load_cov6(src_cov, i, cp);
         double e_new = 0.0;
-        if (orig >= 0) {
+        if (do_new && orig >= 0) {
             if (SORTED)
                 load_cov_sorted(tgt_cov_sorted, spos, cq);
             else
@@ -416,10 +438,10 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             e_new = accumulate_point<ERROR_ONLY>(sP, pp, qx, qy, qz, cp, cq, acc);
             cnt += 1.0;
         }
-        if (DUAL) {  // the trial cost with the previous correspondences
+        if (do_old) {  // the trial cost with the previous correspondences
             const int c = corr_old[i];
             if (c >= 0 && c < nt) {
-                if (orig >= 0 && c == (SPOS ? spos : orig)) {
+                if (kTeam == 1 && orig >= 0 && c == (SPOS ? spos : orig)) {
                     eold[27] += e_new;  // the same pair at the same pose: the same term, bitwise
                 } else {
                     const float4 q = SPOS ? __ldg(pts + c) : __ldg(pts_orig + c);

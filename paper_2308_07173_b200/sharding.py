@@ -2,7 +2,7 @@
 
 The target map/index is replicated on every rank; the source points of a
 registration are split into a FIXED global set of chunks (aligned to the
-linearize kernel's 256-point blocks, independent of the world size), each rank
+linearize kernel's blocks (256-point multiples), independent of the world size), each rank
 linearises its chunks (gicp_linearize on its GPU), the 29-value chunk partials are
 all-gathered over NCCL (NVLink) and summed in chunk order on every rank. Because
 the chunking and the summation order do not depend on the number of ranks, H, b
@@ -15,7 +15,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-PPB = 256          # points per linearize block (csrc/linearize.cu kPPB)
+PPB = 256          # chunk alignment: a multiple of every linearize block size (kLinPPB = 256 / team)
 NUM_CHUNKS = 8     # fixed global chunk count (= the largest world size served)
 
 
