@@ -470,22 +470,35 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     constexpr int NV = DUAL ? kNV : kNumAcc + 1;
     __shared__ double sh[kLinBlock / 32][kNV];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int c = 0; c < kNumAcc; ++c) {
-        if (ERROR_ONLY && c < 27) continue;
-        const double v = warp_sum(acc[c]);
-        if (lane == 0) sh[wid][c] = v;
-    }
-    {
-        const double v = warp_sum(cnt);
-        if (lane == 0) sh[wid][kNumAcc] = v;
-    }
-    if (DUAL) {
-        const double v1 = warp_sum(eold[27]), v2 = warp_sum(cnt_old);
+    if (ERROR_ONLY) {
+        const double v = warp_sum(acc[27]), n = warp_sum(cnt);
         if (lane == 0) {
-            sh[wid][29] = v1;
-            sh[wid][30] = v2;
+            sh[wid][27] = v;
+            sh[wid][kNumAcc] = n;
         }
+    } else {
+        // butterfly reduce-scatter of the (up to) 32 values: at the stage of offset
+        // o a lane keeps the half of its values whose index bit matches its lane bit
+        // and adds its partner's copy of them, so after 5 stages lane L holds the
+        // warp sum of value L -- 31 exchanges instead of 5 per value (fixed order)
+        double val[32];
+#pragma unroll
+        for (int c = 0; c < kNumAcc; ++c) val[c] = acc[c];
+        val[kNumAcc] = cnt;
+        val[29] = DUAL ? eold[27] : 0.0;
+        val[30] = DUAL ? cnt_old : 0.0;
+        val[31] = 0.0;
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool up = lane & h;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const double send = up ? val[i] : val[i + h];
+                const double keep = up ? val[i + h] : val[i];
+                val[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        if (lane < NV) sh[wid][lane] = val[0];
     }
     __syncthreads();
     // block tree: thread c sums component c over the 8 warps in order
