@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -61,3 +62,21 @@ def test_product_path_does_not_touch_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "oracle/" not in txt and "liboracle" not in txt, f
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the CUDA library the package refuses to import."""
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "try:\n    import paper_2308_07173_b200\nexcept ImportError as e:\n    print('IMPORT-ERROR', e)\n"
+            "else:\n    print('IMPORTED')\n") % ROOT
+    env = dict(os.environ, GICP_LIB_VARIANT=str(tmp_path / "missing.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env).stdout
+    assert "IMPORT-ERROR" in out and "IMPORTED" not in out
+
+
+def test_tensors_must_be_on_the_gpu(lib):
+    import numpy as np
+    import torch
+    import paper_2308_07173_b200 as g
+    with pytest.raises(ValueError):  # CPU tensors are rejected before any call (no host fallback)
+        g.build_index(torch.from_numpy(np.zeros((10, 3), np.float32)), 0.5)
