@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -460,20 +461,32 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     // trial cost with the previous correspondences (values 29, 30)
     ls.flag = mo->dflag;
     KernelTiming& kt = kernel_timing();
+    const bool host_trace = getenv("GICP_DEBUG_ALIGN_HOST") != nullptr;  // diagnostics: host-side phases
+    auto last_done = std::chrono::steady_clock::now();
     auto go = [&](const double* T, const double* piv, int flags, int32_t* corr, const int32_t* old) -> int {
         ls.seq = ++mo->seq;
         // per-launch device time of the linearisations (bench.py's roofline): event
         // pairs on the stream, read once the alignment has finished
         const bool timed = kt.on && kt.used < KernelTiming::kCap;
         if (timed) cudaEventRecord(kt.e[2 * kt.used], s);
+        const auto h0 = std::chrono::steady_clock::now();
         int rc = launch_linearize(src_p, cov_p, ns, tgt, tgt_cov, T, piv, prm->max_corr_dist, flags, mo->d,
                                   corr, s, &ls, old);
+        const auto h1 = std::chrono::steady_clock::now();
         if (timed) {
             cudaEventRecord(kt.e[2 * kt.used + 1], s);
             kt.kind[kt.used++] = (old != nullptr) ? 0 : ((flags & GICP_LIN_ERROR_ONLY) ? 2 : 1);
             kt.points = ns;
         }
-        return rc ? rc : wait_mapped(mo, ls.seq, s);
+        if (!rc) rc = wait_mapped(mo, ls.seq, s);
+        if (host_trace) {
+            const auto h2 = std::chrono::steady_clock::now();
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            fprintf(stderr, "[gicp align host] gap %.1f launch %.1f wait %.1f us\n", us(last_done, h0), us(h0, h1),
+                    us(h1, h2));
+            last_done = h2;
+        }
+        return rc;
     };
     auto lin = [&](const double* T, const double* piv, int32_t* corr, const int32_t* old) -> int {
         return go(T, piv, kLinCorrSpos, corr, old);
