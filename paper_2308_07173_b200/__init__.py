@@ -285,9 +285,9 @@ def align(src: torch.Tensor, src_cov: torch.Tensor, tgt: Index, tgt_cov: torch.T
     return T, AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers))
 
 
-def _offsets(offsets, total):
+def _offsets(offsets, total, allow_empty=False):
     o = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64).reshape(-1))
-    if o.size < 2 or o[0] != 0 or o[-1] != total:
+    if o.size < (1 if allow_empty else 2) or o[0] != 0 or o[-1] != total:
         raise ValueError("offsets must be [0, ..., n_points] with B+1 entries")
     return o
 
@@ -343,7 +343,7 @@ def align_batched_ex(src: torch.Tensor, src_cov: torch.Tensor, offsets, entry_re
     entry e of registration entry_reg[e]; reduce(entry_rows [E,32] float64 numpy) ->
     registration rows [B,32] (the cross-rank combine, sharding.make_chunk_reducer)."""
     src = _pts(src, "src")
-    o = _offsets(offsets, src.shape[0])
+    o = _offsets(offsets, src.shape[0], allow_empty=True)  # a rank may hold no entry at all
     E = o.size - 1
     er = np.ascontiguousarray(np.asarray(entry_reg, dtype=np.int32).reshape(E))
     T0h = np.ascontiguousarray(np.asarray(T0s, dtype=np.float64).reshape(B, 16))

@@ -782,7 +782,8 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         return rc;
     }
     if (B < 1) return set_error(GICP_EINVAL, "gicp_align_batched: B < 1");
-    if (!entry_reg && E != B) return set_error(GICP_EINVAL, "gicp_align_batched: entry_reg needed when E != B");
+    if (!entry_reg && E != B && E != 0)
+        return set_error(GICP_EINVAL, "gicp_align_batched: entry_reg needed when E != B");
     for (int e = 0; entry_reg && e < E; ++e)
         if (entry_reg[e] < 0 || entry_reg[e] >= B) return set_error(GICP_EINVAL, "gicp_align_batched: entry_reg");
     auto reg = [&](int e) { return entry_reg ? entry_reg[e] : e; };

@@ -22,9 +22,11 @@ import torch.multiprocessing as mp  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCANS = [(0, 20000), (64, 7777), (200, 3000)]
+TINY = [(10, 200), (90, 150)]  # one chunk each: rank 1 of 2 holds no entry at all
 
 
-def _problem():
+def _problem(scans=None):
+    scans = scans or SCANS
     sys.path.insert(0, ROOT)
     import gen
     import paper_2308_07173_b200 as g
@@ -35,7 +37,7 @@ def _problem():
     _, _, cm = g.knn_cov_self(im, 20, 1e-3, with_nbr=False)
     g.attach_cov(im, cm)
     srcs, covs, T0 = [], [], []
-    for i, n in SCANS:
+    for i, n in scans:
         sc, T, Tp = gen.config_c4_scan(i, n)
         sd = D(sc)
         isc = g.build_index(sd, 0.0)
@@ -48,14 +50,14 @@ def _problem():
     return g, im, cm, torch.cat(srcs).contiguous(), torch.cat(covs).contiguous(), offs, np.array(T0)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, tiny=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sys.path.insert(0, ROOT)
     from paper_2308_07173_b200 import sharding
-    g, im, cm, src, cov, offs, T0 = _problem()
+    g, im, cm, src, cov, offs, T0 = _problem(TINY if tiny else None)
     Ts, infos = sharding.align_batched_sharded(g, src, cov, offs, im, cm, T0)
     q.put((rank, Ts, [(i.iterations, i.converged, i.error, i.inliers) for i in infos]))
     dist.destroy_process_group()
@@ -69,14 +71,14 @@ def _free_port():
     return p
 
 
-def _run(world):
+def _run(world, tiny=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, tiny)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((r, (T, inf)) for r, T, inf in (q.get(timeout=600) for _ in range(world)))
+    res = dict((r, (T, inf)) for r, T, inf in (q.get(timeout=240) for _ in range(world)))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -99,3 +101,12 @@ def test_sharded_align_world2_is_bitwise_world1():
         c = (np.trace(T1[b][:3, :3] @ Tu[b][:3, :3].T) - 1) / 2
         assert np.arccos(min(1.0, c)) <= 1e-4
         assert i1[b][3] > 0 and abs(i1[b][3] - iu[b].inliers) <= 0.001 * iu[b].inliers
+
+
+def test_sharded_align_with_an_idle_rank():
+    """Registrations smaller than one chunk: rank 1 has no entries but still takes
+    part in every round's all_reduce; the result equals world size 1 bitwise."""
+    r1 = _run(1, tiny=True)
+    r2 = _run(2, tiny=True)
+    for r in (0, 1):
+        assert np.array_equal(r2[r][0], r1[0][0]) and r2[r][1] == r1[0][1]
