@@ -14,6 +14,10 @@
 
 #include "gicp_internal.cuh"
 
+#ifndef GICP_ALIGN_CACHE
+#define GICP_ALIGN_CACHE 1  // gicp_align skips the search for certified correspondences (R27)
+#endif
+
 
 namespace gicp {
 
@@ -438,7 +442,8 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     // source and its covariances
     const int64_t nsa = ns > 0 ? ns : 1;
     const size_t lin_bytes = linearize_scratch_bytes(nsa);
-    const size_t bytes = 512 + lin_bytes + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256;
+    const size_t bytes = 512 + lin_bytes + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256 +
+                         (GICP_ALIGN_CACHE ? 2 * nsa * sizeof(float4) + 16 : 0);
     char* scratch = nullptr;
     if (cudaMallocAsync((void**)&scratch, bytes, s) != cudaSuccess) {
         cudaGetLastError();
@@ -451,6 +456,15 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     int32_t* corr_b = corr_a + nsa;
     float* src_p = (float*)(((uintptr_t)(corr_b + nsa) + 15) & ~(uintptr_t)15);
     float* cov_p = (float*)(((uintptr_t)(src_p + 3 * nsa) + 15) & ~(uintptr_t)15);  // float2 loads
+    // the correspondence certificates paired with corr_a / corr_b (reading R27)
+    float4* cache_a = nullptr;
+    float4* cache_b = nullptr;
+    // GICP_ALIGN_NOCACHE: always search (the bitwise A/B check in tests/test_gpu_parity.py)
+    if (GICP_ALIGN_CACHE && getenv("GICP_ALIGN_NOCACHE") == nullptr) {
+        cache_a = (float4*)(((uintptr_t)(cov_p + 6 * nsa) + 15) & ~(uintptr_t)15);
+        cache_b = cache_a + nsa;
+    }
+    auto cache_of = [&](const int32_t* c) -> float4* { return c == corr_a ? cache_a : (c == corr_b ? cache_b : nullptr); };
     int rc0 = check_cuda(cudaMemsetAsync(ls.done, 0, sizeof(unsigned), s), "memset");
     if (!rc0 && ns > 0) rc0 = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s);
     if (rc0) {
@@ -465,6 +479,8 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     auto last_done = std::chrono::steady_clock::now();
     auto go = [&](const double* T, const double* piv, int flags, int32_t* corr, const int32_t* old) -> int {
         ls.seq = ++mo->seq;
+        ls.cache_new = (flags & GICP_LIN_REUSE_CORR) ? nullptr : cache_of(corr);
+        ls.cache_old = old ? cache_of(old) : nullptr;
         // per-launch device time of the linearisations (bench.py's roofline): event
         // pairs on the stream, read once the alignment has finished
         const bool timed = kt.on && kt.used < KernelTiming::kCap;
@@ -570,6 +586,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                     }
                     std::memcpy(lin29, h, sizeof(lin29));
                     std::swap(corr_a, corr_b);
+                    std::swap(cache_a, cache_b);
                     const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);
                     lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
                     nu = 2.0;

@@ -245,6 +245,11 @@ struct LinScratch {
     // block stores `seq` to *flag (host-mapped memory) so the host can spin on it
     volatile unsigned* flag = nullptr;
     unsigned seq = 0;
+    // optional correspondence certificates (gicp_align, reading R27): per source
+    // point {search point, rho} of the search that produced corr_old (read) and of
+    // this launch's corr (written); nullptr: always search
+    float4* cache_new = nullptr;
+    const float4* cache_old = nullptr;
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
 constexpr int kLinDual = 1 << 9;      // internal flag: also the trial cost with corr_old (values 29, 30)

@@ -66,23 +66,37 @@ struct Levels {
 // coarser levels up to `ring_level`, then ring expansion there.
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
                                           float qy, float qz, float r2, unsigned long long& best, int& bj,
-                                          int& overflow, const int t) {
+                                          int& overflow, const int t, float& rho) {
     // the key (d2 bits << 32 | original index) is kept as two words: the common
     // case (d2 larger) is one 32-bit compare, and only the sorted position of the
     // winner is tracked (its coordinates are loaded once, by the caller)
     unsigned bh = 0xffffffffu, bo = 0xffffffffu;
     overflow = 0;
     bj = -1;
+    // certificate of the result for the next iteration (R27): the second-smallest
+    // scanned d2 and the smallest lower bound of the voxels left unscanned
+    unsigned sh2 = 0xffffffffu;
+    float lbp = __int_as_float(0x7f800000);
+    rho = -1.0f;
     auto bound = [&]() { return fminf(__uint_as_float(bh), r2); };
     auto consider_p = [&](int j, const float4 p) {
         const unsigned h = __float_as_uint(dist2(qx, qy, qz, p.x, p.y, p.z));
         const unsigned o = __float_as_uint(p.w);
         const bool better = h < bh || (h == bh && o < bo);
+        sh2 = better ? bh : (h < sh2 ? h : sh2);
         bh = better ? h : bh;
         bo = better ? o : bo;
         bj = better ? j : bj;
     };
     auto consider = [&](int j) { consider_p(j, __ldg(pts + j)); };
+    // rho = half the gap between the best distance and every other point's lower
+    // bound, minus a rounding margin: a search point that moved less than rho keeps
+    // this nearest neighbour (distances change by at most the move)
+    auto certify = [&](float m2) {
+        const float l2 = fminf(fminf(__uint_as_float(sh2), lbp * kRel), m2);
+        const float d1 = sqrtf(__uint_as_float(bh)), dl = sqrtf(l2);
+        rho = 0.5f * (dl - d1) - 1e-6f * (dl + d1) - 1e-6f;
+    };
     auto finish = [&]() { best = ((unsigned long long)bh << 32) | bo; };
     // the team's lanes split the level-0 candidates; their bests combine by a
     // butterfly min of the (d2 bits, original index) keys after every voxel
@@ -139,7 +153,10 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                     continue;
                 const float lb2 =
                     __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
-                if (lb2 * kRel > r2) continue;  // beyond the gate: cannot hold an inlier
+                if (lb2 * kRel > r2) {  // beyond the gate: cannot hold an inlier
+                    lbp = fminf(lbp, lb2);
+                    continue;
+                }
                 const unsigned long long key = cell_key(cx, cy, cz);
                 const int2 e = hash_find(g, key);
                 if (e.y <= e.x) continue;
@@ -171,7 +188,10 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                     r = rl[k];
                     lb2 = lbl[k];
                 }
-                if (lb2 * kRel > bound()) r = make_int2(0, 0);
+                if (lb2 * kRel > bound()) {
+                    r = make_int2(0, 0);
+                    lbp = fminf(lbp, lb2);
+                }
             }
             const int len = r.y - r.x;
             const int lmax = __reduce_max_sync(0xffffffffu, len);
@@ -192,8 +212,13 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         }
         if (!active) { finish(); return; }
         const float m = cube_margin(G, s, slack, 1);
-        if (m > 0.0f && bound() < m * m * kRel) { finish(); return; }
+        if (m > 0.0f && bound() < m * m * kRel) {
+            if (kTeam == 1 && bh != 0xffffffffu) certify(m * m * kRel);
+            finish();
+            return;
+        }
         if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) {
+            if (kTeam == 1 && bh != 0xffffffffu) certify(__int_as_float(0x7f800000));  // the cube holds the whole grid
             finish();
             return;
         }
@@ -332,7 +357,8 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                                                          int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
                                                          double* __restrict__ partials, unsigned* __restrict__ done,
                                                          double* __restrict__ out29, volatile unsigned* flag,
-                                                         unsigned seq, BatchView bv) {
+                                                         unsigned seq, BatchView bv, float4* __restrict__ cache_new,
+                                                         const float4* __restrict__ cache_old) {
     LPROF(const long long tk0 = clock64();)
     // batched launches: this block's registration, its block index within it and
     // its point range; every registration is partitioned exactly like a single
@@ -395,10 +421,22 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             }
         } else {
             const float sx = (float)pp[0], sy = (float)pp[1], sz = (float)pp[2];
+            // certificate check (R27): the previous correspondence stays the nearest
+            // neighbour while the search point moved less than its rho
+            bool cached = false;
+            float4 cc = make_float4(0.f, 0.f, 0.f, -1.f);
+            if (DUAL && cache_old && active) {
+                cc = __ldg(cache_old + i);
+                if (cc.w > 0.0f) {
+                    const double ex = (double)sx - cc.x, ey = (double)sy - cc.y, ez = (double)sz - cc.z;
+                    cached = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc.w;
+                }
+            }
             unsigned long long best;
             int bj, ovf;
+            float rho;
             LPROF(const long long t0 = clock64();)
-            nn_search(pts, lvs, active, sx, sy, sz, r2, best, bj, ovf, tl);
+            nn_search(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho);
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
@@ -410,12 +448,22 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                 }
             })
             if (active) {
+                if (cached) {  // the certified pair: its key at the new search point
+                    bj = SPOS ? corr_old[i] : __float_as_int(__ldg(pts_orig + corr_old[i]).w);
+                    const float4 q = __ldg(pts + bj);
+                    best = ((unsigned long long)__float_as_uint(dist2(sx, sy, sz, q.x, q.y, q.z)) << 32) |
+                           __float_as_uint(q.w);
+                    ovf = 0;
+                    rho = cc.w;
+                }
                 if (ovf) nn_bruteforce(pts, nt, sx, sy, sz, best, bj);
                 const float bd2 = __uint_as_float((unsigned)(best >> 32));
                 const bool inl = best != kEmptyKey && bd2 < r2;
                 orig = inl ? (int)(best & 0xffffffffu) : -1;
                 spos = inl ? bj : -1;
                 if (corr && tl == 0) corr[i] = SPOS ? spos : orig;
+                if (cache_new && tl == 0)
+                    cache_new[i] = cached ? cc : make_float4(sx, sy, sz, (inl && !ovf) ? rho : -1.0f);
                 if (inl) {
                     const float4 q = __ldg(pts + bj);
                     qx = q.x;
@@ -615,7 +663,7 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
     const bool dual = (flags & kLinDual) && !reuse && !eonly;
 #define GICP_LIN_ARGS                                                                                            \
     src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
-        done, out29, flag, seq, bv
+        done, out29, flag, seq, bv, scr.cache_new, scr.cache_old
 #define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_RE(S, SP)           \

@@ -400,3 +400,40 @@ def test_covariances_kd_external_queries_and_errors(orc):
         g.covariances_kd(D(xyz), D(nbr), "laplacian", sigma=0.0, q=D(q))
     with pytest.raises(g.GicpError):
         g.covariances_kd(D(xyz), D(nbr), "polynomial", degree=0, q=D(q))
+
+
+# ---------------------------------------------------------------------------
+# correspondence certificates (reading R27): gicp_align skips the NN
+# search for a point whose search point moved less than the certified radius of
+# its previous search. The search is exact, so the alignment must be BITWISE the
+# one that searches every point every time (GICP_ALIGN_NOCACHE=1).
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["c3", "c2"])
+def test_align_certificates_bitwise(monkeypatch, cfg):
+    if cfg == "c3":  # the bench's workload and launch configuration
+        sc, mp, _, T0 = gen.config_c3()
+        imap = g.build_index(D(mp), 0.5)
+        k = 20
+    else:
+        sc, mp, _, T0 = gen.config_c2(30_000)
+        imap = g.build_index(D(mp), 0.0)
+        k = 20
+    _, _, cov_map = g.knn_cov_self(imap, k, 1e-3, with_nbr=True)
+    g.attach_cov(imap, cov_map)
+    iscan = g.build_index(D(sc), 0.0)
+    _, _, cov_scan = g.knn_cov_self(iscan, k, 1e-3, with_nbr=True)
+    res = {}
+    for mode in ("cache", "nocache"):
+        if mode == "nocache":
+            monkeypatch.setenv("GICP_ALIGN_NOCACHE", "1")
+        else:
+            monkeypatch.delenv("GICP_ALIGN_NOCACHE", raising=False)
+        for lm in (True, False):
+            T, info = g.align(D(sc), cov_scan, imap, cov_map, T0, lm=lm)
+            res[(mode, lm)] = (T, info)
+    for lm in (True, False):
+        Ta, ia = res[("cache", lm)]
+        Tb, ib = res[("nocache", lm)]
+        assert np.array_equal(Ta, Tb), (lm, Ta, Tb)
+        assert ia == ib, (lm, ia, ib)
