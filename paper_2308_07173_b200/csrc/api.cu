@@ -477,8 +477,21 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     KernelTiming& kt = kernel_timing();
     const bool host_trace = getenv("GICP_DEBUG_ALIGN_HOST") != nullptr;  // diagnostics: host-side phases
     auto last_done = std::chrono::steady_clock::now();
+    // cube-stage level of the search (kLinCoarse): level 1 while the
+    // last pose step moved the source points by more than 0.8 level-0 cells (far-off
+    // poses: many nearest neighbours lie beyond level 0's cube), level 0 near the
+    // optimum. Exact either way; the choice only moves work (C3 sweep, DESIGN.md
+    // §4.3: 0.8 cell = 0.4 m was the fastest of 0.02 ... 1 m and never/always).
+    double coarse_thr = 0.8 * (double)tgt->lv[0].cell;
+    if (const char* e = getenv("GICP_LIN_COARSE_THR")) coarse_thr = atof(e);  // experiments
+    double step_disp = INFINITY;  // the first linearisation: the initial guess's error is unknown
+    auto disp_of = [](const double* d) {  // |dv| + |dw| * 20 m (a typical range of the scan points)
+        return std::sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]) +
+               20.0 * std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    };
     auto go = [&](const double* T, const double* piv, int flags, int32_t* corr, const int32_t* old) -> int {
         ls.seq = ++mo->seq;
+        if (step_disp > coarse_thr) flags |= kLinCoarse;
         ls.cache_new = (flags & GICP_LIN_REUSE_CORR) ? nullptr : cache_of(corr);
         ls.cache_old = old ? cache_of(old) : nullptr;
         // per-launch device time of the linearisations (bench.py's roofline): event
@@ -508,6 +521,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         return go(T, piv, kLinCorrSpos, corr, old);
     };
     const bool debug = getenv("GICP_DEBUG_ALIGN") != nullptr;
+    std::vector<float4> dbg_prev;
     double T[16];
     std::memcpy(T, T0, sizeof(T));
     double lambda = -1.0, nu = 2.0, err = 0.0;
@@ -540,6 +554,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
             double E[16];
             pivoted_exp(delta, piv, E);
             mul44(E, T, T);
+            step_disp = disp_of(delta);
         } else {
             if (lambda < 0) {
                 double mx = 0.0;
@@ -562,6 +577,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 double E[16], Tn[16];
                 pivoted_exp(delta, piv, E);
                 mul44(E, T, Tn);
+                step_disp = disp_of(delta);
                 // trial: e' with the current correspondences at Tn. The first trial of
                 // an iteration is usually accepted, so it also computes, speculatively,
                 // the full linearisation at Tn in the same pass; later trials (after a
@@ -609,6 +625,25 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         if (debug)
             fprintf(stderr, "[gicp align] it=%d e=%.6f n=%lld lambda=%.3e |dw|=%.3e |dv|=%.3e\n", it, err,
                     (long long)inl, lambda, mw, mv);
+        if (debug && cache_a && ns > 0) {  // certificate statistics of the current correspondences
+            std::vector<float4> cur((size_t)ns);
+            cudaMemcpyAsync(cur.data(), cache_a, ns * sizeof(float4), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            int64_t valid = 0, kept = 0;
+            std::vector<float> rh;
+            for (int64_t i = 0; i < ns; ++i) {
+                if (cur[i].w > 0.0f) {
+                    ++valid;
+                    rh.push_back(cur[i].w);
+                    if (!dbg_prev.empty() && std::memcmp(&cur[i], &dbg_prev[i], sizeof(float4)) == 0) ++kept;
+                }
+            }
+            std::sort(rh.begin(), rh.end());
+            fprintf(stderr, "[gicp align]   certificates valid=%lld carried=%lld rho p10=%.2e p50=%.2e\n",
+                    (long long)valid, (long long)kept, rh.empty() ? 0.0 : rh[rh.size() / 10],
+                    rh.empty() ? 0.0 : rh[rh.size() / 2]);
+            dbg_prev.swap(cur);
+        }
         if (mw < prm->rot_eps && mv < prm->trans_eps) {
             converged = 1;
             break;

@@ -252,6 +252,7 @@ struct LinScratch {
     const float4* cache_old = nullptr;
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
+constexpr int kLinCoarse = 1 << 10;   // internal flag: the lockstep cube stage at level 1 (far-off poses)
 constexpr int kLinDual = 1 << 9;      // internal flag: also the trial cost with corr_old (values 29, 30)
 constexpr int kLinNV = 31;            // values a DUAL launch reduces per registration
 size_t linearize_partials_bytes(int64_t nblocks);

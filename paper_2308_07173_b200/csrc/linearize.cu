@@ -53,7 +53,8 @@ struct Levels {
     Grid lv[kMaxLevels];
     int n;
     int ring_level;  // finest level with cell >= r/2: rings there reach the gate in <= 3 steps
-    const int2* adj_oc;  // level-0 voxel adjacency lists (index.cu)
+    int l0;          // the level of the lockstep cube stage (0, or 1 for far-off poses: kLinCoarse)
+    const int2* adj_oc;  // level-l0 voxel adjacency lists (index.cu)
     const int2* adj_rng;
 };
 
@@ -116,7 +117,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     };
     // (1) level 0, the 27-voxel cube, lanes in lockstep
     {
-        const Grid& g = lvs.lv[0];
+        const Grid& g = lvs.lv[lvs.l0];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
         int2 rl[27];
@@ -225,7 +226,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     }
     // (2) per lane: coarser levels' cubes up to ring_level, then rings there
     LPROF(atomicAdd(&g_lprof[1], 1ull);)
-    for (int l = 1; l <= lvs.ring_level; ++l) {
+    for (int l = lvs.l0 + 1; l <= lvs.ring_level; ++l) {
         const Grid& g = lvs.lv[l];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
@@ -643,14 +644,20 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
-    lvs.adj_oc = tgt->adj_oc;
-    lvs.adj_rng = tgt->adj_rng;
     lvs.ring_level = lvs.n - 1;
     for (int l = 0; l < lvs.n; ++l)
         if (2.0f * tgt->lv[l].cell >= max_corr_dist) {
             lvs.ring_level = l;
             break;
         }
+    // the cube stage at level 1 (kLinCoarse): its 27 cells certify the gate for
+    // far-off search points that level 0's cube cannot settle (the search is exact
+    // at either level; the choice only moves the work)
+    const bool coarse = (flags & kLinCoarse) && lvs.n > 1 && (tgt->adj_oc1 != nullptr || tgt->adj_oc == nullptr);
+    lvs.l0 = coarse ? 1 : 0;
+    lvs.adj_oc = coarse ? tgt->adj_oc1 : tgt->adj_oc;
+    lvs.adj_rng = coarse ? tgt->adj_rng1 : tgt->adj_rng;
+    if (lvs.ring_level < lvs.l0) lvs.ring_level = lvs.l0;
     unsigned* done = scr.done;
     double* partials = scr.partials;
     volatile unsigned* flag = scr.flag;
