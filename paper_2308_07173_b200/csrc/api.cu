@@ -425,6 +425,20 @@ GICP_API int gicp_linearize(const float* src, const float* src_cov, int64_t ns, 
                             (cudaStream_t)stream);
 }
 
+// cube-stage level of the search (kLinCoarse): level 1 while the
+// last pose step moved the source points by more than 0.8 level-0 cells (far-off
+// poses: many nearest neighbours lie beyond level 0's cube), level 0 near the
+// optimum. Exact either way; the choice only moves work (C3 sweep, DESIGN.md §4.3:
+// 0.8 cell = 0.4 m was the fastest of 0.02 ... 1 m and never/always).
+static double coarse_threshold(const gicp_index_s* tgt) {
+    if (const char* e = getenv("GICP_LIN_COARSE_THR")) return atof(e);  // experiments
+    return 0.8 * (double)tgt->lv[0].cell;
+}
+// |dv| + |dw| * 20 m (a typical range of the scan points): the step's point motion
+static double step_displacement(const double* d) {
+    return std::sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]) + 20.0 * std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+}
+
 GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp_index tgt, const float* tgt_cov,
                         const double T0[16], const gicp_align_params* prm, gicp_align_result* res, void* stream) {
     if (!tgt || !tgt_cov || !T0 || !prm || !res || (ns > 0 && (!src || !src_cov)))
@@ -477,18 +491,8 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     KernelTiming& kt = kernel_timing();
     const bool host_trace = getenv("GICP_DEBUG_ALIGN_HOST") != nullptr;  // diagnostics: host-side phases
     auto last_done = std::chrono::steady_clock::now();
-    // cube-stage level of the search (kLinCoarse): level 1 while the
-    // last pose step moved the source points by more than 0.8 level-0 cells (far-off
-    // poses: many nearest neighbours lie beyond level 0's cube), level 0 near the
-    // optimum. Exact either way; the choice only moves work (C3 sweep, DESIGN.md
-    // §4.3: 0.8 cell = 0.4 m was the fastest of 0.02 ... 1 m and never/always).
-    double coarse_thr = 0.8 * (double)tgt->lv[0].cell;
-    if (const char* e = getenv("GICP_LIN_COARSE_THR")) coarse_thr = atof(e);  // experiments
+    const double coarse_thr = coarse_threshold(tgt);
     double step_disp = INFINITY;  // the first linearisation: the initial guess's error is unknown
-    auto disp_of = [](const double* d) {  // |dv| + |dw| * 20 m (a typical range of the scan points)
-        return std::sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]) +
-               20.0 * std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    };
     auto go = [&](const double* T, const double* piv, int flags, int32_t* corr, const int32_t* old) -> int {
         ls.seq = ++mo->seq;
         if (step_disp > coarse_thr) flags |= kLinCoarse;
@@ -554,7 +558,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
             double E[16];
             pivoted_exp(delta, piv, E);
             mul44(E, T, T);
-            step_disp = disp_of(delta);
+            step_disp = step_displacement(delta);
         } else {
             if (lambda < 0) {
                 double mx = 0.0;
@@ -577,7 +581,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
                 double E[16], Tn[16];
                 pivoted_exp(delta, piv, E);
                 mul44(E, T, Tn);
-                step_disp = disp_of(delta);
+                step_disp = step_displacement(delta);
                 // trial: e' with the current correspondences at Tn. The first trial of
                 // an iteration is usually accepted, so it also computes, speculatively,
                 // the full linearisation at Tn in the same pass; later trials (after a
@@ -882,6 +886,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     struct St {
         double T[16], piv[3], lin29[29], Tn[16], pn[3], delta[6], Hm[36], b[6];
         double lambda = -1.0, nu = 2.0, err = 0.0, e = 0.0;
+        double disp = INFINITY;  // the last step's point motion (kLinCoarse)
         int it = 0, converged = 0, done = 0, cur = 0, rc = GICP_OK, inner_ok = 0, accepted = 0, relin = 0;
         int64_t inl = 0;
     };
@@ -900,6 +905,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     // DUAL reads the current buffer as corr_old and writes the other one. Every
     // rank calls `reduce` on every round (collectives stay matched) even when it
     // launches nothing.
+    const double coarse_thr = coarse_threshold(tgt);
     auto round = [&](auto who, auto pose, int flags) -> int {
         int n_active = 0;
         for (int e = 0; e < E; ++e) {
@@ -911,6 +917,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             pst[e] = make_pose(Tp, pp);
             pst[e].active = a;
             pst[e].cur = st[b].cur;
+            pst[e].coarse = st[b].disp > coarse_thr;  // per registration
             n_active += a;
         }
         int r = GICP_OK;
@@ -989,6 +996,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
                 }
                 double E[16];
                 pivoted_exp(q.delta, q.piv, E);
+                q.disp = step_displacement(q.delta);
                 mul44(E, q.T, q.T);
             } else if (q.lambda < 0) {
                 double mx = 0.0;
@@ -1018,6 +1026,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
                     }
                     double E[16];
                     pivoted_exp(q.delta, q.piv, E);
+                    q.disp = step_displacement(q.delta);
                     mul44(E, q.T, q.Tn);
                     q.pn[0] = q.Tn[3];
                     q.pn[1] = q.Tn[7];

@@ -225,6 +225,7 @@ struct Pose {
     float Rf[9];
     int active;   // batched: the registration takes part in this launch
     int cur;      // batched: which correspondence buffer is current (0: corr, 1: corr_old)
+    int coarse;   // the search's lockstep cube stage on level 1 (kLinCoarse; far-off poses)
 };
 
 // batched launches (gicp_linearize_batched / gicp_align_batched): per block
@@ -252,7 +253,7 @@ struct LinScratch {
     const float4* cache_old = nullptr;
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
-constexpr int kLinCoarse = 1 << 10;   // internal flag: the lockstep cube stage at level 1 (far-off poses)
+constexpr int kLinCoarse = 1 << 10;   // internal flag: single launches set Pose::coarse
 constexpr int kLinDual = 1 << 9;      // internal flag: also the trial cost with corr_old (values 29, 30)
 constexpr int kLinNV = 31;            // values a DUAL launch reduces per registration
 size_t linearize_partials_bytes(int64_t nblocks);

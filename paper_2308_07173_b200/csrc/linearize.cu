@@ -53,9 +53,9 @@ struct Levels {
     Grid lv[kMaxLevels];
     int n;
     int ring_level;  // finest level with cell >= r/2: rings there reach the gate in <= 3 steps
-    int l0;          // the level of the lockstep cube stage (0, or 1 for far-off poses: kLinCoarse)
-    const int2* adj_oc;  // level-l0 voxel adjacency lists (index.cu)
-    const int2* adj_rng;
+    int coarse_ok;   // level 1 may host the lockstep cube stage (Pose::coarse)
+    const int2* adj_oc[2];  // level-0 and level-1 voxel adjacency lists (index.cu)
+    const int2* adj_rng[2];
 };
 
 // Exact gated 1-NN: best = smallest (d2 bits << 32 | original index) over all
@@ -65,9 +65,10 @@ struct Levels {
 // in lockstep (no divergent per-voxel loops); the few points the stop rule (no
 // unsearched point below min(best, r2)) does not settle continue per lane:
 // coarser levels up to `ring_level`, then ring expansion there.
+template <bool CERT>
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
                                           float qy, float qz, float r2, unsigned long long& best, int& bj,
-                                          int& overflow, const int t, float& rho) {
+                                          int& overflow, const int t, float& rho, const int l0) {
     // the key (d2 bits << 32 | original index) is kept as two words: the common
     // case (d2 larger) is one 32-bit compare, and only the sorted position of the
     // winner is tracked (its coordinates are loaded once, by the caller)
@@ -84,7 +85,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         const unsigned h = __float_as_uint(dist2(qx, qy, qz, p.x, p.y, p.z));
         const unsigned o = __float_as_uint(p.w);
         const bool better = h < bh || (h == bh && o < bo);
-        sh2 = better ? bh : (h < sh2 ? h : sh2);
+        if (CERT) sh2 = better ? bh : (h < sh2 ? h : sh2);
         bh = better ? h : bh;
         bo = better ? o : bo;
         bj = better ? j : bj;
@@ -117,7 +118,9 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     };
     // (1) level 0, the 27-voxel cube, lanes in lockstep
     {
-        const Grid& g = lvs.lv[lvs.l0];
+        const Grid& g = lvs.lv[l0];
+        const int2* __restrict__ adj_oc = lvs.adj_oc[l0];
+        const int2* __restrict__ adj_rng = lvs.adj_rng[l0];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
         int2 rl[27];
@@ -125,11 +128,11 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         int nr = 0;
         int a0 = 0, a1 = 0;
         bool use_adj = false;
-        if (active && lvs.adj_oc != nullptr) {
+        if (active && adj_oc != nullptr) {
             const int2 own = cell_lookup(g, G.cx, G.cy, G.cz);
             if (own.y > own.x) {
                 use_adj = true;
-                const int2 oc = __ldg(lvs.adj_oc + own.x);
+                const int2 oc = __ldg(adj_oc + own.x);
                 a0 = oc.x;
                 a1 = oc.x + oc.y;
             }
@@ -155,7 +158,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 const float lb2 =
                     __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
                 if (lb2 * kRel > r2) {  // beyond the gate: cannot hold an inlier
-                    lbp = fminf(lbp, lb2);
+                    if (CERT) lbp = fminf(lbp, lb2);
                     continue;
                 }
                 const unsigned long long key = cell_key(cx, cy, cz);
@@ -175,14 +178,14 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         // the next entry is loaded one entry ahead; candidates go kUnroll at a time
         // (independent loads in flight together: the search is latency-bound)
         int2 ne = make_int2(0, 0);
-        if (use_adj && cnt > 0) ne = __ldg(lvs.adj_rng + a0);
+        if (use_adj && cnt > 0) ne = __ldg(adj_rng + a0);
         for (int k = 0; k < kmax; ++k) {
             int2 r = make_int2(0, 0);
             if (k < cnt) {
                 float lb2;
                 if (use_adj) {
                     const int2 e = ne;
-                    if (k + 1 < cnt) ne = __ldg(lvs.adj_rng + a0 + k + 1);
+                    if (k + 1 < cnt) ne = __ldg(adj_rng + a0 + k + 1);
                     r = adj_range(e);
                     lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
                 } else {
@@ -191,7 +194,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 }
                 if (lb2 * kRel > bound()) {
                     r = make_int2(0, 0);
-                    lbp = fminf(lbp, lb2);
+                    if (CERT) lbp = fminf(lbp, lb2);
                 }
             }
             const int len = r.y - r.x;
@@ -214,19 +217,20 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         if (!active) { finish(); return; }
         const float m = cube_margin(G, s, slack, 1);
         if (m > 0.0f && bound() < m * m * kRel) {
-            if (kTeam == 1 && bh != 0xffffffffu) certify(m * m * kRel);
+            if (CERT && kTeam == 1 && bh != 0xffffffffu) certify(m * m * kRel);
             finish();
             return;
         }
         if (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2) {
-            if (kTeam == 1 && bh != 0xffffffffu) certify(__int_as_float(0x7f800000));  // the cube holds the whole grid
+            if (CERT && kTeam == 1 && bh != 0xffffffffu) certify(__int_as_float(0x7f800000));  // the cube holds the whole grid
             finish();
             return;
         }
     }
     // (2) per lane: coarser levels' cubes up to ring_level, then rings there
     LPROF(atomicAdd(&g_lprof[1], 1ull);)
-    for (int l = lvs.l0 + 1; l <= lvs.ring_level; ++l) {
+    const int ring_level = max(lvs.ring_level, l0);
+    for (int l = l0 + 1; l <= ring_level; ++l) {
         const Grid& g = lvs.lv[l];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
@@ -246,7 +250,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         }
     }
     {
-        const Grid& g = lvs.lv[lvs.ring_level];
+        const Grid& g = lvs.lv[ring_level];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
         const int R0 = max(max(max(-G.cx, G.cx - (g.nx - 1)), max(-G.cy, G.cy - (g.ny - 1))),
@@ -349,7 +353,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 // sorted positions (internal to gicp_align) instead of original indices; DUAL
 // (gicp_align's speculative step): in the same pass also the cost e' with the
 // PREVIOUS correspondences corr_old at this T (LM's trial evaluation), values 29-30.
-template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS, bool DUAL>
+// CERT: correspondence certificates (gicp_align, R27): read cache_old (DUAL) and
+// write cache_new; the other callers compile the tracking out
+template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS, bool DUAL, bool CERT>
 __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
                                                          const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             // neighbour while the search point moved less than its rho
             bool cached = false;
             float4 cc = make_float4(0.f, 0.f, 0.f, -1.f);
-            if (DUAL && cache_old && active) {
+            if (DUAL && CERT && cache_old && active) {
                 cc = __ldg(cache_old + i);
                 if (cc.w > 0.0f) {
                     const double ex = (double)sx - cc.x, ey = (double)sy - cc.y, ez = (double)sz - cc.z;
@@ -437,7 +443,8 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             int bj, ovf;
             float rho;
             LPROF(const long long t0 = clock64();)
-            nn_search(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho);
+            nn_search<CERT>(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho,
+                      (sP.coarse && lvs.coarse_ok) ? 1 : 0);
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                 orig = inl ? (int)(best & 0xffffffffu) : -1;
                 spos = inl ? bj : -1;
                 if (corr && tl == 0) corr[i] = SPOS ? spos : orig;
-                if (cache_new && tl == 0)
+                if (CERT && cache_new && tl == 0)
                     cache_new[i] = cached ? cc : make_float4(sx, sy, sz, (inl && !ovf) ? rho : -1.0f);
                 if (inl) {
                     const float4 q = __ldg(pts + bj);
@@ -653,11 +660,12 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
     // the cube stage at level 1 (kLinCoarse): its 27 cells certify the gate for
     // far-off search points that level 0's cube cannot settle (the search is exact
     // at either level; the choice only moves the work)
-    const bool coarse = (flags & kLinCoarse) && lvs.n > 1 && (tgt->adj_oc1 != nullptr || tgt->adj_oc == nullptr);
-    lvs.l0 = coarse ? 1 : 0;
-    lvs.adj_oc = coarse ? tgt->adj_oc1 : tgt->adj_oc;
-    lvs.adj_rng = coarse ? tgt->adj_rng1 : tgt->adj_rng;
-    if (lvs.ring_level < lvs.l0) lvs.ring_level = lvs.l0;
+    // (per registration: Pose::coarse, set from kLinCoarse for a single launch)
+    lvs.coarse_ok = lvs.n > 1 && (tgt->adj_oc1 != nullptr || tgt->adj_oc == nullptr);
+    lvs.adj_oc[0] = tgt->adj_oc;
+    lvs.adj_rng[0] = tgt->adj_rng;
+    lvs.adj_oc[1] = tgt->adj_oc1;
+    lvs.adj_rng[1] = tgt->adj_rng1;
     unsigned* done = scr.done;
     double* partials = scr.partials;
     volatile unsigned* flag = scr.flag;
@@ -671,8 +679,10 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
 #define GICP_LIN_ARGS                                                                                            \
     src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
         done, out29, flag, seq, bv, scr.cache_new, scr.cache_old
-#define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
-#define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
+#define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
+#define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
+    // certificates (gicp_align: sorted source, sorted-position correspondences)
+    const bool cert = (scr.cache_new || scr.cache_old) && spos && !reuse && !eonly;
 #define GICP_LIN_RE(S, SP)           \
     if (reuse && eonly)              \
         GICP_LIN_GO(true, true, S, SP);   \
@@ -682,7 +692,11 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
         GICP_LIN_GO(false, true, S, SP);  \
     else                             \
         GICP_LIN_GO(false, false, S, SP);
-    if (dual) {
+    if (cert && dual) {
+        k_linearize<false, false, true, true, true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+    } else if (cert) {
+        k_linearize<false, false, true, true, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+    } else if (dual) {
         if (spos)
             GICP_LIN_DUAL(true, true);
         else if (sorted)
@@ -711,7 +725,8 @@ int launch_linearize(const float* src, const float* src_cov, int64_t ns, const g
         k_zero29<<<1, 32, 0, s>>>(out29);
         return check_cuda(cudaGetLastError(), "linearize launch");
     }
-    const Pose P = make_pose(T, pivot);
+    Pose P = make_pose(T, pivot);
+    P.coarse = (flags & kLinCoarse) ? 1 : 0;
     const int64_t nb = (ns + kPPB - 1) / kPPB;
     void* scratch = nullptr;
     LinScratch scr;
