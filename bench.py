@@ -305,10 +305,10 @@ def main():
         cov_map_h = torch.empty((mp.shape[0], 6), dtype=torch.float32).pin_memory()
         cov_scan_h = torch.empty((sc.shape[0], 6), dtype=torch.float32).pin_memory()
         e2e_ms = []
-        # transfers overlap the compute on a copy stream: the scan upload with the
-        # map's index build, the map covariances' download with the scan's work and
-        # the alignment. Both are non-default streams (the legacy default stream
-        # would serialise them).
+        # transfers overlap the compute on a copy stream: the scan goes up first and
+        # its index + kNN/covariances run while the map uploads; the map covariances'
+        # download overlaps the alignment. Both are non-default streams (the legacy
+        # default stream would serialise them).
         cp = torch.cuda.Stream(device=dev)
         es = torch.cuda.Stream(device=dev)
         for it in range(args.steps + 1):
@@ -318,20 +318,21 @@ def main():
                 a, b = ev(), ev()
                 a.record(es)
                 cp.wait_stream(es)
-                md = map_h.to(dev, non_blocking=True)
+                sd = scan_h.to(dev, non_blocking=True)
                 with torch.cuda.stream(cp):
-                    sd = scan_h.to(dev, non_blocking=True)
+                    md = map_h.to(dev, non_blocking=True)
                     up = torch.cuda.Event()
                     up.record(cp)
+                iscan = g.build_index(sd, 0.0)
+                _, _, cs = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
+                es.wait_event(up)  # the map's upload
+                md.record_stream(es)
                 imap = g.build_index(md, MAP_CELL)
                 _, _, cm = g.knn_cov_self(imap, K, EPS, with_nbr=True)
                 g.attach_cov(imap, cm)
                 cp.wait_stream(es)
                 with torch.cuda.stream(cp):
                     cov_map_h.copy_(cm, non_blocking=True)
-                es.wait_event(up)  # the scan's upload only (the download keeps running)
-                iscan = g.build_index(sd, 0.0)
-                _, _, cs = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
                 T, info = g.align(sd, cs, imap, cm, T0)
                 cov_scan_h.copy_(cs, non_blocking=True)
                 es.wait_stream(cp)
