@@ -855,12 +855,21 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     // device: batch scratch + two correspondence buffers + the sorted source copy
     BatchScratch bs;
     char* ex = nullptr;
-    if ((rc = batch_scratch(offsets, E, 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64, s, bs, &ex)))
+    // + the correspondence certificates paired with the two buffers (R27)
+    const bool certs = GICP_ALIGN_CACHE && getenv("GICP_ALIGN_NOCACHE") == nullptr;
+    if ((rc = batch_scratch(offsets, E,
+                            2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
+                                (certs ? 2 * nsa * sizeof(float4) + 16 : 0),
+                            s, bs, &ex)))
         return rc;
     int32_t* corrA = (int32_t*)ex;
     int32_t* corrB = corrA + nsa;
     float* src_p = (float*)(((uintptr_t)(corrB + nsa) + 15) & ~(uintptr_t)15);
     float* cov_p = (float*)(((uintptr_t)(src_p + 3 * nsa) + 15) & ~(uintptr_t)15);  // float2 loads
+    if (certs) {  // cache_new pairs with corrA, cache_old with corrB; the kernel maps them per `cur`
+        bs.ls.cache_new = (float4*)(((uintptr_t)(cov_p + 6 * nsa) + 15) & ~(uintptr_t)15);
+        bs.ls.cache_old = bs.ls.cache_new + nsa;
+    }
     if (ns > 0 && (rc = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s, bs.offs, E))) {
         cudaFreeAsync(bs.base, s);
         return rc;

@@ -392,6 +392,12 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         int32_t* oth = sP.cur ? corr : const_cast<int32_t*>(corr_old);
         corr = REUSE ? cur : oth;
         corr_old = cur;
+        if (CERT) {  // the certificates follow their correspondence buffers
+            float4* ccur = sP.cur ? const_cast<float4*>(cache_old) : cache_new;
+            float4* coth = sP.cur ? cache_new : const_cast<float4*>(cache_old);
+            cache_new = coth;
+            cache_old = ccur;
+        }
     }
     double acc[kNumAcc];
 #pragma unroll

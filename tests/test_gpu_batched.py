@@ -130,3 +130,15 @@ def test_batched_argument_errors(problem):
     bad[1], bad[2] = bad[2], bad[1]
     with pytest.raises(g.GicpError):
         g.linearize_batched(p["src"], p["cov"], bad, p["im"], p["cm"], p["T0"])
+
+
+def test_align_batched_certificates_bitwise(problem, monkeypatch):
+    """Correspondence certificates (R27) in the batched align: every
+    registration bitwise the same with and without them (GICP_ALIGN_NOCACHE=1)."""
+    p = problem
+    Ta, ia = g.align_batched(p["src"], p["cov"], p["offs"], p["im"], p["cm"], p["T0"], allow_degenerate=True)
+    monkeypatch.setenv("GICP_ALIGN_NOCACHE", "1")
+    Tb, ib = g.align_batched(p["src"], p["cov"], p["offs"], p["im"], p["cm"], p["T0"], allow_degenerate=True)
+    assert np.array_equal(np.asarray(Ta), np.asarray(Tb))
+    assert [(i.iterations, i.converged, i.error, i.inliers) for i in ia] == \
+        [(i.iterations, i.converged, i.error, i.inliers) for i in ib]
