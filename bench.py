@@ -199,6 +199,12 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    # the scan's path (index + kNN/covariances, latency-bound small grids) runs on a
+    # high-priority side stream inside the map's kNN (throughput-bound, 15.6k blocks):
+    # its blocks take SM slots as the map's retire, so it costs its share of the
+    # machine, not its latency. The alignment joins both.
+    sb = torch.cuda.Stream(device=dev, priority=-1)
+
     def step(record=None):
         e = [ev() for _ in range(6)]
         e[0].record(stream)
@@ -207,9 +213,13 @@ def main():
         _, _, cov_map = g.knn_cov_self(imap, K, EPS, with_nbr=True)
         g.attach_cov(imap, cov_map)
         e[2].record(stream)
-        iscan = g.build_index(scan_d, 0.0)
-        _, _, cov_scan = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
-        e[3].record(stream)
+        sb.wait_event(e[1])
+        with torch.cuda.stream(sb):
+            iscan = g.build_index(scan_d, 0.0)
+            _, _, cov_scan = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
+            e[3].record(sb)
+        stream.wait_stream(sb)
+        cov_scan.record_stream(stream)
         T, info = g.align(scan_d, cov_scan, imap, cov_map, T0)
         e[4].record(stream)
         if record is not None:
@@ -254,8 +264,11 @@ def main():
         ms = float(t.item())
     build_ms = statistics.mean(r[0][0].elapsed_time(r[0][1]) for r in rec)
     knncov_ms = statistics.mean(r[0][1].elapsed_time(r[0][2]) for r in rec)
-    scan_ms = statistics.mean(r[0][2].elapsed_time(r[0][3]) for r in rec)
-    align_ms = statistics.mean(r[0][3].elapsed_time(r[0][4]) for r in rec)
+    # the scan path overlaps the map's kNN: scan_ms from the map index's end to its own
+    # end; align from the later of the two ends
+    scan_ms = statistics.mean(r[0][1].elapsed_time(r[0][3]) for r in rec)
+    align_ms = statistics.mean(r[0][0].elapsed_time(r[0][4]) - max(r[0][0].elapsed_time(r[0][2]),
+                                                                    r[0][0].elapsed_time(r[0][3])) for r in rec)
     iters = statistics.mean(r[1].iterations for r in rec)
     T_last = rec[-1][2]
     dt_err = float(np.linalg.norm(T_last[:3, 3] - T_true[:3, 3]))
