@@ -76,6 +76,8 @@ def lib():
                                          ctypes.POINTER(AlignResult)]
         L.oracle_align.argtypes = [P, P, i64, P, P, i64, P, ctypes.POINTER(AlignParams),
                                    ctypes.POINTER(AlignResult), i32]
+        L.oracle_align_ex.argtypes = [P, P, i64, P, P, i64, P, ctypes.POINTER(AlignParams),
+                                      ctypes.POINTER(AlignResult), i32, P, i32, ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
 
@@ -282,20 +284,31 @@ def ldlt_solve6(A, y):
     return x
 
 
+TRACE_W = 40
+
+
 def align(src, src_cov, tgt, tgt_cov, T0, max_iter=64, lm=True, rot_eps=1e-6, trans_eps=1e-5,
-          max_corr_dist=1.0, nthreads=0):
-    """O4: returns dict(T, iterations, converged, error, inliers)."""
+          max_corr_dist=1.0, nthreads=0, trace=False):
+    """O4: returns dict(T, iterations, converged, error, inliers) and, with trace=True,
+    'trace': one row per LM trial [it, lambda, e, e', rho, accepted, delta(6), b(6), H(21), 0]."""
     src, tgt = _f32(src), _f32(tgt)
     src_cov, tgt_cov = _f32(src_cov), _f32(tgt_cov)
     T0 = np.ascontiguousarray(T0, dtype=np.float64)
     p = AlignParams(max_iter, int(lm), rot_eps, trans_eps, max_corr_dist)
     r = AlignResult()
-    rc = lib().oracle_align(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
-                            _ptr(T0), ctypes.byref(p), ctypes.byref(r), nthreads)
+    cap = 10 * max_iter if trace else 0
+    tr = np.zeros((max(cap, 1), TRACE_W))
+    ntr = ctypes.c_int(0)
+    rc = lib().oracle_align_ex(_ptr(src), _ptr(src_cov), src.shape[0], _ptr(tgt), _ptr(tgt_cov), tgt.shape[0],
+                               _ptr(T0), ctypes.byref(p), ctypes.byref(r), nthreads,
+                               _ptr(tr) if trace else None, cap, ctypes.byref(ntr))
     if rc != OK:
         raise OracleError(rc, "oracle_align")
-    return dict(T=np.array(r.T[:]).reshape(4, 4), iterations=r.iterations, converged=bool(r.converged),
-                error=r.error, inliers=r.inliers)
+    out = dict(T=np.array(r.T[:]).reshape(4, 4), iterations=r.iterations, converged=bool(r.converged),
+               error=r.error, inliers=r.inliers)
+    if trace:
+        out["trace"] = tr[:ntr.value].copy()
+    return out
 
 
 def pack_cov(cov6):

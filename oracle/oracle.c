@@ -771,10 +771,33 @@ static void unpack_H(const double* o29, double H[36], double b[6]) {
     for (int a = 0; a < 6; ++a) b[a] = o29[21 + a];
 }
 
-/* O4: LM (lm=1) or Gauss-Newton (lm=0: lambda = 0, every step accepted). */
-int oracle_align(const float* src, const float* src_cov, int64_t ns, const float* tgt, const float* tgt_cov,
-                 int64_t nt, const double T0[16], const oracle_align_params* prm, oracle_align_result* res,
-                 int nthreads) {
+/* One record per LM trial (test instrumentation: recorded, never read back here).
+ * [0] outer iteration, [1] lambda of the trial, [2] e at T, [3] e' at the trial pose,
+ * [4] rho, [5] accepted, [6..11] delta, [12..17] b, [18..38] H (upper 21). */
+#define ORACLE_TRACE_W 40
+static void trace_put(double* tr, int cap, int* nt, int it, double lambda, double e, double en, double rho,
+                      int acc, const double delta[6], const double* o29) {
+    if (!tr || *nt >= cap) return;
+    double* r = tr + (int64_t)ORACLE_TRACE_W * (*nt);
+    r[0] = it;
+    r[1] = lambda;
+    r[2] = e;
+    r[3] = en;
+    r[4] = rho;
+    r[5] = acc;
+    for (int a = 0; a < 6; ++a) r[6 + a] = delta[a];
+    for (int a = 0; a < 6; ++a) r[12 + a] = o29[21 + a];
+    for (int a = 0; a < 21; ++a) r[18 + a] = o29[a];
+    r[39] = 0.0;
+    ++*nt;
+}
+
+/* O4: LM (lm=1) or Gauss-Newton (lm=0: lambda = 0, every step accepted).
+ * oracle_align_ex additionally records every LM trial into trace[cap][40] (may be NULL). */
+int oracle_align_ex(const float* src, const float* src_cov, int64_t ns, const float* tgt, const float* tgt_cov,
+                    int64_t nt, const double T0[16], const oracle_align_params* prm, oracle_align_result* res,
+                    int nthreads, double* trace, int trace_cap, int* n_trace) {
+    int ntr = 0;
     if (!prm || !res || !T0) return ORACLE_EINVAL;
     double T[16];
     memcpy(T, T0, sizeof(T));
@@ -841,6 +864,7 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
                 double den = 0.0;
                 for (int a = 0; a < 6; ++a) den += delta[a] * (lambda * delta[a] - b[a]);
                 double rho = (e - en) / den;
+                trace_put(trace, trace_cap, &ntr, it, lambda, e, en, rho, rho > 0, delta, o29);
                 if (rho > 0) {
                     memcpy(T, Tn, sizeof(T));
                     double f = 1.0 - pow(2.0 * rho - 1.0, 3);
@@ -873,7 +897,14 @@ int oracle_align(const float* src, const float* src_cov, int64_t ns, const float
     res->converged = converged;
     res->error = err;
     res->inliers = inl;
+    if (n_trace) *n_trace = ntr;
     return rc;
+}
+
+int oracle_align(const float* src, const float* src_cov, int64_t ns, const float* tgt, const float* tgt_cov,
+                 int64_t nt, const double T0[16], const oracle_align_params* prm, oracle_align_result* res,
+                 int nthreads) {
+    return oracle_align_ex(src, src_cov, ns, tgt, tgt_cov, nt, T0, prm, res, nthreads, NULL, 0, NULL);
 }
 
 /* -------------------------------------------------------------------------- */
