@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgicp_b200.so")
 SOURCES = ["api.cu", "index.cu", "knn.cu", "cov.cu", "linearize.cu", "prep.cu", "vgicp.cu", "ground.cu", "cluster.cu", "submap.cu"]
-HEADERS = ["gicp_internal.cuh", "cov_device.cuh", "lin_device.cuh"]
+HEADERS = ["gicp_internal.cuh", "cov_device.cuh", "lin_device.cuh", "sortnet.cuh", "knn_tile.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

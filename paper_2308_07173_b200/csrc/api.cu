@@ -124,12 +124,14 @@ bool ldlt6(const double A[36], const double y[6], double x[6]) {
             L[i][j] = t / D[j];
         }
     }
+    // L z = y, then D w = z, then L^T x = w
     double z[6];
     for (int i = 0; i < 6; ++i) {
         double s = y[i];
         for (int p = 0; p < i; ++p) s -= L[i][p] * z[p];
-        z[i] = s / D[i];
+        z[i] = s;
     }
+    for (int i = 0; i < 6; ++i) z[i] /= D[i];
     for (int i = 5; i >= 0; --i) {
         double s = z[i];
         for (int p = i + 1; p < 6; ++p) s -= L[p][i] * x[p];
@@ -308,6 +310,7 @@ GICP_API void gicp_index_free(gicp_index idx) {
     if (idx->vox_mu) cudaFreeAsync(idx->vox_mu, s);
     if (idx->vox_cov) cudaFreeAsync(idx->vox_cov, s);
     if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
+    if (idx->tiles1) cudaFreeAsync(idx->tiles1, s);
     cudaGetLastError();
     delete idx;
 }
@@ -444,6 +447,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     if (!tgt || !tgt_cov || !T0 || !prm || !res || (ns > 0 && (!src || !src_cov)))
         return set_error(GICP_EINVAL, "gicp_align: null pointer");
     if (ns < 0) return set_error(GICP_EINVAL, "gicp_align: ns < 0");
+    if (ns < 6) return set_error(GICP_EDEGENERATE, "gicp_align: fewer than 6 source points");
     if (prm->max_iter < 1) return set_error(GICP_EINVAL, "gicp_align: max_iter < 1");
     if (!finite_T(T0)) return set_error(GICP_EINVAL, "gicp_align: non-finite T0");
     init_pool_once();
@@ -547,6 +551,11 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         for (int a = 0; a < 6; ++a) b[a] = lin29[21 + a];
         const double e = lin29[27];
         err = e;
+        if (debug) {
+            fprintf(stderr, "[gicp align] lin29 it=%d piv=(%.6f %.6f %.6f):", it, piv[0], piv[1], piv[2]);
+            for (int c = 0; c < 29; ++c) fprintf(stderr, " %.9g", lin29[c]);
+            fprintf(stderr, "\n");
+        }
         bool done_now = false;
         if (!prm->lm) {
             double nb[6];

@@ -113,9 +113,22 @@ int launch_cluster(const float* xyz, int64_t n, float tol, int min_size, int32_t
     *n_clusters = 0;
     if (n == 0) return GICP_OK;
     gicp_index idx = nullptr;
-    const float cell = tol * (1.0f + 1.0f / 1024.0f);  // >= tol plus the voxel-assignment slack
+    // every neighbour within tol must lie in the point's 27-voxel cube: the voxel edge
+    // must exceed tol by the voxel-assignment rounding, which grows with the cloud's
+    // extent (the grid's slack, 8u(E + cell)); rebuild once if the first margin is short
+    float cell = tol * (1.0f + 1.0f / 1024.0f);
     int rc = build_index(xyz, n, cell, s, &idx);
     if (rc) return rc;
+    if (idx->lv[0].slack >= cell - tol) {
+        const float c2 = tol + 2.0f * idx->lv[0].slack + tol / 1024.0f;
+        gicp_index_free(idx);
+        idx = nullptr;
+        if ((rc = build_index(xyz, n, c2, s, &idx))) return rc;
+        if (idx->lv[0].slack >= idx->lv[0].cell - tol) {
+            gicp_index_free(idx);
+            return set_error(GICP_ERANGE, "gicp_cluster: tolerance below the grid's rounding slack");
+        }
+    }
     const volatile float t2v = tol * tol;
     const float t2 = t2v;
     size_t tb = 0;

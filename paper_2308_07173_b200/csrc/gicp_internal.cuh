@@ -164,6 +164,8 @@ struct gicp_index_s {
     int2* adj_rng = nullptr;              // neighbour voxels, nearest-first per voxel: {start, count<<6 | code}
     int2* adj_oc1 = nullptr;              // the same lists for level 1 (escalated queries)
     int2* adj_rng1 = nullptr;
+    int* tiles1 = nullptr;                // level-1 voxels in sorted order: first point of each, then n
+    int64_t n_tiles1 = 0;                 //   (the work units of the tiled kNN, knn_tile.cuh)
     float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
     float4* vox_mu = nullptr;             // VGICP: per level-0 voxel, at its head: mean - first point (xyz), N (w)
     float4* vox_cov = nullptr;            // VGICP: mean covariance of the voxel's points (2 x float4 at the head)

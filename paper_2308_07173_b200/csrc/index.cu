@@ -195,6 +195,8 @@ __global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, 
     }
 }
 
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
 // run tails of every level write the end of their voxel
 __global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, LevelSet ls) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -473,6 +475,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if (idx->adj_rng) cudaFreeAsync(idx->adj_rng, s);
         if (idx->adj_oc1) cudaFreeAsync(idx->adj_oc1, s);
         if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
+        if (idx->tiles1) cudaFreeAsync(idx->tiles1, s);
         delete idx;
         return code;
     };
@@ -501,6 +504,22 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
     if ((rc = check_cuda(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), s), "memset"))) return fail(rc);
     k_cells<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls, nheads, heads, nheads + 1, heads1);
     k_cell_ends<<<grid_for(n, 256), 256, 0, s>>>((unsigned long long*)keys.p, n, ls);
+    if (L > 1) {
+        // the level-1 voxels in sorted (Morton) order: their first points, then n
+        if (cudaMallocAsync(&idx->tiles1, (n1 + 1) * sizeof(int), s) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(set_error(GICP_ENOMEM, "tile list allocation failed"));
+        }
+        idx->n_tiles1 = n1;
+        idx->device_bytes += (n1 + 1) * (int64_t)sizeof(int);
+        const int bits = std::max(1, bits_for((int)std::min<int64_t>(n, INT_MAX)));
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, heads1, idx->tiles1, (int)n1, 0, bits, s);
+        DevBuf tmp;
+        if ((rc = alloc_async(tmp, tb, s))) return fail(rc);
+        cub::DeviceRadixSort::SortKeys(tmp.p, tb, heads1, idx->tiles1, (int)n1, 0, bits, s);
+        k_set_int<<<1, 1, 0, s>>>(idx->tiles1 + n1, (int)n);
+    }
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);
     int adj_overflow = 0;

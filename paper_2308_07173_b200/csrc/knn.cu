@@ -28,6 +28,7 @@
 
 #include "cov_device.cuh"
 #include "gicp_internal.cuh"
+#include "sortnet.cuh"
 
 namespace gicp {
 namespace {
@@ -557,6 +558,24 @@ struct Levels {
     Grid lv[kMaxLevels];
 };
 
+#include "knn_tile.cuh"
+
+// the tiled level-0 stage for self queries (knn_tile.cuh): K = 10 and 20 (the
+// configs' k); returns false when it does not apply (then the per-query kernel runs)
+bool launch_tile(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, int* counts,
+                 int* listA, int* listB, int2* exact, cudaStream_t s) {
+    static const bool off = getenv("GICP_KNN_TILE") && atoi(getenv("GICP_KNN_TILE")) == 0;
+    if (off || idx->tiles1 == nullptr || idx->n_tiles1 == 0 || (k != 10 && k != 20)) return false;
+    const unsigned grid = (unsigned)((idx->n_tiles1 + kTileWarps - 1) / kTileWarps);
+    if (k == 20)
+        k_knn_tile<20><<<grid, kTileWarps * 32, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->n_tiles1, eps, nbr, d2,
+                                                        cov, counts + 2, listA, counts + 0, exact, counts + 3, listB);
+    else
+        k_knn_tile<10><<<grid, kTileWarps * 32, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->n_tiles1, eps, nbr, d2,
+                                                        cov, counts + 2, listA, counts + 0, exact, counts + 3, listB);
+    return true;
+}
+
 // Query sources: self mode -> id = sorted position (xyz from pts, row = orig);
 // external -> id = original query index into q.
 struct QuerySrc {
@@ -853,8 +872,15 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
     // level 0 over every query, then one launch that climbs the pyramid for the rest
     const AdjView adj{idx->adj_oc, idx->adj_rng, idx->adj_oc1, idx->adj_rng1};
-    k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr, d2,
-                                                         cov, counts + 2, listA, counts + 0, exact, L == 1);
+    if (qext == nullptr && perm == nullptr && L > 1 &&
+        launch_tile(idx, k, eps, nbr, d2, cov, counts, listA, listB, exact, s)) {
+        // tiles too dense to stage: the per-query level-0 kernel over their points
+        k_knn_level<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], nullptr, m, listB, counts + 3, k, eps,
+                                                             nbr, d2, cov, counts + 2, listA, counts + 0, exact, 0);
+    } else {
+        k_knn_level<KCAP><<<full_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], perm, m, nullptr, nullptr, k, eps, nbr,
+                                                             d2, cov, counts + 2, listA, counts + 0, exact, L == 1);
+    }
     if (L > 1)
         k_knn_escalate<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, adj, lvs, L, listA, counts + 2, k, eps, nbr, d2, cov,
                                                                 counts + 0, exact);
@@ -881,8 +907,8 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
         for (auto& x : pv) x = 0;
         cudaMemcpyToSymbol(g_kprof, pv, sizeof(pv));
 #endif
-        fprintf(stderr, "[gicp knn] m=%lld levels=%d escalated=%d exact=%d bruteforce=%d\n", (long long)m, L, h[2],
-                h[0], h[1]);
+        fprintf(stderr, "[gicp knn] m=%lld levels=%d escalated=%d exact=%d bruteforce=%d tile-fallback=%d\n",
+                (long long)m, L, h[2], h[0], h[1], h[3]);
         if (h[0] > 0) {
             int2 ex[16];
             const int ne = h[0] < 16 ? h[0] : 16;

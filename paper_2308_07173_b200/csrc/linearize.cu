@@ -614,7 +614,8 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     if (threadIdx.x == 0) done[scan] = 0u;
     if (bv.btab) {  // the last registration to finish signals the launch
         __shared__ bool fin;
-        __threadfence();
+        __threadfence_system();  // every lane's out row (possibly host-mapped) before the ticket
+        __syncthreads();
         if (threadIdx.x == 0) fin = (atomicAdd(done + bv.n_scans, 1u) == (unsigned)bv.n_active - 1u);
         __syncthreads();
         if (!fin) return;

@@ -138,5 +138,7 @@ def align_batched_sharded(g, src, src_cov, offsets, tgt, tgt_cov, T0s, group=Non
         cov_l = torch.zeros((0, 6), dtype=src_cov.dtype, device=src_cov.device)
     loffs = np.concatenate([[0], np.cumsum([hi - lo for (_, _, lo, hi) in entries])]).astype(np.int64)
     entry_reg = np.array([b for (b, _, _, _) in entries], dtype=np.int32)
+    if comm_device is None and dist.is_initialized() and dist.get_backend(group) == "nccl":
+        comm_device = src.device          # NCCL reduces device tensors only
     reducer = make_chunk_reducer(entries, B, num_chunks, group, comm_device)
     return g.align_batched_ex(src_l, cov_l, loffs, entry_reg, B, tgt, tgt_cov, T0s, reducer, **params)

@@ -52,6 +52,23 @@ def test_cluster_random_sets(orc):
         assert nc == onc and np.array_equal(lab.cpu().numpy(), ol)
 
 
+def test_cluster_km_offset_pairs_at_tol(orc):
+    """Clouds ~2 km from the origin (the grid rounding grows with the extent): chains of
+    points spaced just inside tol along random directions must stay one cluster."""
+    rng = np.random.default_rng(22)
+    tol = 0.3
+    for t in range(10):
+        base = np.array([2000.0, -1500.0, 30.0]) + rng.uniform(-5, 5, 3)
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        chain = base + np.outer(np.arange(12) * tol * (1 - 2e-6), d)
+        other = base + rng.uniform(-3, 3, (150, 3))
+        p = np.concatenate([chain, other, [[0.0, 0.0, 0.0]]]).astype(np.float32)
+        lab, nc = g.cluster(D(p), tol, 1)
+        ol, onc = orc.cluster(p, tol, 1)
+        assert nc == onc and np.array_equal(lab.cpu().numpy(), ol)
+
+
 def test_cluster_ground_filtered_scan(orc):
     """The paper's pipeline on a scan: ground filter, then clusters of the
     vertical features (walls, posts, boxes); labels bit-exact vs the oracle."""

@@ -287,19 +287,17 @@ def test_align_c2(orc):
         dt, dr = _pose_err(T, ref["T"])
         assert dt <= 1e-3 and dr <= 1e-4
     else:
-        # Below the eps floor (align) the optimum is a flat
-        # valley: LM accept/reject decisions hinge on cost differences at the
-        # rounding level, so the two LM paths may stop at different points of the
-        # valley. Gauss-Newton has no such decisions: its poses must agree. Each LM
-        # result must reach the GN optimum's cost to within 5e-3 relative.
+        # Below the eps floor (SURVEY.md §8(c) tolerances, align) pose parity is not
+        # asserted: both LM results must reach costs within 1e-4 relative of each other.
+        # Gauss-Newton takes no accept/reject decisions: its poses must agree too.
+        e_gpu = orc.linearize(src, cs, tgt, ct, T, 1.0)[0][27]
+        e_ref = o29[27]
+        print(f"C2 eps floor: kappa'={kp:.3g} e_gpu={e_gpu:.9g} e_ref={e_ref:.9g} rel={(e_gpu - e_ref) / e_ref:.3g}")
+        assert abs(e_gpu - e_ref) <= 1e-4 * e_ref, (kp, e_gpu, e_ref)
         Tg, ig = g.align(D(src), D(cs), idx, D(ct), T0, lm=False)
         rg = orc.align(src, cs, tgt, ct, T0, lm=False)
         dt, dr = _pose_err(Tg, rg["T"])
         assert dt <= 1e-3 and dr <= 1e-4, (kp, dt, dr)
-        e_gn = orc.linearize(src, cs, tgt, ct, rg["T"], 1.0)[0][27]
-        e_gpu = orc.linearize(src, cs, tgt, ct, T, 1.0)[0][27]
-        e_ref = o29[27]
-        assert e_gpu <= e_gn * (1 + 5e-3) and e_ref <= e_gn * (1 + 5e-3), (kp, e_gpu, e_ref, e_gn)
 
 
 def test_align_degenerate(orc):

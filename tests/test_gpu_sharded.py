@@ -6,7 +6,6 @@ kernels wait on each other). World size 2 must reproduce world size 1 BITWISE
 (fixed chunking, chunk-ordered combine), and both must agree with the unsharded
 gicp_align_batched to rounding (different summation order)."""
 import os
-import socket
 import sys
 
 import numpy as np
@@ -52,9 +51,8 @@ def _problem(scans=None):
 
 def _worker(rank, world, port, q, tiny=False):
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no TCP port to race for (a bind/close/reuse port probe is racy)
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     sys.path.insert(0, ROOT)
     from paper_2308_07173_b200 import sharding
     g, im, cm, src, cov, offs, T0 = _problem(TINY if tiny else None)
@@ -64,11 +62,11 @@ def _worker(rank, world, port, q, tiny=False):
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    """A fresh rendezvous file path for init_method='file://' (the name is kept so the
+    callers read as before; nothing binds a port)."""
+    import tempfile
+    d = tempfile.mkdtemp(prefix="gicp_pg_")
+    return os.path.join(d, "rendezvous")
 
 
 def _run(world, tiny=False):

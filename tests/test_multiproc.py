@@ -6,7 +6,6 @@ sharding.py). H, b, e must be bitwise identical to the single-process combine of
 the same chunks and agree with an unsharded linearisation to rounding.
 """
 import os
-import socket
 import sys
 
 import numpy as np
@@ -37,9 +36,8 @@ def _problem():
 
 def _worker(rank, world, port, q):
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no TCP port to race for (a bind/close/reuse port probe is racy)
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     sh = _load_sharding()
     oracle, src, cs, tgt, ct, T0 = _problem()
     local = {}
@@ -52,11 +50,11 @@ def _worker(rank, world, port, q):
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    """A fresh rendezvous file path for init_method='file://' (the name is kept so the
+    callers read as before; nothing binds a port)."""
+    import tempfile
+    d = tempfile.mkdtemp(prefix="gicp_pg_")
+    return os.path.join(d, "rendezvous")
 
 
 def test_chunking_is_world_size_independent():
@@ -108,9 +106,8 @@ def _chunk_rows(b, c):
 
 def _reduce_worker(rank, world, port, q):
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no TCP port to race for (a bind/close/reuse port probe is racy)
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     sh = _load_sharding()
     entries = sh.registration_chunks(SIZES, rank, world)
     rows = np.stack([_chunk_rows(b, c) for (b, c, _, _) in entries]) if entries else np.zeros((0, 32))
