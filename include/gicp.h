@@ -291,6 +291,39 @@ int gicp_align_batched_ex(const float* src, const float* src_cov, const int64_t*
                           const double* T0 /* host [B][16] */, const gicp_align_params* params /* host */,
                           gicp_align_result* result /* host [B] */, gicp_reduce_fn reduce, void* user, void* stream);
 
+/* gicp_align_batched_sharded -- the sharded form with the reduction on the device
+ * ("one NCCL allreduce of the 27-float H/b over NVLink per
+ * iteration"; the paper's data parallelism over points).
+ * This process holds E entries (point ranges offsets[E+1] of src); entry e is
+ * chunk c of registration b and entry_chunk[e] (host) = b * num_chunks + c, the
+ * chunking being FIXED globally (independent of the number of processes). After
+ * every evaluation round the library zeroes `table` (device, caller-owned,
+ * [B * num_chunks][32] doubles), writes each launched entry's row (H 21, b 6, e,
+ * count, trial cost, its count, pad) at its chunk row, calls
+ *     allreduce(table, B * num_chunks * 32, user, stream)
+ * which must sum `table` over all processes IN PLACE, stream-ordered on `stream`
+ * (e.g. ncclAllReduce on it; NULL: a single process), then sums each
+ * registration's chunk rows in chunk order on the device. Every row has one
+ * contributor, so the allreduce is exact and H, b, e are bitwise identical for
+ * any process count; every process then runs the identical host LM (all take the
+ * same rounds: the collectives stay matched; a process without entries passes
+ * E = 0 and still takes part). Returns as gicp_align_batched; allreduce returning
+ * non-zero -> GICP_ECUDA. Synchronous. */
+typedef int (*gicp_allreduce_fn)(double* table, int64_t count, void* user, void* stream);
+
+int gicp_align_batched_sharded(const float* src, const float* src_cov, const int64_t* offsets /* host [E+1] */,
+                               int E, const int* entry_chunk /* host [E] */, int num_chunks, int B, gicp_index tgt,
+                               const float* tgt_cov, const double* T0 /* host [B][16] */,
+                               const gicp_align_params* params /* host */, gicp_align_result* result /* host [B] */,
+                               double* table /* device [B * num_chunks][32] */, gicp_allreduce_fn allreduce,
+                               void* user, void* stream);
+
+/* gicp_combine_chunks -- out[b][c] = sum over k = 0 .. num_chunks-1 (in that order)
+ * of table[b][k][c]; table (device) [B][num_chunks][width], out (device) [B][width].
+ * The chunk-ordered sum of a sharded one-shot linearisation (after the caller's
+ * allreduce of the chunk table). Stream-ordered. */
+int gicp_combine_chunks(const double* table, int B, int num_chunks, int width, double* out, void* stream);
+
 
 /* ---------------------------------------------------------------------------
  * Voxelized GICP ("extends and optimizes the Voxelized-GICP";

@@ -92,11 +92,16 @@ REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctyp
                              ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_void_p)
 _lib.gicp_align_batched_ex.argtypes = [_P, _P, _P, _i32, _P, _i32, _P, _P, _P, ctypes.POINTER(AlignParams), _P,
                                        REDUCE_FN, _P, _P]
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
+_lib.gicp_align_batched_sharded.argtypes = [_P, _P, _P, _i32, _P, _i32, _i32, _P, _P, _P, ctypes.POINTER(AlignParams),
+                                            _P, _P, ALLREDUCE_FN, _P, _P]
+_lib.gicp_combine_chunks.argtypes = [_P, _i32, _i32, _i32, _P, _P]
 
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
-           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_covariances_kd",
+           "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_align_batched_sharded",
+           "gicp_combine_chunks", "gicp_covariances_kd",
            "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter",
            "gicp_cluster", "gicp_submap_build", "gicp_submap_query", "gicp_submap_free", "gicp_align_timing"]
 
@@ -372,6 +377,55 @@ def align_batched_ex(src: torch.Tensor, src_cov: torch.Tensor, offsets, entry_re
         _check(rc)
     Ts = np.array([np.array(r.T[:], dtype=np.float64).reshape(4, 4) for r in res])
     return Ts, [AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers)) for r in res]
+
+
+def align_batched_sharded(src: torch.Tensor, src_cov: torch.Tensor, offsets, entry_chunk, num_chunks: int, B: int,
+                          tgt: Index, tgt_cov: torch.Tensor, T0s, allreduce=None, max_iter=64, lm=True, rot_eps=1e-6,
+                          trans_eps=1e-5, max_corr_dist=1.0, allow_degenerate=False):
+    """Sharded batched align with the reduction on the device
+    (gicp_align_batched_sharded): E local entries (offsets [E+1]), entry e = chunk
+    row entry_chunk[e] = b * num_chunks + c. allreduce(table) must sum the float64
+    device tensor `table` [B * num_chunks * 32] over the ranks in place on the
+    current stream (torch.distributed.all_reduce; sharding.make_allreduce), or None
+    for a single process."""
+    src = _pts(src, "src")
+    o = _offsets(offsets, src.shape[0], allow_empty=True)
+    E = o.size - 1
+    ec = np.ascontiguousarray(np.asarray(entry_chunk, dtype=np.int32).reshape(E))
+    T0h = np.ascontiguousarray(np.asarray(T0s, dtype=np.float64).reshape(B, 16))
+    p = AlignParams(int(max_iter), int(bool(lm)), float(rot_eps), float(trans_eps), float(max_corr_dist))
+    res = (AlignResult * B)()
+    table = torch.zeros(B * int(num_chunks) * 32, dtype=torch.float64, device=tgt.device)
+    err = []
+
+    def cb(ptr, count, user, stream):
+        try:
+            allreduce(table)
+            return 0
+        except Exception as e:  # reported after the call returns
+            err.append(e)
+            return 1
+    cfn = ALLREDUCE_FN(cb) if allreduce is not None else ALLREDUCE_FN()
+    rc = _lib.gicp_align_batched_sharded(_dptr(src) if src.shape[0] else None,
+                                         _dptr(src_cov.contiguous()) if src.shape[0] else None, o.ctypes.data_as(_P),
+                                         E, ec.ctypes.data_as(_P) if E else None, int(num_chunks), B, tgt.handle,
+                                         _dptr(tgt_cov.contiguous()), T0h.ctypes.data_as(_P), ctypes.byref(p),
+                                         ctypes.cast(res, _P), _dptr(table), cfn, None, _stream())
+    if err:
+        raise err[0]
+    if not (allow_degenerate and rc == EDEGENERATE):
+        _check(rc)
+    Ts = np.array([np.array(r.T[:], dtype=np.float64).reshape(4, 4) for r in res])
+    return Ts, [AlignInfo(int(r.iterations), bool(r.converged), float(r.error), int(r.inliers)) for r in res]
+
+
+def combine_chunks(table: torch.Tensor, B: int, num_chunks: int, width: int, out=None) -> torch.Tensor:
+    """gicp_combine_chunks: [B][num_chunks][width] float64 device -> [B][width], summed
+    over the chunks in chunk order."""
+    table = table.contiguous()
+    out = out if out is not None else torch.empty((B, width), dtype=torch.float64, device=table.device)
+    _check(_lib.gicp_combine_chunks(_dptr(table), int(B), int(num_chunks), int(width), _dptr(out), _stream()))
+    return out
 
 
 def attach_voxels(index: Index, cov: torch.Tensor):

@@ -10,7 +10,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgicp_b200.so")
-SOURCES = ["api.cu", "index.cu", "knn.cu", "cov.cu", "linearize.cu", "prep.cu", "vgicp.cu", "ground.cu", "cluster.cu", "submap.cu"]
+SOURCES = ["api.cu", "index.cu", "knn.cu", "cov.cu", "linearize.cu", "prep.cu", "vgicp.cu", "ground.cu", "cluster.cu", "submap.cu", "shard.cu"]
 HEADERS = ["gicp_internal.cuh", "cov_device.cuh", "lin_device.cuh", "sortnet.cuh", "knn_tile.cuh"]
 
 NVCC_FLAGS = [

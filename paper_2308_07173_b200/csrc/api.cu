@@ -311,6 +311,7 @@ GICP_API void gicp_index_free(gicp_index idx) {
     if (idx->vox_cov) cudaFreeAsync(idx->vox_cov, s);
     if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
     if (idx->tiles1) cudaFreeAsync(idx->tiles1, s);
+    if (idx->tile_of) cudaFreeAsync(idx->tile_of, s);
     cudaGetLastError();
     delete idx;
 }
@@ -836,12 +837,34 @@ GICP_API int gicp_linearize_batched(const float* src, const float* src_cov, cons
 // belonging to registration entry_reg[e]; after every round the entry rows are
 // turned into registration rows by `reduce` (a cross-rank combine) or, without
 // one, summed in entry order.
+// device-side sharding (gicp_align_batched_sharded): entry e is global chunk row
+// gid[e] = b * nc + c; rows go through the device chunk table and `ar` (shard.cu)
+struct DevShard {
+    const int* gid;
+    int nc;
+    double* table;
+    gicp_allreduce_fn ar;
+    void* user;
+};
+
 static int align_batched_impl(const float* src, const float* src_cov, const int64_t* offsets, int E,
                               const int* entry_reg, int B, gicp_index tgt, const float* tgt_cov, const double* T0,
                               const gicp_align_params* prm, gicp_align_result* res, gicp_reduce_fn reduce,
-                              void* user, void* stream) {
+                              void* user, void* stream, const DevShard* ds = nullptr) {
     int rc;
-    if (E == 0 && reduce) {  // a process without entries still takes part in the rounds
+    std::vector<int> dreg;
+    if (ds) {  // the registration of each entry from its global chunk row
+        if (ds->nc < 1 || !ds->table || (E > 0 && !ds->gid))
+            return set_error(GICP_EINVAL, "gicp_align_batched_sharded: num_chunks / table / entry_chunk");
+        dreg.resize(E);
+        for (int e = 0; e < E; ++e) {
+            if (ds->gid[e] < 0 || ds->gid[e] >= B * ds->nc)
+                return set_error(GICP_EINVAL, "gicp_align_batched_sharded: entry_chunk out of range");
+            dreg[e] = ds->gid[e] / ds->nc;
+        }
+        entry_reg = dreg.data();
+    }
+    if (E == 0 && (reduce || ds)) {  // a process without entries still takes part in the rounds
         if (!offsets || offsets[0] != 0) return set_error(GICP_EINVAL, "gicp_align_batched: offsets");
     } else if ((rc = check_offsets(offsets, E, "gicp_align_batched"))) {
         return rc;
@@ -866,11 +889,24 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     char* ex = nullptr;
     // + the correspondence certificates paired with the two buffers (R27)
     const bool certs = GICP_ALIGN_CACHE && getenv("GICP_ALIGN_NOCACHE") == nullptr;
+    const size_t dev_extra = ds ? (size_t)std::max(E, 1) * (32 * sizeof(double) + sizeof(int)) + 64 : 0;
     if ((rc = batch_scratch(offsets, E,
                             2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
-                                (certs ? 2 * nsa * sizeof(float4) + 16 : 0),
+                                (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + dev_extra,
                             s, bs, &ex)))
         return rc;
+    double* Ed = nullptr;  // device entry rows [E][32] (device sharding)
+    int* gid_d = nullptr;
+    if (ds) {
+        Ed = (double*)(((uintptr_t)ex + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
+                        (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + 255) & ~(uintptr_t)255);
+        gid_d = (int*)(Ed + 32 * (size_t)std::max(E, 1));
+        if (E > 0 &&
+            (rc = check_cuda(cudaMemcpyAsync(gid_d, ds->gid, E * sizeof(int), cudaMemcpyHostToDevice, s), "H2D"))) {
+            cudaFreeAsync(bs.base, s);
+            return rc;
+        }
+    }
     int32_t* corrA = (int32_t*)ex;
     int32_t* corrB = corrA + nsa;
     float* src_p = (float*)(((uintptr_t)(corrB + nsa) + 15) & ~(uintptr_t)15);
@@ -883,8 +919,9 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         cudaFreeAsync(bs.base, s);
         return rc;
     }
-    // host-mapped: entry rows [E][32] | flag | pinned pose staging [E]
-    const size_t rows = (size_t)E * 32 * sizeof(double);
+    // host-mapped: entry rows [E][32] (device sharding: registration rows [B][32]) |
+    // flag | pinned pose staging [E]
+    const size_t rows = (size_t)(ds ? std::max(E, B) : E) * 32 * sizeof(double);
     MappedBatch* mb = mapped_batch(rows + 256 + (size_t)E * sizeof(Pose));
     if (!mb) {
         cudaFreeAsync(bs.base, s);
@@ -950,10 +987,27 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             bv.n_active = n_active;
             bv.out_stride = 32;
             bs.ls.seq = ++seq;
-            r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags, Hd, corrA, s,
-                                      bs.ls, corrB, bv, bs.nb);
+            LinScratch lsr = bs.ls;
+            if (ds) lsr.flag = nullptr;  // the combine kernel signals
+            r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags,
+                                      ds ? Ed : Hd, corrA, s, lsr, corrB, bv, bs.nb);
+            if (!r && !ds) r = wait_mapped(&mo, bs.ls.seq, s);
+            if (r) return r;
+        }
+        if (ds) {
+            // device chunk table: zero, this rank's rows, allreduce, chunk-ordered combine
+            const size_t tb = (size_t)B * ds->nc * 32 * sizeof(double);
+            r = check_cuda(cudaMemsetAsync(ds->table, 0, tb, s), "memset");
+            if (!r && n_active > 0) r = launch_scatter_rows(Ed, E, gid_d, bs.poses, ds->table, s);
+            if (!r && ds->ar && ds->ar(ds->table, (int64_t)B * ds->nc * 32, ds->user, stream) != 0)
+                r = set_error(GICP_ECUDA, "gicp_align_batched_sharded: the allreduce callback failed");
+            if (r) return r;
+            bs.ls.seq = ++seq;
+            r = launch_combine_chunks(ds->table, B, ds->nc, 32, Hd, bs.ls.flag, bs.ls.seq, s);
             if (!r) r = wait_mapped(&mo, bs.ls.seq, s);
             if (r) return r;
+            std::memcpy(Hr.data(), He, (size_t)B * 32 * sizeof(double));
+            return GICP_OK;
         }
         for (int e = 0; e < E; ++e)  // rows of entries not launched this round are zero
             if (!pst[e].active) std::memset(He + 32 * e, 0, 32 * sizeof(double));
@@ -1140,6 +1194,24 @@ GICP_API int gicp_align_batched(const float* src, const float* src_cov, const in
                                 const gicp_align_params* prm, gicp_align_result* res, void* stream) {
     return align_batched_impl(src, src_cov, offsets, B, nullptr, B, tgt, tgt_cov, T0, prm, res, nullptr, nullptr,
                               stream);
+}
+
+GICP_API int gicp_align_batched_sharded(const float* src, const float* src_cov, const int64_t* offsets, int E,
+                                        const int* entry_chunk, int num_chunks, int B, gicp_index tgt,
+                                        const float* tgt_cov, const double* T0, const gicp_align_params* prm,
+                                        gicp_align_result* res, double* table, gicp_allreduce_fn allreduce,
+                                        void* user, void* stream) {
+    const DevShard ds{entry_chunk, num_chunks, table, allreduce, user};
+    return align_batched_impl(src, src_cov, offsets, E, nullptr, B, tgt, tgt_cov, T0, prm, res, nullptr, nullptr,
+                              stream, &ds);
+}
+
+GICP_API int gicp_combine_chunks(const double* table, int B, int num_chunks, int width, double* out, void* stream) {
+    if (!table || !out || B < 0 || num_chunks < 1 || width < 1)
+        return set_error(GICP_EINVAL, "gicp_combine_chunks: arguments");
+    if (B == 0) return GICP_OK;
+    init_pool_once();
+    return launch_combine_chunks(table, B, num_chunks, width, out, nullptr, 0u, (cudaStream_t)stream);
 }
 
 GICP_API int gicp_align_batched_ex(const float* src, const float* src_cov, const int64_t* offsets, int E,

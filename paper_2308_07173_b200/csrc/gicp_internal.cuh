@@ -165,7 +165,8 @@ struct gicp_index_s {
     int2* adj_oc1 = nullptr;              // the same lists for level 1 (escalated queries)
     int2* adj_rng1 = nullptr;
     int* tiles1 = nullptr;                // level-1 voxels in sorted order: first point of each, then n
-    int64_t n_tiles1 = 0;                 //   (the work units of the tiled kNN, knn_tile.cuh)
+    int64_t n_tiles1 = 0;                 //   (the staging units of the tiled kNN, knn_tile.cuh)
+    int* tile_of = nullptr;               // [n] the level-1 voxel (index into tiles1) of each sorted point
     float4* cov_sorted = nullptr;         // attached covariances in sorted order (2 x float4 per point)
     float4* vox_mu = nullptr;             // VGICP: per level-0 voxel, at its head: mean - first point (xyz), N (w)
     float4* vox_cov = nullptr;            // VGICP: mean covariance of the voxel's points (2 x float4 at the head)
@@ -296,6 +297,11 @@ size_t vgicp_scratch_bytes(int64_t ns);
 int launch_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, const gicp_index_s* tgt,
                            const double T[16], const double* pivot, int mode, int flags, int* base, double* out29,
                            cudaStream_t s, const LinScratch* pre = nullptr);
+// sharded linearisation (shard.cu): entry rows -> global chunk table, chunk-ordered combine
+int launch_scatter_rows(const double* rows, int E, const int* gid_dev, const Pose* poses_dev, double* table,
+                        cudaStream_t s);
+int launch_combine_chunks(const double* table, int B, int nc, int width, double* out, volatile unsigned* flag,
+                          unsigned seq, cudaStream_t s);
 int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
                 cudaStream_t s, const int64_t* offs = nullptr, int nseg = 1);
 

@@ -197,6 +197,14 @@ __global__ void k_cells(const unsigned long long* __restrict__ keys, int64_t n, 
 
 __global__ void k_set_int(int* p, int v) { *p = v; }
 
+// tile_of[p] = t for every point p of tile t (one warp per tile)
+__global__ void k_tile_of(const int* __restrict__ tiles, int64_t nt, int* __restrict__ tile_of) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (w >= nt) return;
+    const int a = tiles[w], b = tiles[w + 1];
+    for (int p = a + (int)(threadIdx.x & 31); p < b; p += 32) tile_of[p] = (int)w;
+}
+
 // run tails of every level write the end of their voxel
 __global__ void k_cell_ends(const unsigned long long* __restrict__ keys, int64_t n, LevelSet ls) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -476,6 +484,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if (idx->adj_oc1) cudaFreeAsync(idx->adj_oc1, s);
         if (idx->adj_rng1) cudaFreeAsync(idx->adj_rng1, s);
         if (idx->tiles1) cudaFreeAsync(idx->tiles1, s);
+        if (idx->tile_of) cudaFreeAsync(idx->tile_of, s);
         delete idx;
         return code;
     };
@@ -519,6 +528,12 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
         if ((rc = alloc_async(tmp, tb, s))) return fail(rc);
         cub::DeviceRadixSort::SortKeys(tmp.p, tb, heads1, idx->tiles1, (int)n1, 0, bits, s);
         k_set_int<<<1, 1, 0, s>>>(idx->tiles1 + n1, (int)n);
+        if (cudaMallocAsync(&idx->tile_of, n * sizeof(int), s) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(set_error(GICP_ENOMEM, "tile map allocation failed"));
+        }
+        idx->device_bytes += n * (int64_t)sizeof(int);
+        k_tile_of<<<grid_for(n1 * 32, 256), 256, 0, s>>>(idx->tiles1, n1, idx->tile_of);
     }
     k_scatter<<<grid_for(n, 256), 256, 0, s>>>(xyz, (int*)perm.p, n, idx->pts, idx->pts_orig);
     if ((rc = check_cuda(cudaGetLastError(), "build kernels"))) return fail(rc);

@@ -565,14 +565,14 @@ struct Levels {
 bool launch_tile(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, int* counts,
                  int* listA, int* listB, int2* exact, cudaStream_t s) {
     static const bool off = getenv("GICP_KNN_TILE") && atoi(getenv("GICP_KNN_TILE")) == 0;
-    if (off || idx->tiles1 == nullptr || idx->n_tiles1 == 0 || (k != 10 && k != 20)) return false;
-    const unsigned grid = (unsigned)((idx->n_tiles1 + kTileWarps - 1) / kTileWarps);
+    if (off || idx->tiles1 == nullptr || idx->tile_of == nullptr || idx->n == 0 || (k != 10 && k != 20)) return false;
+    const unsigned grid = (unsigned)((idx->n + kTB - 1) / kTB);
     if (k == 20)
-        k_knn_tile<20><<<grid, kTileWarps * 32, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->n_tiles1, eps, nbr, d2,
-                                                        cov, counts + 2, listA, counts + 0, exact, counts + 3, listB);
+        k_knn_tile<20><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, idx->n, eps, nbr, d2, cov,
+                                            counts + 2, listA, counts + 0, exact, counts + 3, listB);
     else
-        k_knn_tile<10><<<grid, kTileWarps * 32, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->n_tiles1, eps, nbr, d2,
-                                                        cov, counts + 2, listA, counts + 0, exact, counts + 3, listB);
+        k_knn_tile<10><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, idx->n, eps, nbr, d2, cov,
+                                            counts + 2, listA, counts + 0, exact, counts + 3, listB);
     return true;
 }
 

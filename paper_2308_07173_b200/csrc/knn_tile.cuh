@@ -13,25 +13,29 @@
 // takes one of the tile's points as its query and scans the staged list in lockstep
 // with the warp: every lane reads the same candidate (a shared-memory broadcast), no
 // per-lane range bookkeeping. The top K+1 keys live in registers as 32-bit packed
-// keys (bits(d2) with the low 8 bits replaced by the candidate's slot + 1), updated
+// keys (bits(d2) with the low 9 bits replaced by the candidate's slot + 1), updated
 // by comparator networks of single-instruction min/max (sortnet.cuh): the first 32
 // candidates are sorted directly; later candidates below the current (K+1)-th key go
 // to an 8-key register buffer, merged into the list when a lane's buffer fills.
 //
 // Exactness: the packed order equals the (d2, index) order except among keys whose
-// d2 agree in their upper 24 bits. If no two adjacent keys of the K+1 list share
+// d2 agree in their upper 23 bits. If no two adjacent keys of the K+1 list share
 // them, the K smallest are exactly the first K in this order (every other candidate
 // has a strictly larger d2). Otherwise (near-ties, exact ties) the query goes to the
 // exact path. The query is final when the K-th d2 (an upper bound: low bits set) is
 // below the squared distance from the query to the box boundary minus the grid's
 // rounding slack (every point outside the box is farther); else it escalates to the
-// pyramid path. Tiles with more than 255 staged points run the per-query level-0
+// pyramid path. Tiles with more than 511 staged points run the per-query level-0
 // kernel instead.
 
-constexpr int kTileWarps = 4;
-constexpr int kTileCap = 255;  // staged points per tile (slot + 1 fits 8 bits)
-constexpr int kTileFirst = 32; // candidates sorted directly before the buffered merges
-constexpr int kTileBuf = 8;    // pending keys per lane
+constexpr int kTB = 128;        // queries (threads) per block: consecutive sorted positions
+constexpr int kBlkTiles = 12;   // tiles a block may stage (sparser blocks: per-query kernel)
+constexpr int kBlkCap = 1536;   // staged points per block (+ kTileCap of padding: unclamped reads)
+constexpr int kSlotBits = 9;    // low key bits holding the candidate's slot + 1
+constexpr unsigned kSlotMask = (1u << kSlotBits) - 1u;
+constexpr int kTileCap = (int)kSlotMask;  // staged points per tile (slot + 1 fits the slot bits)
+constexpr int kTileFirst = 32;  // candidates sorted directly before the buffered merges
+constexpr int kTileBuf = 12;    // pending keys per lane (shared memory); merged once >= 8
 
 // the 56 outer voxels of the box (offsets -1..2 per axis around the tile's 2x2x2
 // block at 0..1), nearest-first: 24 face-, 24 edge-, 8 corner-adjacent
@@ -85,74 +89,120 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 __device__ __forceinline__ unsigned pack_key(float d2, int slot) {
-    return (__float_as_uint(d2) & 0xffffff00u) | (unsigned)(slot + 1);
+    return (__float_as_uint(d2) & ~kSlotMask) | (unsigned)(slot + 1);
 }
 
-// merge the 8-key buffer into the sorted (K+1)-list; buffer reset to empty
+// merge the lane's pending keys (buf[0..nb) of its shared-memory column) into the
+// sorted (K+1)-list
 template <int NL>
-__device__ __forceinline__ void tile_merge(unsigned (&T)[NL], unsigned (&B)[kTileBuf]) {
-    constexpr net::Net s8 = net::make_sort_net<kTileBuf, kTileBuf>();
+__device__ __forceinline__ void tile_merge(unsigned (&T)[NL], const unsigned* __restrict__ col, int nb) {
+    constexpr net::Net sb = net::make_sort_net<kTileBuf, kTileBuf>();
+    constexpr net::Net mg = net::make_merge_net<NL, kTileBuf, NL>();
+    unsigned b[kTileBuf];
+#pragma unroll
+    for (int i = 0; i < kTileBuf; ++i) b[i] = i < nb ? col[i * kTB] : 0xffffffffu;
+    GICP_APPLY_NET(b, sb);
     unsigned w[NL + kTileBuf];
 #pragma unroll
-    for (int i = 0; i < kTileBuf; ++i) w[i] = B[i];
-    {
-        unsigned b8[kTileBuf];
-#pragma unroll
-        for (int i = 0; i < kTileBuf; ++i) b8[i] = B[i];
-        GICP_APPLY_NET(b8, s8);
-#pragma unroll
-        for (int i = 0; i < kTileBuf; ++i) w[NL + i] = b8[s8.out[i]];
-    }
-#pragma unroll
     for (int i = 0; i < NL; ++i) w[i] = T[i];
-    constexpr net::Net mg = net::make_merge_net<NL, kTileBuf, NL>();
+#pragma unroll
+    for (int i = 0; i < kTileBuf; ++i) w[NL + i] = b[sb.out[i]];
     GICP_APPLY_NET(w, mg);
 #pragma unroll
     for (int i = 0; i < NL; ++i) T[i] = w[mg.out[i]];
-#pragma unroll
-    for (int i = 0; i < kTileBuf; ++i) B[i] = 0xffffffffu;
 }
 
+// exact (d2, original index) order of two staged candidates for query q
+__device__ __forceinline__ bool exact_less(const float4& q, const float4& a, const float4& b) {
+    const float da = dist2(q.x, q.y, q.z, a.x, a.y, a.z), db = dist2(q.x, q.y, q.z, b.x, b.y, b.z);
+    return da < db || (da == db && __float_as_int(a.w) < __float_as_int(b.w));
+}
+
+#ifndef GICP_TILE_MINB
+#define GICP_TILE_MINB 1
+#endif
 template <int K>
-__global__ void __launch_bounds__(kTileWarps * 32) k_knn_tile(const float4* __restrict__ pts, Grid g0,
-                                                              const int* __restrict__ tiles, int64_t ntiles, float eps,
-                                                              int32_t* __restrict__ nbr, float* __restrict__ d2out,
-                                                              float* __restrict__ cov, int* __restrict__ esc_count,
-                                                              int* __restrict__ esc_list, int* __restrict__ exact_count,
-                                                              int2* __restrict__ exact_list,
-                                                              int* __restrict__ fb_count, int* __restrict__ fb_list) {
+__global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* __restrict__ pts, Grid g0,
+                                                  const int* __restrict__ tiles, const int* __restrict__ tile_of,
+                                                  int64_t n, float eps, int32_t* __restrict__ nbr,
+                                                  float* __restrict__ d2out, float* __restrict__ cov,
+                                                  int* __restrict__ esc_count, int* __restrict__ esc_list,
+                                                  int* __restrict__ exact_count, int2* __restrict__ exact_list,
+                                                  int* __restrict__ fb_count, int* __restrict__ fb_list) {
     constexpr int NL = K + 1;
-    __shared__ __align__(128) float4 s_cand[kTileWarps][kTileCap + 1];
-    __shared__ __align__(8) unsigned long long s_bar[kTileWarps];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4* cand = s_cand[warp];
-    unsigned long long* bar = &s_bar[warp];
-    if (lane == 0) mbar_init(bar, 1);
+    __shared__ __align__(128) float4 cand[kBlkCap + kTileCap];
+    __shared__ unsigned buf[kTileBuf][kTB];
+    __shared__ int2 rng[kBlkTiles][57];
+    __shared__ int t_off[kBlkTiles], t_cnt[kBlkTiles], t_start[kBlkTiles], t_base[kBlkTiles][3];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ int s_ta, s_nt, s_ok;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t q0 = (int64_t)blockIdx.x * kTB, q = q0 + tid;
+    const bool act = q < n;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        const int ta = __ldg(tile_of + q0), tb = __ldg(tile_of + min(q0 + kTB, n) - 1);
+        s_ta = ta;
+        s_nt = tb - ta + 1;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    unsigned phase = 0;
-    const float s = g0.cell, slack = g0.slack;
-    for (int64_t t = (int64_t)blockIdx.x * kTileWarps + warp; t < ntiles; t += (int64_t)gridDim.x * kTileWarps) {
+    __syncthreads();
+    const int ta = s_ta, nt = s_nt;
+    auto fallback_all = [&]() { push_warp(fb_count, fb_list, act, (int)q); };
+    if (nt > kBlkTiles) {  // sparse region: many tiny tiles
+        fallback_all();
+        return;
+    }
+    // (1) per tile (warp w: tiles w, w + 4): the ranges of its box
+    for (int lt = warp; lt < nt; lt += kTB / 32) {
+        const int t = ta + lt;
         const int s1 = __ldg(tiles + t), e1 = __ldg(tiles + t + 1);
-        const int Q = e1 - s1;
-        // the tile's level-0 base coordinates (even): the level-1 voxel of its first point
         const float4 f0 = __ldg(pts + s1);
         const int bx = cell_coord(f0.x, g0.ox, g0.inv_cell) & ~1;
         const int by = cell_coord(f0.y, g0.oy, g0.inv_cell) & ~1;
         const int bz = cell_coord(f0.z, g0.oz, g0.inv_cell) & ~1;
-        // the 56 outer voxels: lane takes outer cells lane and lane + 32
-        int2 ra = make_int2(0, 0), rb = make_int2(0, 0);
-        {
-            const signed char* d = c_outer.d[lane];
-            ra = cell_lookup(g0, bx + d[0], by + d[1], bz + d[2]);
-            if (lane < 24) {
-                const signed char* e = c_outer.d[lane + 32];
-                rb = cell_lookup(g0, bx + e[0], by + e[1], bz + e[2]);
-            }
+        const signed char* d = c_outer.d[lane];
+        const int2 ra = cell_lookup(g0, bx + d[0], by + d[1], bz + d[2]);
+        int2 rb = make_int2(0, 0);
+        if (lane < 24) {
+            const signed char* e = c_outer.d[lane + 32];
+            rb = cell_lookup(g0, bx + e[0], by + e[1], bz + e[2]);
         }
         const int ca = max(ra.y - ra.x, 0), cb = max(rb.y - rb.x, 0);
-        // offsets: inner block [0, Q), then the outer voxels in table order
-        int ia = ca, ib = cb;
+        rng[lt][1 + lane] = make_int2(ra.x, ca);
+        if (lane < 24) rng[lt][33 + lane] = make_int2(rb.x, cb);
+        const int tot = __reduce_add_sync(0xffffffffu, ca + cb);
+        if (lane == 0) {
+            rng[lt][0] = make_int2(s1, e1 - s1);
+            t_cnt[lt] = e1 - s1 + tot;
+            t_start[lt] = s1;
+            t_base[lt][0] = bx;
+            t_base[lt][1] = by;
+            t_base[lt][2] = bz;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int o = 0, ok = 1;
+        for (int lt = 0; lt < nt; ++lt) {
+            t_off[lt] = o;
+            o += t_cnt[lt];
+            ok &= t_cnt[lt] <= kTileCap;
+        }
+        ok &= o <= kBlkCap;
+        s_ok = ok;
+        if (ok) mbar_arrive_expect_tx(&bar, (unsigned)o * 16u);
+    }
+    __syncthreads();
+    if (!s_ok) {  // a tile too dense to stage
+        fallback_all();
+        return;
+    }
+    // (2) one TMA bulk copy per non-empty range, completion on the block's barrier
+    for (int lt = warp; lt < nt; lt += kTB / 32) {
+        const int2 a = rng[lt][lane];
+        const int2 b = lane + 32 < 57 ? rng[lt][lane + 32] : make_int2(0, 0);
+        int ia = a.y, ib = b.y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int va = __shfl_up_sync(0xffffffffu, ia, o), vb = __shfl_up_sync(0xffffffffu, ib, o);
@@ -161,143 +211,147 @@ __global__ void __launch_bounds__(kTileWarps * 32) k_knn_tile(const float4* __re
                 ib += vb;
             }
         }
-        const int tot_a = __shfl_sync(0xffffffffu, ia, 31), tot_b = __shfl_sync(0xffffffffu, ib, 31);
-        const int oa = Q + ia - ca, ob = Q + tot_a + ib - cb;
-        const int C = Q + tot_a + tot_b;
-        if (C > kTileCap) {  // dense tile: the per-query level-0 kernel
-            for (int q0 = 0; q0 < Q; q0 += 32) {
-                const bool a = q0 + lane < Q;
-                push_warp(fb_count, fb_list, a, s1 + q0 + lane);
-            }
-            continue;
-        }
-        // stage the box: one bulk copy per non-empty range, completion on the barrier
-        if (lane == 0) {
-            mbar_arrive_expect_tx(bar, (unsigned)C * 16u);
-            bulk_g2s(cand, pts + s1, (unsigned)Q * 16u, bar);
-        }
-        __syncwarp();
-        if (ca > 0) bulk_g2s(cand + oa, pts + ra.x, (unsigned)ca * 16u, bar);
-        if (cb > 0) bulk_g2s(cand + ob, pts + rb.x, (unsigned)cb * 16u, bar);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-
-        for (int q0 = 0; q0 < Q; q0 += 32) {
-            const int qi = q0 + lane;
-            const bool act = qi < Q;
-            const float4 qp = cand[act ? qi : q0];
-            // (1) the first kTileFirst candidates, sorted directly
-            unsigned T[NL];
-            {
-                constexpr net::Net sn = net::make_sort_net<kTileFirst, NL>();
-                unsigned v[kTileFirst];
-#pragma unroll
-                for (int i = 0; i < kTileFirst; ++i) {
-                    v[i] = 0xffffffffu;
-                    if (i < C) {
-                        const float4 p = cand[i];
-                        v[i] = pack_key(dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z), i);
-                    }
-                }
-                GICP_APPLY_NET(v, sn);
-#pragma unroll
-                for (int i = 0; i < NL; ++i) T[i] = v[sn.out[i]];
-            }
-            // (2) the rest: keys below the current (K+1)-th go through the buffer
-            unsigned B[kTileBuf];
-#pragma unroll
-            for (int i = 0; i < kTileBuf; ++i) B[i] = 0xffffffffu;
-            int nb = 0;
-            unsigned thr = T[NL - 1];
-            for (int c = kTileFirst; c < C; ++c) {
-                const float4 p = cand[c];
-                const unsigned key = pack_key(dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z), c);
-                const bool pass = act && key < thr;
-                if (__any_sync(0xffffffffu, pass)) {
-#pragma unroll
-                    for (int i = kTileBuf - 1; i > 0; --i) B[i] = pass ? B[i - 1] : B[i];
-                    B[0] = pass ? key : B[0];
-                    nb += pass ? 1 : 0;
-                    if (__any_sync(0xffffffffu, nb == kTileBuf)) {
-                        tile_merge<NL>(T, B);
-                        nb = 0;
-                        thr = T[NL - 1];
-                    }
-                }
-            }
-            if (__any_sync(0xffffffffu, nb > 0)) tile_merge<NL>(T, B);
-            // (3) decisions: enough candidates, stop rule on the box, near-ties
-            int st = 0;  // 0 emit, 1 escalate, 2 exact path
-            if (act) {
-                bool amb = false;
-#pragma unroll
-                for (int r = 0; r < K; ++r) amb |= (T[r] >> 8) == (T[r + 1] >> 8);
-                const float kth = __uint_as_float(T[K - 1] | 0xffu);  // >= the K-th d2
-                const QGeom G = make_geom(g0, qp.x, qp.y, qp.z);
-                const float mx = fminf(G.fx + (float)(G.cx - bx + 1) * s, (float)(bx + 3 - G.cx) * s - G.fx);
-                const float my = fminf(G.fy + (float)(G.cy - by + 1) * s, (float)(by + 3 - G.cy) * s - G.fy);
-                const float mz = fminf(G.fz + (float)(G.cz - bz + 1) * s, (float)(bz + 3 - G.cz) * s - G.fz);
-                const float m = fminf(mx, fminf(my, mz)) - slack;
-                const bool full = T[K - 1] != 0xffffffffu;
-                const bool fin = full && m > 0.0f && kth < m * m * kRel;
-                st = !fin ? 1 : (amb ? 2 : 0);
-            }
-            push_warp(esc_count, esc_list, act && st == 1, s1 + qi);
-            push_warp2(exact_count, exact_list, act && st == 2, make_int2(s1 + qi, 0));
-            if (!act || st != 0) continue;
-            // (4) emit: original indices, exact d2, covariance of the K neighbours
-            const int64_t row = __float_as_int(qp.w);
-            const float4 p0 = cand[(T[0] & 0xffu) - 1];
-            float sx = 0.f, sy = 0.f, sz = 0.f;
-            // rows written 4 (K % 4 == 0), 2 or 1 values at a time as they are formed
-            constexpr int VW = (K % 4 == 0) ? 4 : ((K % 2 == 0) ? 2 : 1);
-#pragma unroll
-            for (int r0 = 0; r0 < K; r0 += VW) {
-                int ids[VW];
-                float dd[VW];
-#pragma unroll
-                for (int u = 0; u < VW; ++u) {
-                    const float4 p = cand[(T[r0 + u] & 0xffu) - 1];
-                    ids[u] = __float_as_int(p.w);
-                    dd[u] = dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z);
-                    sx += p.x - p0.x;
-                    sy += p.y - p0.y;
-                    sz += p.z - p0.z;
-                }
-                if (VW == 4) {
-                    if (nbr) *reinterpret_cast<int4*>(nbr + row * K + r0) = make_int4(ids[0], ids[1 % VW], ids[2 % VW], ids[3 % VW]);
-                    if (d2out)
-                        *reinterpret_cast<float4*>(d2out + row * K + r0) = make_float4(dd[0], dd[1 % VW], dd[2 % VW], dd[3 % VW]);
-                } else if (VW == 2) {
-                    if (nbr) *reinterpret_cast<int2*>(nbr + row * K + r0) = make_int2(ids[0], ids[1 % VW]);
-                    if (d2out) *reinterpret_cast<float2*>(d2out + row * K + r0) = make_float2(dd[0], dd[1 % VW]);
-                } else {
-                    if (nbr) nbr[row * K + r0] = ids[0];
-                    if (d2out) d2out[row * K + r0] = dd[0];
-                }
-            }
-            if (!cov) continue;
-            const float invk = 1.0f / (float)K;
-            const float mxm = sx * invk, mym = sy * invk, mzm = sz * invk;
-            float c00 = 0.f, c01 = 0.f, c02 = 0.f, c11 = 0.f, c12 = 0.f, c22 = 0.f;
-#pragma unroll
-            for (int r = 0; r < K; ++r) {
-                const float4 p = cand[(T[r] & 0xffu) - 1];
-                const float x = (p.x - p0.x) - mxm, y = (p.y - p0.y) - mym, z = (p.z - p0.z) - mzm;
-                c00 = fmaf(x, x, c00);
-                c01 = fmaf(x, y, c01);
-                c02 = fmaf(x, z, c02);
-                c11 = fmaf(y, y, c11);
-                c12 = fmaf(y, z, c12);
-                c22 = fmaf(z, z, c22);
-            }
-            float cc[6];
-            plane_cov(c00 * invk, c01 * invk, c02 * invk, c11 * invk, c12 * invk, c22 * invk, eps, cc);
-            store_cov(cov, row, cc);
-        }
-        // the next tile's bulk copies overwrite the buffer: order this warp's reads
-        // (generic proxy) before them (async proxy)
-        __syncwarp();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int tot_a = __shfl_sync(0xffffffffu, ia, 31);
+        const int oa = t_off[lt] + ia - a.y, ob = t_off[lt] + tot_a + ib - b.y;
+        if (a.y > 0) bulk_g2s(cand + oa, pts + a.x, (unsigned)a.y * 16u, &bar);
+        if (b.y > 0) bulk_g2s(cand + ob, pts + b.x, (unsigned)b.y * 16u, &bar);
     }
+    mbar_wait(&bar, 0);
+    // (3) per lane: its query and its tile's staged box
+    int lt = 0, base = 0, C = 0;
+    float4 qp = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+        lt = __ldg(tile_of + q) - ta;
+        base = t_off[lt];
+        C = t_cnt[lt];
+        qp = cand[base + (int)(q - t_start[lt])];
+    }
+    unsigned T[NL];
+    {
+        constexpr net::Net sn = net::make_sort_net<kTileFirst, NL>();
+        unsigned v[kTileFirst];
+#pragma unroll
+        for (int i = 0; i < kTileFirst; ++i) {
+            v[i] = 0xffffffffu;
+            if (i < C) {
+                const float4 p = cand[base + i];
+                v[i] = pack_key(dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z), i);
+            }
+        }
+        GICP_APPLY_NET(v, sn);
+#pragma unroll
+        for (int i = 0; i < NL; ++i) T[i] = v[sn.out[i]];
+    }
+    unsigned* col = &buf[0][tid];
+    int nb = 0;
+    unsigned thr = T[NL - 1] | kSlotMask;
+    const int cmax = __reduce_max_sync(0xffffffffu, C);
+    for (int c = kTileFirst; c < cmax; c += 4) {
+        unsigned kk[4];
+        bool ps[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int cc = c + u;
+            const float4 p = cand[base + cc];  // past C: padding or the next tile (masked below)
+            const float dd = dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z);
+            ps[u] = cc < C && __float_as_uint(dd) <= thr;
+            kk[u] = pack_key(dd, cc);
+        }
+        if (__any_sync(0xffffffffu, ps[0] | ps[1] | ps[2] | ps[3])) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ps[u]) col[(nb++) * kTB] = kk[u];
+            if (__any_sync(0xffffffffu, nb >= kTileBuf - 4)) {
+                tile_merge<NL>(T, col, nb);
+                nb = 0;
+                thr = T[NL - 1] | kSlotMask;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, nb > 0)) tile_merge<NL>(T, col, nb);
+    // (4) decisions: enough candidates, stop rule on the box, order certainty
+    int st = 0;  // 0 emit, 1 escalate, 2 exact path
+    bool amb_in = false, amb_b = false;
+    if (act) {
+#pragma unroll
+        for (int r = 0; r < K - 1; ++r) amb_in |= (T[r] >> kSlotBits) == (T[r + 1] >> kSlotBits);
+        amb_b = (T[K - 1] >> kSlotBits) == (T[K] >> kSlotBits);
+    }
+    if (__any_sync(0xffffffffu, amb_in && !amb_b)) {
+        // near-equal neighbours inside the list: their packed order must be the exact one
+        bool bad = false;
+        if (amb_in && !amb_b) {
+#pragma unroll
+            for (int r = 0; r < K - 1; ++r)
+                if ((T[r] >> kSlotBits) == (T[r + 1] >> kSlotBits))
+                    bad |= !exact_less(qp, cand[base + (int)(T[r] & kSlotMask) - 1],
+                                       cand[base + (int)(T[r + 1] & kSlotMask) - 1]);
+        }
+        amb_in = bad;
+    }
+    if (act) {
+        const int bx = t_base[lt][0], by = t_base[lt][1], bz = t_base[lt][2];
+        const float s = g0.cell;
+        const float kth = __uint_as_float(T[K - 1] | kSlotMask);  // >= the K-th d2
+        const QGeom G = make_geom(g0, qp.x, qp.y, qp.z);
+        const float mx = fminf(G.fx + (float)(G.cx - bx + 1) * s, (float)(bx + 3 - G.cx) * s - G.fx);
+        const float my = fminf(G.fy + (float)(G.cy - by + 1) * s, (float)(by + 3 - G.cy) * s - G.fy);
+        const float mz = fminf(G.fz + (float)(G.cz - bz + 1) * s, (float)(bz + 3 - G.cz) * s - G.fz);
+        const float m = fminf(mx, fminf(my, mz)) - g0.slack;
+        const bool full = T[K - 1] != 0xffffffffu;
+        const bool fin = full && m > 0.0f && kth < m * m * kRel;
+        st = !fin ? 1 : ((amb_in || amb_b) ? 2 : 0);
+    }
+    push_warp(esc_count, esc_list, act && st == 1, (int)q);
+    push_warp2(exact_count, exact_list, act && st == 2, make_int2((int)q, 0));
+    if (!act || st != 0) return;
+    // (5) emit: original indices, exact d2, covariance of the K neighbours
+    const int64_t row = __float_as_int(qp.w);
+    const float4 p0 = cand[base + (int)(T[0] & kSlotMask) - 1];
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    // rows written 4 (K % 4 == 0), 2 or 1 values at a time as they are formed
+    constexpr int VW = (K % 4 == 0) ? 4 : ((K % 2 == 0) ? 2 : 1);
+#pragma unroll
+    for (int r0 = 0; r0 < K; r0 += VW) {
+        int ids[VW];
+        float dd[VW];
+#pragma unroll
+        for (int u = 0; u < VW; ++u) {
+            const float4 p = cand[base + (int)(T[r0 + u] & kSlotMask) - 1];
+            ids[u] = __float_as_int(p.w);
+            dd[u] = dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z);
+            sx += p.x - p0.x;
+            sy += p.y - p0.y;
+            sz += p.z - p0.z;
+        }
+        if (VW == 4) {
+            if (nbr) *reinterpret_cast<int4*>(nbr + row * K + r0) = make_int4(ids[0], ids[1 % VW], ids[2 % VW], ids[3 % VW]);
+            if (d2out)
+                *reinterpret_cast<float4*>(d2out + row * K + r0) = make_float4(dd[0], dd[1 % VW], dd[2 % VW], dd[3 % VW]);
+        } else if (VW == 2) {
+            if (nbr) *reinterpret_cast<int2*>(nbr + row * K + r0) = make_int2(ids[0], ids[1 % VW]);
+            if (d2out) *reinterpret_cast<float2*>(d2out + row * K + r0) = make_float2(dd[0], dd[1 % VW]);
+        } else {
+            if (nbr) nbr[row * K + r0] = ids[0];
+            if (d2out) d2out[row * K + r0] = dd[0];
+        }
+    }
+    if (!cov) return;
+    const float invk = 1.0f / (float)K;
+    const float mxm = sx * invk, mym = sy * invk, mzm = sz * invk;
+    float c00 = 0.f, c01 = 0.f, c02 = 0.f, c11 = 0.f, c12 = 0.f, c22 = 0.f;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+        const float4 p = cand[base + (int)(T[r] & kSlotMask) - 1];
+        const float x = (p.x - p0.x) - mxm, y = (p.y - p0.y) - mym, z = (p.z - p0.z) - mzm;
+        c00 = fmaf(x, x, c00);
+        c01 = fmaf(x, y, c01);
+        c02 = fmaf(x, z, c02);
+        c11 = fmaf(y, y, c11);
+        c12 = fmaf(y, z, c12);
+        c22 = fmaf(z, z, c22);
+    }
+    float cc[6];
+    plane_cov(c00 * invk, c01 * invk, c02 * invk, c11 * invk, c12 * invk, c22 * invk, eps, cc);
+    store_cov(cov, row, cc);
 }

@@ -1,6 +1,7 @@
 """Point-sharded batched registration (C4 across processes) on the
 GPU: each process linearises its chunks of every registration through
-gicp_align_batched_ex and one all_reduce per round combines them (gloo here:
+gicp_align_batched_sharded and one all_reduce of the device chunk table per round
+combines them, summed in chunk order on the device (gloo here:
 there is one GPU, both processes use it; the host-side collective never makes
 kernels wait on each other). World size 2 must reproduce world size 1 BITWISE
 (fixed chunking, chunk-ordered combine), and both must agree with the unsharded
@@ -108,3 +109,31 @@ def test_sharded_align_with_an_idle_rank():
     r2 = _run(2, tiny=True)
     for r in (0, 1):
         assert np.array_equal(r2[r][0], r1[0][0]) and r2[r][1] == r1[0][1]
+
+
+def test_combine_chunks_is_the_chunk_ordered_sum():
+    sys.path.insert(0, ROOT)
+    import paper_2308_07173_b200 as g
+    rng = np.random.default_rng(3)
+    B, nc, w = 7, 8, 32
+    t = rng.standard_normal((B, nc, w)) * 10.0 ** rng.integers(-8, 8, (B, nc, w))
+    ref = np.zeros((B, w))
+    for k in range(nc):
+        ref = ref + t[:, k]
+    out = g.combine_chunks(torch.from_numpy(t).cuda(), B, nc, w).cpu().numpy()
+    assert np.array_equal(out, ref)
+
+
+def test_sharded_linearize_world1():
+    """sharded_linearize without a process group: the chunk-ordered device combine of
+    the chunk linearisations, equal to the unsharded call to rounding."""
+    sys.path.insert(0, ROOT)
+    from paper_2308_07173_b200 import sharding
+    g, im, cm, src, cov, offs, T0 = _problem(TINY + [(30, 5000)])
+    s, c = src[offs[2]:offs[3]].contiguous(), cov[offs[2]:offs[3]].contiguous()
+    T = T0[2]
+    a = sharding.sharded_linearize(g, s, c, im, cm, T, 1.0, pivot=T[:3, 3]).cpu().numpy()
+    b, _ = g.linearize(s, c, im, cm, T, 1.0, pivot=T[:3, 3])
+    b = b.cpu().numpy()
+    assert a[28] == b[28]
+    assert np.allclose(a[:28], b[:28], rtol=1e-9, atol=1e-9 * np.abs(b[:28]).max())

@@ -1,9 +1,11 @@
-"""Multi-process host logic of the sharded linearisation (gloo, world_size 2, CPU).
+"""Multi-process host logic of the sharded linearisation (gloo, world_size 2-3, CPU).
 
-The chunk partials come from the ORACLE here (no GPU in this test); the sharding,
-all-gather and chunk-ordered combine are the product's (paper_2308_07173_b200/
-sharding.py). H, b, e must be bitwise identical to the single-process combine of
-the same chunks and agree with an unsharded linearisation to rounding.
+The chunk rows come from the ORACLE here (no GPU in this test); the chunking and the
+allreduce of the chunk table are the product's (paper_2308_07173_b200/sharding.py).
+The allreduced table must be bitwise the single-process table for every world size
+(the chunk-ordered sum itself is the library's, tested on the GPU in
+tests/test_gpu_sharded.py), and its chunk-ordered sum agrees with an unsharded
+linearisation to rounding.
 """
 import os
 import sys
@@ -35,17 +37,20 @@ def _problem():
 
 
 def _worker(rank, world, port, q):
+    import torch
     import torch.distributed as dist
     # file rendezvous: no TCP port to race for (a bind/close/reuse port probe is racy)
     dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     sh = _load_sharding()
     oracle, src, cs, tgt, ct, T0 = _problem()
-    local = {}
+    # this rank's chunk rows (the oracle stands in for the GPU linearisation) in the
+    # chunk table, zeros elsewhere; the product's allreduce fills the whole table
+    table = torch.zeros((1, sh.NUM_CHUNKS, 29), dtype=torch.float64)
     for c in sh.chunks_of_rank(rank, world):
         lo, hi = sh.chunk_bounds(len(src))[c]
-        local[c] = oracle.linearize(src[lo:hi], cs[lo:hi], tgt, ct, T0, 1.0, pivot=T0[:3, 3])[0]
-    full = sh.allgather_partials(local)
-    q.put((rank, sh.combine(full)))
+        table[0, c] = torch.from_numpy(oracle.linearize(src[lo:hi], cs[lo:hi], tgt, ct, T0, 1.0, pivot=T0[:3, 3])[0])
+    sh.make_allreduce()(table)
+    q.put((rank, table.numpy().copy()))
     dist.destroy_process_group()
 
 
@@ -70,6 +75,9 @@ def test_chunking_is_world_size_independent():
 
 
 def test_gloo_world2_matches_single_process_bitwise():
+    """The allreduced chunk table is bitwise the single-process table (every row has
+    one non-zero contributor); its chunk-ordered sum (the library's combine, done
+    here in the same order) agrees with an unsharded linearisation to rounding."""
     sh = _load_sharding()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -84,8 +92,10 @@ def test_gloo_world2_matches_single_process_bitwise():
     oracle, src, cs, tgt, ct, T0 = _problem()
     parts = np.stack([oracle.linearize(src[lo:hi], cs[lo:hi], tgt, ct, T0, 1.0, pivot=T0[:3, 3])[0]
                       for lo, hi in sh.chunk_bounds(len(src))])
-    single = sh.combine(parts)
-    assert np.array_equal(res[0], single) and np.array_equal(res[1], single)
+    assert np.array_equal(res[0][0], parts) and np.array_equal(res[1][0], parts)
+    single = np.zeros(29)
+    for c in range(sh.NUM_CHUNKS):
+        single = single + parts[c]
     whole, ab, _ = oracle.linearize(src, cs, tgt, ct, T0, 1.0, pivot=T0[:3, 3])
     assert single[28] == whole[28]
     assert np.all(np.abs(single[:28] - whole[:28]) <= 1e-12 * ab[:28] + 1e-300)
@@ -104,32 +114,33 @@ def _chunk_rows(b, c):
     return rng.standard_normal(32) * 10.0 ** rng.integers(-8, 8, 32)
 
 
-def _reduce_worker(rank, world, port, q):
+def _table_worker(rank, world, port, q):
+    import torch
     import torch.distributed as dist
-    # file rendezvous: no TCP port to race for (a bind/close/reuse port probe is racy)
     dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     sh = _load_sharding()
-    entries = sh.registration_chunks(SIZES, rank, world)
-    rows = np.stack([_chunk_rows(b, c) for (b, c, _, _) in entries]) if entries else np.zeros((0, 32))
-    out = sh.make_chunk_reducer(entries, len(SIZES))(rows)
-    q.put((rank, out))
+    table = torch.zeros((len(SIZES) * sh.NUM_CHUNKS, 32), dtype=torch.float64)
+    for (b, c, _, _) in sh.registration_chunks(SIZES, rank, world):
+        table[b * sh.NUM_CHUNKS + c] = torch.from_numpy(_chunk_rows(b, c))
+    sh.make_allreduce()(table)
+    q.put((rank, table.numpy().copy()))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_chunk_reducer_is_world_size_independent(world):
-    """Every rank gets the chunk-ordered sum of every registration's chunk rows,
-    bitwise equal to the single-process combine, for world sizes 2 and 3."""
+def test_chunk_table_allreduce_is_world_size_independent(world):
+    """Every rank gets the full chunk table of every registration, bitwise equal to
+    the single-process table, for world sizes 2 and 3 (what the library then sums in
+    chunk order on the device: gicp_align_batched_sharded)."""
     sh = _load_sharding()
     B = len(SIZES)
-    table = np.zeros((B * sh.NUM_CHUNKS, 32))
+    single = np.zeros((B * sh.NUM_CHUNKS, 32))
     for (b, c, _, _) in sh.registration_chunks(SIZES, 0, 1):
-        table[b * sh.NUM_CHUNKS + c] = _chunk_rows(b, c)
-    single = sh.combine_chunk_table(table, B)
+        single[b * sh.NUM_CHUNKS + c] = _chunk_rows(b, c)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_reduce_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_table_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in range(world))
