@@ -1,22 +1,37 @@
 #!/usr/bin/env python
-"""bench.py -- the GICP hot path on B200 (BASELINE.json metric, config C3).
+"""bench.py -- the GICP hot path on B200 (BASELINE.json metric; workload C4 by default).
 
-One STEP = one pass of the whole hot path on the C3
-scan-to-map workload: build the voxel index of the 2M-point racetrack map, fused
-kNN(k=20)+covariance of every map point, index + kNN+covariance of the 100k-point
-scan, and GICP alignment of the scan to the map to convergence (linearize on the
-GPU, LM on the host).
+Default workload (--workload c4, BASELINE.json configs[3], the north star's "batched
+scan registration" across GPUs): B = 256 scan-to-map registrations -- 32 distinct
+100k-point 3-LiDAR scans (C4 scans 0, 8, ..., 248: seeds 1000 + i at arc length
+i L / 256) x 8 initial-pose hypotheses each (the perturbations of C4 registrations
+8j .. 8j+7) -- against the shared 2M-point racetrack map, k = 20, GICP to convergence.
 
-value  = (map + scan points through kNN+covariance) / step time  [points/s], inputs
-         resident in HBM, L2 flushed (256 MiB write) before every timed step.
-e2e    = the same through the public API from pinned HOST buffers: H2D of map and
-         scan, the step, D2H of the map/scan covariances and the pose.
-roofline = the fused kNN+covariance kernel on the map: algorithmic bytes
-         (64 + 12k B/point) / its CUDA-event time.
---impl reference times the oracle (CPU, this box's cores) on a bounded sample.
+One STEP = the whole hot path for the batch:
+  A1-A3 map   voxel index + fused kNN(k=20)+covariance of every map point
+              (replicated on every rank: the map is shared),
+  (scans      one NCCL all_gather of the distinct scans' points: rank r holds its
+              32/N scans, every rank needs its chunks of every registration)
+  A1-A3 scans index + kNN(k=20)+covariance of the distinct scans (scan-sharded:
+              rank r its 32/N scans) + one NCCL all_gather of their covariances,
+  A4-A7       the 256 registrations' lockstep LM with every registration's points
+              split over the ranks by a fixed global chunking: per evaluation round
+              one batched linearisation launch, ONE NCCL all_reduce of the device
+              chunk table, the chunk-ordered combine on the device
+              (gicp_align_batched_sharded), the host LM.
+value    = registered scan points / step time (256 x 100k per step), inputs resident
+           in HBM, L2 flushed (256 MiB write) before every timed step, max over ranks.
+e2e      = the same through the public API from pinned HOST buffers (H2D of the map
+           and this rank's scans inside the timed region, D2H of the 256 poses).
+roofline = the step's dominant kernel (the batched linearisation; 80 B per source
+           point per launch); roofline_knn_cov = the map's fused
+           kNN+covariance (304 B/point at k = 20), the north star's 1-GPU target.
+--impl reference times the oracle (CPU, this box's cores) on a bounded sample of
+the same workload: one registration's seeded 2000-point subsample, its covariance
+inputs and the map cropped exactly around it, kNN+covariance + LM to convergence.
 
-Multi-GPU (torchrun): weak scaling -- every rank runs its own C3 instance (map
-replicated, its own scan seed); no data-path collective.
+--workload c3 keeps the round-1 step (one 100k scan vs the 2M map, map index +
+kNN/cov + scan + align; N > 1: replicas) for comparison.
 """
 from __future__ import annotations
 
@@ -36,11 +51,17 @@ import numpy as np  # noqa: E402
 
 K = 20
 EPS = 1e-3
-LIN_BYTES_PER_PT = 80   # linearize, per source point per iteration
+LIN_BYTES_PER_PT = 80   # linearize, per source point per launch
 MAP_CELL = 0.5          # m, ~1.15 x the 20-NN radius at 31 pts/m^2
 METRIC = "kNN+covariance points/sec (k=20) and GICP iters/sec; % HBM roofline"
-WORKLOAD = "C3 scan-to-map: 100k-point scan vs 2M-point racetrack map, k=20, GICP to convergence"
 BYTES_PER_PT = 64 + 12 * K   # kNN+cov, queries = cloud
+N_DISTINCT, N_HYP = 32, 8    # C4: 32 distinct scans x 8 initial poses = 256 registrations
+N_SCAN = 100_000
+WORKLOAD_C4 = ("C4 batched scan-to-map: 256 registrations (32 distinct 100k-point 3-LiDAR scans x 8 initial-pose "
+               "hypotheses) vs the shared 2M-point racetrack map, k=20, GICP to convergence, source points "
+               "sharded over the GPUs (NCCL chunk-table allreduce per round)")
+WORKLOAD_C3 = "C3 scan-to-map: 100k-point scan vs 2M-point racetrack map, k=20, GICP to convergence"
+REF_SUB = 2000               # oracle sample: source points of one registration
 
 
 def peaks():
@@ -108,75 +129,339 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------
+# the C4 batch (shared by both arms)
+# ------------------------------------------------------------------------------
+
+def _gen_scan(j):
+    import gen
+    sc, T, _ = gen.config_c4_scan(N_HYP * j, N_SCAN)
+    return np.ascontiguousarray(sc), T
+
+
+def c4_poses():
+    """T0 of registration b = 8j + h: scan j's T_true composed with the perturbation of
+    C4 registration b (gen.config_c4_scan's recipe), and the T_true of each scan."""
+    import gen
+    Tt, T0 = [], []
+    for j in range(N_DISTINCT):
+        u = N_HYP * j * gen.TRACK_LEN / 256.0
+        T = gen.vehicle_pose(u)
+        Tt.append(T)
+        for h in range(N_HYP):
+            b = N_HYP * j + h
+            T0.append(T @ gen.perturbation(0.5, 1.0, 1000 + b + 7))
+    return np.array(Tt), np.array(T0)
+
+
+def gen_scans(js, workers):
+    """The distinct scans js (process pool: the generator is numpy-bound)."""
+    if workers <= 1 or len(js) <= 1:
+        return [_gen_scan(j) for j in js]
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+        return list(ex.map(_gen_scan, js))
+
+
+# ------------------------------------------------------------------------------
 # reference arm: the oracle on the host cores
 # ------------------------------------------------------------------------------
 
-def run_oracle_sample(n_queries: int, seed: int = 77):
-    """kNN(k=20)+covariance of a fixed sample of map points against the FULL 2M map
-    with the oracle (brute force, all host cores). Returns (points/s, seconds)."""
+def oracle_registration_sample(seed: int):
+    """The oracle on a bounded sample of the C4 workload: registration b = 8 j + h
+    (seeded), a seeded REF_SUB-point subsample of its scan, the map cropped EXACTLY to
+    the subsample's bounding box at T0 plus 4 m (a map point outside can only be a
+    correspondence after a move of > 3 m; kept in original order), the covariance
+    inputs by the oracle's kNN(k=20)+covariance (source points against the full scan,
+    crop points against the crop + 1.5 m), then O4 to convergence. Returns
+    (points/s, seconds, iterations)."""
     import gen
     import oracle
     oracle.build()
-    _, mp, _, _ = gen.config_c3()
     rng = np.random.default_rng(seed)
-    rows = rng.choice(len(mp), n_queries, replace=False)
+    j = int(rng.integers(N_DISTINCT))
+    h = int(rng.integers(N_HYP))
+    sc, _ = _gen_scan(j)
+    _, T0s = c4_poses()
+    T0 = T0s[N_HYP * j + h]
+    mp = gen.racetrack_map(2_000_000, 1)
     t0 = time.perf_counter()
-    nbr, _ = oracle.knn(mp, mp[rows], K)
-    oracle.covariance(mp, nbr, EPS)
+    sub = np.sort(rng.choice(len(sc), REF_SUB, replace=False))
+    src = np.ascontiguousarray(sc[sub])
+    pw = src.astype(np.float64) @ T0[:3, :3].T + T0[:3, 3]
+    lo, hi = pw.min(0) - 4.0, pw.max(0) + 4.0
+    inb = np.all((mp >= lo) & (mp <= hi), axis=1)
+    inb2 = np.all((mp >= lo - 1.5) & (mp <= hi + 1.5), axis=1)
+    crop, crop2 = np.ascontiguousarray(mp[inb]), np.ascontiguousarray(mp[inb2])
+    nb_c, _ = oracle.knn(crop2, crop, K)
+    ct = oracle.covariance(crop2, nb_c, EPS)[0].astype(np.float32)
+    nb_s, _ = oracle.knn(sc, src, K)
+    cs = oracle.covariance(sc, nb_s, EPS)[0].astype(np.float32)
+    r = oracle.align(src, cs, crop, ct, T0)
     dt = time.perf_counter() - t0
-    return n_queries / dt, dt
+    return REF_SUB / dt, dt, r["iterations"]
 
 
 def reference_main(args, rank, world):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    n_q = args.ref_queries
-    vals = []
-    for _ in range(min(args.warmup, 1)):
-        run_oracle_sample(max(16, n_q // 16))
+    for w in range(min(args.warmup, 1)):
+        oracle_registration_sample(900 + w)
+    vals, secs, its = [], [], []
     for s in range(args.steps):
-        v, dt = run_oracle_sample(n_q, seed=77 + s)
+        v, dt, it = oracle_registration_sample(77 + s)
         vals.append(v)
+        secs.append(dt)
+        its.append(it)
     v = statistics.mean(vals)
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (2_100_000 / v),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "registered scan points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
         "data": "synthetic racetrack (gen/, seeded)",
-        "config": {"workload": WORKLOAD, "k": K, "map_points": 2_000_000, "scan_points": 100_000,
-                   "l2": "n/a (CPU)"},
-        "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{n_q} map points (seeded) kNN(k=20)+covariance vs the full 2M map, brute force; "
-                                   f"ms_per_step extrapolated to 2.1M points"},
-        "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": WORKLOAD_C4, "k": K, "map_points": 2_000_000, "scan_points": N_SCAN,
+                   "registrations": N_DISTINCT * N_HYP, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": v, "unit": "registered scan points/s", "cores": cores, "kind": "oracle",
+                         "sample": f"per step one seeded registration: a {REF_SUB}-point subsample of its scan, "
+                                   f"covariance inputs (oracle kNN+cov) and O4 to convergence against the map "
+                                   f"cropped exactly around it (mean {statistics.mean(its):.1f} iterations); "
+                                   f"ms_per_step is the measured time of that sample"},
+        "e2e": {"value": v, "unit": "registered scan points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------------------
-# our arm
+# our arm, C4 (default)
 # ------------------------------------------------------------------------------
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-queries", type=int, default=20000, help="oracle sample per reference step")
-    ap.add_argument("--cpu-queries", type=int, default=60000, help="oracle sample for cpu_baseline (~10 s)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
+def run_c4(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return reference_main(args, rank, world)
+    import gen
+    import paper_2308_07173_b200 as g
+    from paper_2308_07173_b200 import sharding
 
+    if N_DISTINCT % world:
+        raise SystemExit(f"--gpus must divide {N_DISTINCT}")
+    per = N_DISTINCT // world
+    mine = list(range(rank * per, (rank + 1) * per))
+    B = N_DISTINCT * N_HYP
+    # --- inputs (host generation before any CUDA work: the pool forks) ---
+    scans = gen_scans(mine, max(1, min(len(mine), (os.cpu_count() or 1) // world)))
+    mp = gen.racetrack_map(2_000_000, 1)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    T_true, T0 = c4_poses()
+    map_d = torch.from_numpy(mp).to(dev)
+    my_scans = torch.from_numpy(np.concatenate([s for s, _ in scans])).to(dev)   # [per * N_SCAN, 3]
+    all_scans = torch.empty((N_DISTINCT * N_SCAN, 3), dtype=torch.float32, device=dev)
+    cov_mine = torch.empty((per * N_SCAN, 6), dtype=torch.float32, device=dev)
+    cov_all = torch.empty((N_DISTINCT * N_SCAN, 6), dtype=torch.float32, device=dev)
+    offsets = np.arange(B + 1, dtype=np.int64) * N_SCAN
+    reg_base = (np.arange(B) // N_HYP) * N_SCAN                          # registration b -> its scan's rows
+    plan = sharding.ShardPlan(offsets, dev, num_chunks=sharding.NUM_CHUNKS, reg_base=reg_base)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(map_src, scan_src, record=None):
+        e = [ev() for _ in range(5)]
+        e[0].record(stream)
+        if world > 1:                              # every rank needs every scan's points (its chunks)
+            dist.all_gather_into_tensor(all_scans, scan_src)
+        else:
+            all_scans.copy_(scan_src)
+        imap = g.build_index(map_src, MAP_CELL)
+        _, _, cov_map = g.knn_cov_self(imap, K, EPS, with_nbr=True)
+        g.attach_cov(imap, cov_map)
+        e[1].record(stream)
+        for i in range(per):
+            sl = scan_src[i * N_SCAN:(i + 1) * N_SCAN]
+            isc = g.build_index(sl, 0.0)
+            g.knn_cov_self(isc, K, EPS, with_nbr=True, out=(None, None, cov_mine[i * N_SCAN:(i + 1) * N_SCAN]))
+            isc.free()
+        if world > 1:
+            dist.all_gather_into_tensor(cov_all, cov_mine)
+        else:
+            cov_all.copy_(cov_mine)
+        e[2].record(stream)
+        T, infos = sharding.align_batched_sharded(g, all_scans, cov_all, offsets, imap, cov_map, T0, plan=plan)
+        e[3].record(stream)
+        if record is not None:
+            record.append((e, infos, T))
+        imap.free()
+        return T, infos
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step(map_d, my_scans)
+        torch.cuda.synchronize()
+        time.sleep(0.3)
+        rec, step_ms = [], []
+        t_start = time.time()
+        for si in range(args.steps):
+            g.align_timing(si == args.steps - 1)   # per-launch events in the last timed step only
+            flush.zero_()                          # L2 flush (256 MiB > 126 MB L2), outside the timed region
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0, t1 = ev(), ev()
+            t0.record(stream)
+            step(map_d, my_scans, rec)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(t0.elapsed_time(t1))
+        lin_ms, lin_n, lin_pts = g.align_timing(False)
+        t_end = time.time()
+        time.sleep(0.15)
+    clocks = clk.summary(t_start, t_end + 0.1)
+
+    def maxr(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = maxr(statistics.mean(step_ms))
+    map_ms = statistics.mean(r[0][0].elapsed_time(r[0][1]) for r in rec)
+    scan_ms = statistics.mean(r[0][1].elapsed_time(r[0][2]) for r in rec)
+    align_ms = statistics.mean(r[0][2].elapsed_time(r[0][3]) for r in rec)
+    infos = rec[-1][1]
+    iters = sum(i.iterations for i in infos)
+    T_last = rec[-1][2]
+    errs = [float(np.linalg.norm(T_last[b][:3, 3] - T_true[b // N_HYP][:3, 3])) for b in range(B)]
+    value = B * N_SCAN / (ms * 1e-3)
+    peak, peak_kind = peaks()
+
+    # the map's kNN+cov alone (the north star's 1-GPU target), CUDA events, L2 flushed
+    imap = g.build_index(map_d, MAP_CELL)
+    kn = []
+    for _ in range(6):
+        flush.zero_()
+        a, b = ev(), ev()
+        a.record(stream)
+        g.knn_cov_self(imap, K, EPS, with_nbr=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        kn.append(a.elapsed_time(b))
+    imap.free()
+    knn_ms = statistics.median(kn[1:])
+    knn_ach = mp.shape[0] * BYTES_PER_PT / (knn_ms * 1e-3) / 1e9
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+    roof_knn = {"bound": "hbm", "achieved": knn_ach, "peak": peak, "unit": "GB/s", "frac": knn_ach / peak,
+                "traffic": traffic.get("k_knn_self_map_bytes_per_launch"), "peak_kind": peak_kind,
+                "kernel": "gicp_knn_cov_self on the 2M map (tiled stage + per-query fallback, escalation, exact)",
+                "bytes_per_point": BYTES_PER_PT, "ms": knn_ms,
+                "timed": "alone, CUDA events around the call, L2 flushed, median of 5"}
+    # the batched linearisation: algorithmic bytes of the launches' active points
+    lin_all_ms = sum(lin_ms)
+    roof_lin = None
+    if lin_n[0]:
+        ach = LIN_BYTES_PER_PT * lin_pts[0] / (lin_ms[0] * 1e-3) / 1e9
+        roof_lin = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": traffic.get("k_linearize_batched_bytes_per_launch"), "peak_kind": peak_kind,
+                    "kernel": "k_linearize (batched speculative dual launch, gicp_align_batched_sharded)",
+                    "bytes_per_point": LIN_BYTES_PER_PT, "points_per_launch": lin_pts[0] / lin_n[0],
+                    "launch_ms": lin_ms[0] / lin_n[0], "launches_per_step": sum(lin_n),
+                    "linearize_ms_per_step": lin_all_ms,
+                    "timed": "CUDA events around every linearisation launch of the last timed step"}
+
+    # --- launches per step (CUPTI via torch.profiler, one extra untimed step) ---
+    gpu_launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(map_d, my_scans)
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        ours = [n for n in names if ("gicp" in n or "cub" in n.lower())]
+        gpu_launches = len(ours) * args.steps
+    except Exception:
+        gpu_launches = None
+
+    # --- e2e: the same step through the public API from pinned host buffers ---
+    e2e = None
+    if not args.no_e2e:
+        map_h = torch.from_numpy(mp).pin_memory()
+        scan_h = my_scans.cpu().pin_memory()
+        pose_h = torch.empty((B, 16), dtype=torch.float64).pin_memory()
+        em = []
+        for it in range(max(2, args.steps // 4) + 1):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            md = map_h.to(dev, non_blocking=True)
+            sd = scan_h.to(dev, non_blocking=True)
+            T, _ = step(md, sd)
+            pose_h.copy_(torch.from_numpy(np.asarray(T).reshape(B, 16)))   # the poses come back to the host
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it > 0:
+                em.append(a.elapsed_time(b))
+        e2e_ms = maxr(statistics.mean(em))
+        e2e = {"value": B * N_SCAN / (e2e_ms * 1e-3), "unit": "registered scan points/s",
+               "h2d_bytes_per_step": int(mp.nbytes + scan_h.numel() * 4), "d2h_bytes_per_step": int(B * 16 * 8),
+               "ms_per_step": e2e_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, it = oracle_registration_sample(77)
+        cpu = {"value": v, "unit": "registered scan points/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"one seeded registration: a {REF_SUB}-point subsample, its covariance inputs (oracle "
+                         f"kNN+cov) and O4 to convergence ({it} iterations) against the map cropped exactly "
+                         f"around it, {dt:.1f} s"}
+
+    if rank == 0:
+        dominant = roof_lin if (roof_lin is not None and lin_all_ms >= knn_ms) else roof_knn
+        line = {
+            "metric": METRIC, "value": value, "unit": "registered scan points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (kNN/cov, per-point terms), f64 (transform, reductions, LM)",
+            "data": "synthetic racetrack (gen/, seeded): 2M-point map, 32 distinct 100k-point 3-LiDAR scans",
+            "config": {"workload": WORKLOAD_C4, "k": K, "map_points": int(mp.shape[0]), "scan_points": N_SCAN,
+                       "registrations": B, "distinct_scans": N_DISTINCT, "map_cell_m": MAP_CELL,
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"points of every registration sharded over {world} GPU(s) "
+                                      f"({sharding.NUM_CHUNKS} fixed chunks, NCCL chunk-table allreduce per round); "
+                                      f"distinct scans sharded for kNN+cov (NCCL all_gather); map replicated"},
+            "gicp_iters_per_s": iters / (align_ms * 1e-3),
+            "knn_cov_points_per_s": mp.shape[0] / (knn_ms * 1e-3),
+            "breakdown_ms": {"map_index_knn_cov": map_ms, "scan_index_knn_cov_allgather": scan_ms,
+                             "batched_align": align_ms, "iterations_total": iters,
+                             "iterations_mean": iters / B},
+            "align_translation_error_m": {"median": float(np.median(errs)), "max": float(np.max(errs))},
+            "roofline": dominant,
+            "roofline_knn_cov": roof_knn,
+            "roofline_linearize": roof_lin,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------------------
+# our arm, C3 (round 1's step; --workload c3)
+# ------------------------------------------------------------------------------
+
+def run_c3(args, rank, world, local):
     import torch
     import torch.distributed as dist
 
@@ -187,32 +472,16 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    # --- inputs (resident in HBM) ---
-    scan_seed = 1000 + rank
-    sc, mp, T_true, T0 = gen.config_c3(scan_seed=scan_seed)
-    map_d = torch.from_numpy(mp).to(dev)
-    scan_d = torch.from_numpy(sc).to(dev)
+    sc, mp, T_true, T0 = gen.config_c3(scan_seed=1000 + rank)
+    map_d = torch.from_numpy(np.array(mp)).to(dev)
+    scan_d = torch.from_numpy(np.array(sc)).to(dev)
     n_pts = mp.shape[0] + sc.shape[0]
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
-    # the scan's path (index + kNN/covariances, latency-bound small grids) runs on a
-    # high-priority side stream inside the map's kNN (throughput-bound, 15.6k blocks):
-    # its blocks take SM slots as the map's retire, so it costs its share of the
-    # machine, not its latency. The alignment joins both.
     sb = torch.cuda.Stream(device=dev, priority=-1)
-    # BENCH_SCAN_THREAD=1 (default): a host worker thread issues the scan's path from
-    # the step's start, so its index build (host-synchronising: bbox, level counts)
-    # overlaps the map's index build instead of following it. The library's host
-    # state is thread-local and its allocations stream-ordered; ctypes drops the GIL.
-    scan_thread = os.environ.get("BENCH_SCAN_THREAD", "1") == "1"
-    pool = None
-    if scan_thread:
-        from concurrent.futures import ThreadPoolExecutor
-        pool = ThreadPoolExecutor(max_workers=1, initializer=lambda: torch.cuda.set_device(local))
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=1, initializer=lambda: torch.cuda.set_device(local))
 
     def scan_path(e, after):
         sb.wait_event(after)
@@ -226,13 +495,13 @@ def main():
     def step(record=None):
         e = [ev() for _ in range(6)]
         e[0].record(stream)
-        fut = pool.submit(scan_path, e, e[0]) if scan_thread else None
+        fut = pool.submit(scan_path, e, e[0])
         imap = g.build_index(map_d, MAP_CELL)
         e[1].record(stream)
         _, _, cov_map = g.knn_cov_self(imap, K, EPS, with_nbr=True)
         g.attach_cov(imap, cov_map)
         e[2].record(stream)
-        iscan, cov_scan = fut.result() if scan_thread else scan_path(e, e[1])
+        iscan, cov_scan = fut.result()
         stream.wait_stream(sb)
         cov_scan.record_stream(stream)
         T, info = g.align(scan_d, cov_scan, imap, cov_map, T0)
@@ -243,25 +512,20 @@ def main():
         iscan.free()
         return T, info
 
-    # warm-up (the clock sampler starts first: nvidia-smi needs ~0.1-0.5 s to come up)
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
         time.sleep(0.3)
-        rec = []
-        step_ms = []
+        rec, step_ms = [], []
         t_start = time.time()
         for si in range(args.steps):
-            # per-launch CUDA events around gicp_align's linearisations during the last
-            # timed step only (the event records would otherwise add ~4 % to every step)
             g.align_timing(si == args.steps - 1)
-            flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the timed region
+            flush.zero_()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            t0 = ev()
-            t1 = ev()
+            t0, t1 = ev(), ev()
             t0.record(stream)
             step(rec)
             t1.record(stream)
@@ -271,7 +535,6 @@ def main():
         t_end = time.time()
         time.sleep(0.15)
     clocks = clk.summary(t_start, t_end + 0.1)
-
     ms = statistics.mean(step_ms)
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -279,154 +542,64 @@ def main():
         ms = float(t.item())
     build_ms = statistics.mean(r[0][0].elapsed_time(r[0][1]) for r in rec)
     knncov_ms = statistics.mean(r[0][1].elapsed_time(r[0][2]) for r in rec)
-    # the scan path overlaps the map's index build and kNN: scan_ms from its own start
-    # to its own end; align from the later of the two ends
     scan_ms = statistics.mean(r[0][5].elapsed_time(r[0][3]) for r in rec)
     align_ms = statistics.mean(r[0][0].elapsed_time(r[0][4]) - max(r[0][0].elapsed_time(r[0][2]),
                                                                     r[0][0].elapsed_time(r[0][3])) for r in rec)
     iters = statistics.mean(r[1].iterations for r in rec)
-    T_last = rec[-1][2]
-    dt_err = float(np.linalg.norm(T_last[:3, 3] - T_true[:3, 3]))
-
-    value = world * n_pts / (ms * 1e-3)
     peak, peak_kind = peaks()
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
     achieved = mp.shape[0] * BYTES_PER_PT / (knncov_ms * 1e-3) / 1e9
-    # the linearisation (the step's largest kernel share: 26 launches per step):
-    # algorithmic bytes per source point per launch = 12 xyz + 24 cov
-    # + 40 target float4 + cov + 4 corr = 80 B; average launch time from the events
-    lin_bytes = LIN_BYTES_PER_PT * lin_pts
-    lin_launch_ms = lin_ms[0] / max(lin_n[0], 1)
-    lin_achieved = lin_bytes / (lin_launch_ms * 1e-3) / 1e9 if lin_n[0] else None
-    lin_step_ms = sum(lin_ms)  # one step's worth (the last timed step)
-    lin_traffic = None
-    if os.path.exists(tp):
-        try:
-            lin_traffic = json.load(open(tp)).get("k_linearize_dual_bytes_per_launch")
-        except Exception:
-            lin_traffic = None
-    traffic = None
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("k_knn_self_map_bytes_per_launch")
-        except Exception:
-            traffic = None
-
-    # --- launches per step (CUPTI via torch.profiler, one extra untimed step) ---
-    gpu_launches = None
-    try:
-        from torch.profiler import ProfilerActivity, profile
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            step()
-            torch.cuda.synchronize()
-        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
-        ours = [n for n in names if ("gicp" in n or "cub" in n.lower())]
-        gpu_launches = len(ours) * args.steps
-    except Exception:
-        gpu_launches = None
-
-    # --- e2e through the public API from pinned host buffers ---
-    e2e = None
-    if not args.no_e2e:
-        map_h = torch.from_numpy(mp).pin_memory()
-        scan_h = torch.from_numpy(sc).pin_memory()
-        cov_map_h = torch.empty((mp.shape[0], 6), dtype=torch.float32).pin_memory()
-        cov_scan_h = torch.empty((sc.shape[0], 6), dtype=torch.float32).pin_memory()
-        e2e_ms = []
-        # transfers overlap the compute on a copy stream: the scan goes up first and
-        # its index + kNN/covariances run while the map uploads; the map covariances'
-        # download overlaps the alignment. Both are non-default streams (the legacy
-        # default stream would serialise them).
-        cp = torch.cuda.Stream(device=dev)
-        es = torch.cuda.Stream(device=dev)
-        for it in range(args.steps + 1):
-            flush.zero_()
-            torch.cuda.synchronize()
-            with torch.cuda.stream(es):
-                a, b = ev(), ev()
-                a.record(es)
-                cp.wait_stream(es)
-                sd = scan_h.to(dev, non_blocking=True)
-                with torch.cuda.stream(cp):
-                    md = map_h.to(dev, non_blocking=True)
-                    up = torch.cuda.Event()
-                    up.record(cp)
-                iscan = g.build_index(sd, 0.0)
-                _, _, cs = g.knn_cov_self(iscan, K, EPS, with_nbr=True)
-                es.wait_event(up)  # the map's upload
-                md.record_stream(es)
-                imap = g.build_index(md, MAP_CELL)
-                _, _, cm = g.knn_cov_self(imap, K, EPS, with_nbr=True)
-                g.attach_cov(imap, cm)
-                cp.wait_stream(es)
-                with torch.cuda.stream(cp):
-                    cov_map_h.copy_(cm, non_blocking=True)
-                T, info = g.align(sd, cs, imap, cm, T0)
-                cov_scan_h.copy_(cs, non_blocking=True)
-                es.wait_stream(cp)
-                b.record(es)
-            torch.cuda.synchronize()
-            imap.free()
-            iscan.free()
-            if it > 0:
-                e2e_ms.append(a.elapsed_time(b))
-        em = statistics.mean(e2e_ms)
-        if world > 1:
-            t = torch.tensor([em], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            em = float(t.item())
-        e2e = {"value": world * n_pts / (em * 1e-3), "unit": "points/s",
-               "h2d_bytes_per_step": int(mp.nbytes + sc.nbytes),
-               "d2h_bytes_per_step": int(cov_map_h.numel() * 4 + cov_scan_h.numel() * 4 + 16 * 8),
-               "ms_per_step": em}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt = run_oracle_sample(args.cpu_queries)
-        cpu = {"value": v, "unit": "points/s", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"{args.cpu_queries} seeded map points, kNN(k=20)+covariance vs the full 2M map "
-                         f"(brute force), {dt:.1f} s"}
-
-    roof_knn = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_kind": peak_kind, "kernel": "k_knn_self (fused kNN+cov, map: level, escalate, exact)",
-                "bytes_per_point": BYTES_PER_PT, "ms_per_step": knncov_ms}
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_kind": peak_kind, "kernel": "gicp_knn_cov_self on the 2M map (in the step)",
+            "bytes_per_point": BYTES_PER_PT, "ms_per_step": knncov_ms}
     roof_lin = None
-    if lin_achieved is not None:
-        roof_lin = {"bound": "hbm", "achieved": lin_achieved, "peak": peak, "unit": "GB/s",
-                    "frac": lin_achieved / peak, "traffic": lin_traffic, "peak_kind": peak_kind,
-                    "kernel": "k_linearize (speculative dual launch inside gicp_align)",
-                    "bytes_per_point": LIN_BYTES_PER_PT, "points": lin_pts, "launch_ms": lin_launch_ms,
-                    "launches_per_step": sum(lin_n), "ms_per_step": lin_step_ms,
-                    "timed": "CUDA events around every linearisation launch of the last timed step"}
+    if lin_n[0]:
+        ach = LIN_BYTES_PER_PT * lin_pts[0] / (lin_ms[0] * 1e-3) / 1e9
+        roof_lin = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": None, "peak_kind": peak_kind, "kernel": "k_linearize (speculative dual launch)",
+                    "bytes_per_point": LIN_BYTES_PER_PT, "launch_ms": lin_ms[0] / lin_n[0],
+                    "launches_per_step": sum(lin_n), "ms_per_step": sum(lin_ms)}
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 (kNN/cov), f64 (transform, reductions, LM)",
+            "metric": METRIC, "value": world * n_pts / (ms * 1e-3), "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (kNN/cov), f64 (transform, reductions, LM)",
             "data": "synthetic racetrack (gen/, seeded): 2M-point map, 100k-point 3-LiDAR scan",
-            "config": {"workload": WORKLOAD, "k": K, "map_points": int(mp.shape[0]),
+            "config": {"workload": WORKLOAD_C3, "k": K, "map_points": int(mp.shape[0]),
                        "scan_points": int(sc.shape[0]), "map_cell_m": MAP_CELL,
-                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas x{world}",
-                       "scan_issue": "host worker thread" if scan_thread else "main thread"},
+                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas x{world}"},
             "gicp_iters_per_s": iters / (align_ms * 1e-3),
-            "breakdown_ms": {"map_index_build": build_ms, "map_knn_cov": knncov_ms,
-                             "scan_index_knn_cov": scan_ms, "align": align_ms, "align_iterations": iters},
-            "knn_cov_kernel_pts_per_s": mp.shape[0] / (knncov_ms * 1e-3),
-            "align_translation_error_m": dt_err,
-            # the kernel with the largest share of the step (per-step device time)
-            "roofline": (roof_knn if knncov_ms >= lin_step_ms or lin_achieved is None else roof_lin),
-            "roofline_knn_cov": roof_knn,
-            "roofline_linearize": roof_lin,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": gpu_launches,
-            "clocks": clocks,
+            "breakdown_ms": {"map_index_build": build_ms, "map_knn_cov": knncov_ms, "scan_index_knn_cov": scan_ms,
+                             "align": align_ms, "align_iterations": iters},
+            "align_translation_error_m": float(np.linalg.norm(rec[-1][2][:3, 3] - T_true[:3, 3])),
+            "roofline": roof if (roof_lin is None or knncov_ms >= sum(lin_ms)) else roof_lin,
+            "roofline_knn_cov": roof, "roofline_linearize": roof_lin, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_main(args, rank, world)
+    if args.workload == "c3":
+        return run_c3(args, rank, world, local)
+    return run_c4(args, rank, world, local)
 
 
 if __name__ == "__main__":

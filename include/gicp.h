@@ -404,11 +404,12 @@ void gicp_submap_free(gicp_submap sm);
 
 
 /* gicp_align_timing -- opt-in diagnostics (bench.py's roofline): while enabled,
- * gicp_align records CUDA events on its stream around every linearisation launch
- * of the calling thread. The call returns the accumulated device milliseconds and
- * launch counts per kind ([0] speculative dual launches, [1] full linearisations,
- * [2] trial costs) and the source size of the last one, resets them, and sets the
- * enable flag. Host pointers, nullable. */
+ * gicp_align and the batched aligns record CUDA events on their stream around every
+ * linearisation launch of the calling thread. The call returns, per kind ([0]
+ * speculative dual launches, [1] full linearisations, [2] trial costs), the
+ * accumulated device milliseconds, launch counts and source points linearised
+ * (active registrations' points, summed over the launches), resets them, and sets
+ * the enable flag. Host pointers ([3] each), nullable. */
 int gicp_align_timing(int enable, double* ms, int64_t* launches, int64_t* points);
 
 #ifdef __cplusplus

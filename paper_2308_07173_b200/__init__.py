@@ -526,14 +526,15 @@ class Submap:
 
 
 def align_timing(enable: bool = True):
-    """Per-launch device timing of gicp_align's linearisations on this thread:
-    returns (ms [dual, full, trial], launches [dual, full, trial], points) accumulated
-    since the previous call, resets them and sets the enable flag."""
+    """Per-launch device timing of the aligns' linearisations on this thread: returns
+    (ms, launches, points), each [dual, full, trial], accumulated since the previous
+    call (points: source points linearised, summed over the launches), resets them
+    and sets the enable flag."""
     ms = (ctypes.c_double * 3)()
     n = (ctypes.c_int64 * 3)()
-    pts = ctypes.c_int64(0)
-    _check(_lib.gicp_align_timing(int(bool(enable)), ctypes.cast(ms, _P), ctypes.cast(n, _P), ctypes.byref(pts)))
-    return list(ms), list(n), int(pts.value)
+    pts = (ctypes.c_int64 * 3)()
+    _check(_lib.gicp_align_timing(int(bool(enable)), ctypes.cast(ms, _P), ctypes.cast(n, _P), ctypes.cast(pts, _P)))
+    return list(ms), list(n), list(pts)
 
 
 def version() -> int:

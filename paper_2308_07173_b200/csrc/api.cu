@@ -196,14 +196,15 @@ int wait_mapped(MappedOut* m, unsigned seq, cudaStream_t s) {
 // the launching stream): [0] speculative dual launches, [1] full linearisations,
 // [2] trial costs. gicp_align_timing() enables / reads / resets it.
 struct KernelTiming {
-    static constexpr int kCap = 256;  // launches timed per gicp_align call
+    static constexpr int kCap = 2048;  // launches timed per call (batched aligns: up to ~10 per iteration)
     int on = 0;
     cudaEvent_t e[2 * kCap] = {};
     int kind[kCap] = {};
+    int64_t lpts[kCap] = {};  // source points the launch linearised (active registrations)
     int used = 0;  // event pairs recorded by the current call
     double ms[3] = {0, 0, 0};
     int64_t n[3] = {0, 0, 0};
-    int64_t points = 0;
+    int64_t pts[3] = {0, 0, 0};
 };
 KernelTiming& kernel_timing() {
     static thread_local KernelTiming t;
@@ -216,6 +217,7 @@ void kernel_timing_collect(KernelTiming& t) {
         if (cudaEventElapsedTime(&m, t.e[2 * i], t.e[2 * i + 1]) == cudaSuccess) {
             t.ms[t.kind[i]] += m;
             t.n[t.kind[i]] += 1;
+            t.pts[t.kind[i]] += t.lpts[i];
         }
     }
     cudaGetLastError();
@@ -513,8 +515,8 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         const auto h1 = std::chrono::steady_clock::now();
         if (timed) {
             cudaEventRecord(kt.e[2 * kt.used + 1], s);
+            kt.lpts[kt.used] = ns;
             kt.kind[kt.used++] = (old != nullptr) ? 0 : ((flags & GICP_LIN_ERROR_ONLY) ? 2 : 1);
-            kt.points = ns;
         }
         if (!rc) rc = wait_mapped(mo, ls.seq, s);
         if (host_trace) {
@@ -889,7 +891,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     char* ex = nullptr;
     // + the correspondence certificates paired with the two buffers (R27)
     const bool certs = GICP_ALIGN_CACHE && getenv("GICP_ALIGN_NOCACHE") == nullptr;
-    const size_t dev_extra = ds ? (size_t)std::max(E, 1) * (32 * sizeof(double) + sizeof(int)) + 64 : 0;
+    const size_t dev_extra = ds ? (size_t)std::max(E, 1) * (32 * sizeof(double) + sizeof(int)) + 512 : 0;
     if ((rc = batch_scratch(offsets, E,
                             2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
                                 (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + dev_extra,
@@ -951,7 +953,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         st[b].piv[0] = st[b].T[3];
         st[b].piv[1] = st[b].T[7];
         st[b].piv[2] = st[b].T[11];
-        if (!reduce && !entry_reg && offsets[b + 1] == offsets[b]) {  // no points: no correspondences
+        if (!reduce && !ds && !entry_reg && offsets[b + 1] == offsets[b]) {  // no points: no correspondences
             st[b].done = 1;
             st[b].rc = GICP_EDEGENERATE;
         }
@@ -989,8 +991,19 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             bs.ls.seq = ++seq;
             LinScratch lsr = bs.ls;
             if (ds) lsr.flag = nullptr;  // the combine kernel signals
+            KernelTiming& kt = kernel_timing();
+            const bool timed = kt.on && kt.used < KernelTiming::kCap;
+            if (timed) cudaEventRecord(kt.e[2 * kt.used], s);
             r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags,
                                       ds ? Ed : Hd, corrA, s, lsr, corrB, bv, bs.nb);
+            if (timed) {
+                cudaEventRecord(kt.e[2 * kt.used + 1], s);
+                int64_t ap = 0;
+                for (int e = 0; e < E; ++e)
+                    if (pst[e].active) ap += offsets[e + 1] - offsets[e];
+                kt.lpts[kt.used] = ap;
+                kt.kind[kt.used++] = (flags & kLinDual) ? 0 : ((flags & GICP_LIN_ERROR_ONLY) ? 2 : 1);
+            }
             if (!r && !ds) r = wait_mapped(&mo, bs.ls.seq, s);
             if (r) return r;
         }
@@ -1175,6 +1188,13 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         }
     }
     cudaFreeAsync(bs.base, s);
+    {
+        KernelTiming& kt = kernel_timing();
+        if (kt.used) {
+            cudaStreamSynchronize(s);
+            kernel_timing_collect(kt);
+        }
+    }
     int any_degenerate = 0;
     for (int b = 0; b < B; ++b) {
         std::memcpy(res[b].T, st[b].T, sizeof(res[b].T));
@@ -1380,16 +1400,18 @@ GICP_API int gicp_cluster(const float* xyz, int64_t n, float tol, int min_size, 
 
 // ---- diagnostics ----------------------------------------------------------------
 GICP_API int gicp_align_timing(int enable, double* ms /* host [3] or NULL */, int64_t* launches /* host [3] */,
-                               int64_t* points) {
+                               int64_t* points /* host [3] */) {
     KernelTiming& t = kernel_timing();
     if (ms)
         for (int k = 0; k < 3; ++k) ms[k] = t.ms[k];
     if (launches)
         for (int k = 0; k < 3; ++k) launches[k] = t.n[k];
-    if (points) *points = t.points;
+    if (points)
+        for (int k = 0; k < 3; ++k) points[k] = t.pts[k];
     for (int k = 0; k < 3; ++k) {
         t.ms[k] = 0.0;
         t.n[k] = 0;
+        t.pts[k] = 0;
     }
     if (enable && !t.e[0]) {
         for (auto& ev : t.e)

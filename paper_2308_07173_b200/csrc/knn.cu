@@ -566,13 +566,20 @@ bool launch_tile(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float*
                  int* listA, int* listB, int2* exact, cudaStream_t s) {
     static const bool off = getenv("GICP_KNN_TILE") && atoi(getenv("GICP_KNN_TILE")) == 0;
     if (off || idx->tiles1 == nullptr || idx->tile_of == nullptr || idx->n == 0 || (k != 10 && k != 20)) return false;
+    // the staged boxes pay off on dense, even clouds (the C3 map: ~35 points per
+    // level-1 voxel); sparse, uneven ones (a scan's 1/r^2 falloff) run per query
+    if (idx->n < 24 * idx->n_tiles1) return false;
     const unsigned grid = (unsigned)((idx->n + kTB - 1) / kTB);
-    if (k == 20)
-        k_knn_tile<20><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, idx->n, eps, nbr, d2, cov,
-                                            counts + 2, listA, counts + 0, exact, counts + 3, listB);
-    else
-        k_knn_tile<10><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, idx->n, eps, nbr, d2, cov,
-                                            counts + 2, listA, counts + 0, exact, counts + 3, listB);
+    static const bool rows = !(getenv("GICP_KNN_ROWS") && atoi(getenv("GICP_KNN_ROWS")) == 0);
+#define GICP_TILE_LAUNCH(KK, RR)                                                                                  \
+    k_knn_tile<KK, RR><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, idx->n, eps, nbr, d2, \
+                                            cov, counts + 2, listA, counts + 0, exact, counts + 3, listB)
+    if (k == 20) {
+        if (rows) GICP_TILE_LAUNCH(20, true); else GICP_TILE_LAUNCH(20, false);
+    } else {
+        if (rows) GICP_TILE_LAUNCH(10, true); else GICP_TILE_LAUNCH(10, false);
+    }
+#undef GICP_TILE_LAUNCH
     return true;
 }
 

@@ -121,7 +121,11 @@ __device__ __forceinline__ bool exact_less(const float4& q, const float4& a, con
 #ifndef GICP_TILE_MINB
 #define GICP_TILE_MINB 1
 #endif
-template <int K>
+// ROWS: each lane scans only the 27 voxels around its own (nine x-rows of three
+// voxels of the box, staged in (z, y, x) order so every row is contiguous) and the
+// stop rule uses that cube; the block's lanes are regrouped by the parity of their
+// voxel (the same relative rows), so a warp's lanes step through the same rows.
+template <int K, bool ROWS>
 __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* __restrict__ pts, Grid g0,
                                                   const int* __restrict__ tiles, const int* __restrict__ tile_of,
                                                   int64_t n, float eps, int32_t* __restrict__ nbr,
@@ -130,9 +134,12 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
                                                   int* __restrict__ exact_count, int2* __restrict__ exact_list,
                                                   int* __restrict__ fb_count, int* __restrict__ fb_list) {
     constexpr int NL = K + 1;
-    __shared__ __align__(128) float4 cand[kBlkCap + kTileCap];
+    __shared__ __align__(128) float4 cand[kBlkCap + kTileCap + 4];
     __shared__ unsigned buf[kTileBuf][kTB];
-    __shared__ int2 rng[kBlkTiles][57];
+    constexpr int NR = ROWS ? 64 : 57;  // staged ranges per tile
+    __shared__ int2 rng[kBlkTiles][NR];
+    __shared__ int cell_off[ROWS ? kBlkTiles : 1][65];  // ROWS: box cell starts in cand, then the end
+    __shared__ int s_order[ROWS ? kTB : 1], s_pc[8];
     __shared__ int t_off[kBlkTiles], t_cnt[kBlkTiles], t_start[kBlkTiles], t_base[kBlkTiles][3];
     __shared__ __align__(8) unsigned long long bar;
     __shared__ int s_ta, s_nt, s_ok;
@@ -161,20 +168,31 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
         const int bx = cell_coord(f0.x, g0.ox, g0.inv_cell) & ~1;
         const int by = cell_coord(f0.y, g0.oy, g0.inv_cell) & ~1;
         const int bz = cell_coord(f0.z, g0.oz, g0.inv_cell) & ~1;
-        const signed char* d = c_outer.d[lane];
-        const int2 ra = cell_lookup(g0, bx + d[0], by + d[1], bz + d[2]);
-        int2 rb = make_int2(0, 0);
-        if (lane < 24) {
-            const signed char* e = c_outer.d[lane + 32];
-            rb = cell_lookup(g0, bx + e[0], by + e[1], bz + e[2]);
+        int2 ra, rb = make_int2(0, 0);
+        if constexpr (ROWS) {  // box cell ci = (z * 4 + y) * 4 + x, offsets -1..2 per axis
+            ra = cell_lookup(g0, bx - 1 + (lane & 3), by - 1 + ((lane >> 2) & 3), bz - 1 + (lane >> 4));
+            const int c2 = lane + 32;
+            rb = cell_lookup(g0, bx - 1 + (c2 & 3), by - 1 + ((c2 >> 2) & 3), bz - 1 + (c2 >> 4));
+        } else {
+            const signed char* d = c_outer.d[lane];
+            ra = cell_lookup(g0, bx + d[0], by + d[1], bz + d[2]);
+            if (lane < 24) {
+                const signed char* e = c_outer.d[lane + 32];
+                rb = cell_lookup(g0, bx + e[0], by + e[1], bz + e[2]);
+            }
         }
         const int ca = max(ra.y - ra.x, 0), cb = max(rb.y - rb.x, 0);
-        rng[lt][1 + lane] = make_int2(ra.x, ca);
-        if (lane < 24) rng[lt][33 + lane] = make_int2(rb.x, cb);
+        if constexpr (ROWS) {
+            rng[lt][lane] = make_int2(ra.x, ca);
+            rng[lt][32 + lane] = make_int2(rb.x, cb);
+        } else {
+            rng[lt][1 + lane] = make_int2(ra.x, ca);
+            if (lane < 24) rng[lt][33 + lane] = make_int2(rb.x, cb);
+        }
         const int tot = __reduce_add_sync(0xffffffffu, ca + cb);
         if (lane == 0) {
-            rng[lt][0] = make_int2(s1, e1 - s1);
-            t_cnt[lt] = e1 - s1 + tot;
+            if (!ROWS) rng[lt][0] = make_int2(s1, e1 - s1);
+            t_cnt[lt] = (ROWS ? 0 : e1 - s1) + tot;
             t_start[lt] = s1;
             t_base[lt][0] = bx;
             t_base[lt][1] = by;
@@ -201,7 +219,7 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
     // (2) one TMA bulk copy per non-empty range, completion on the block's barrier
     for (int lt = warp; lt < nt; lt += kTB / 32) {
         const int2 a = rng[lt][lane];
-        const int2 b = lane + 32 < 57 ? rng[lt][lane + 32] : make_int2(0, 0);
+        const int2 b = lane + 32 < NR ? rng[lt][lane + 32] : make_int2(0, 0);
         int ia = a.y, ib = b.y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -215,19 +233,96 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
         const int oa = t_off[lt] + ia - a.y, ob = t_off[lt] + tot_a + ib - b.y;
         if (a.y > 0) bulk_g2s(cand + oa, pts + a.x, (unsigned)a.y * 16u, &bar);
         if (b.y > 0) bulk_g2s(cand + ob, pts + b.x, (unsigned)b.y * 16u, &bar);
+        if (ROWS) {
+            cell_off[lt][lane] = oa;
+            cell_off[lt][32 + lane] = ob;
+            if (lane == 31) cell_off[lt][64] = ob + b.y;
+        }
+    }
+    if (ROWS) {
+        // regroup the block's queries by the parity of their voxel (which of the
+        // tile's 2x2x2 voxels): lanes of one group scan the same relative rows
+        if (tid < 8) s_pc[tid] = 0;
+        __syncthreads();
+        int par = 0, rk = 0;
+        if (act) {
+            const float4 pq = __ldg(pts + q);
+            par = (cell_coord(pq.x, g0.ox, g0.inv_cell) & 1) | ((cell_coord(pq.y, g0.oy, g0.inv_cell) & 1) << 1) |
+                  ((cell_coord(pq.z, g0.oz, g0.inv_cell) & 1) << 2);
+            rk = atomicAdd(&s_pc[par], 1);
+        }
+        __syncthreads();
+        if (act) {
+            int b0 = 0;
+            for (int i = 0; i < par; ++i) b0 += s_pc[i];
+            s_order[b0 + rk] = tid;
+        }
+        __syncthreads();
     }
     mbar_wait(&bar, 0);
     // (3) per lane: its query and its tile's staged box
     int lt = 0, base = 0, C = 0;
     float4 qp = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (act) {
-        lt = __ldg(tile_of + q) - ta;
+    const int nq = (int)min((int64_t)kTB, n - q0);
+    const int me = ROWS ? (tid < nq ? s_order[tid] : tid) : tid;  // the lane's query (block-relative)
+    const int64_t qq = q0 + me;
+    const bool on = ROWS ? tid < nq : act;
+    if (on) {
+        lt = __ldg(tile_of + qq) - ta;
         base = t_off[lt];
         C = t_cnt[lt];
-        qp = cand[base + (int)(q - t_start[lt])];
+        qp = ROWS ? __ldg(pts + qq) : cand[base + (int)(qq - t_start[lt])];
     }
     unsigned T[NL];
-    {
+    unsigned* col = &buf[0][tid];
+    int nb = 0;
+    if constexpr (ROWS) {
+#pragma unroll
+        for (int i = 0; i < NL; ++i) T[i] = 0xffffffffu;
+        unsigned thr = 0xffffffffu;
+        int ix = 0, iy = 0, iz = 0;
+        if (on) {
+            ix = cell_coord(qp.x, g0.ox, g0.inv_cell) - t_base[lt][0] + 1;
+            iy = cell_coord(qp.y, g0.oy, g0.inv_cell) - t_base[lt][1] + 1;
+            iz = cell_coord(qp.z, g0.oz, g0.inv_cell) - t_base[lt][2] + 1;
+        }
+        // the nine rows (dz, dy), nearest first; each covers x = ix-1 .. ix+1
+        constexpr signed char kRow[9][2] = {{0, 0}, {0, -1}, {0, 1}, {-1, 0}, {1, 0},
+                                            {-1, -1}, {-1, 1}, {1, -1}, {1, 1}};
+#pragma unroll 1
+        for (int r = 0; r < 9; ++r) {
+            int a = 0, len = 0;
+            if (on) {
+                const int ci = ((iz + kRow[r][0]) * 4 + (iy + kRow[r][1])) * 4 + ix - 1;
+                a = cell_off[lt][ci];
+                len = cell_off[lt][ci + 3] - a;
+            }
+            const int rel = a - base;  // slot of the row's first point within the tile
+            const int lmax = __reduce_max_sync(0xffffffffu, len);
+            for (int c = 0; c < lmax; c += 4) {
+                unsigned kk[4];
+                bool ps[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = c + u;
+                    const float4 p = cand[a + cc];  // past len: padding or other points (masked below)
+                    const float dd = dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z);
+                    ps[u] = cc < len && __float_as_uint(dd) <= thr;
+                    kk[u] = pack_key(dd, rel + cc);
+                }
+                if (__any_sync(0xffffffffu, ps[0] | ps[1] | ps[2] | ps[3])) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (ps[u]) col[(nb++) * kTB] = kk[u];
+                    if (__any_sync(0xffffffffu, nb >= kTileBuf - 4)) {
+                        tile_merge<NL>(T, col, nb);
+                        nb = 0;
+                        thr = T[NL - 1] | kSlotMask;
+                    }
+                }
+            }
+        }
+    } else {
         constexpr net::Net sn = net::make_sort_net<kTileFirst, NL>();
         unsigned v[kTileFirst];
 #pragma unroll
@@ -241,9 +336,6 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
         GICP_APPLY_NET(v, sn);
 #pragma unroll
         for (int i = 0; i < NL; ++i) T[i] = v[sn.out[i]];
-    }
-    unsigned* col = &buf[0][tid];
-    int nb = 0;
     unsigned thr = T[NL - 1] | kSlotMask;
     const int cmax = __reduce_max_sync(0xffffffffu, C);
     for (int c = kTileFirst; c < cmax; c += 4) {
@@ -268,43 +360,112 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
             }
         }
     }
+    }  // ROWS
     if (__any_sync(0xffffffffu, nb > 0)) tile_merge<NL>(T, col, nb);
-    // (4) decisions: enough candidates, stop rule on the box, order certainty
+    // (4) order certainty. (a) Boundary near-tie: the K-th and (K+1)-th keys share
+    // their d2 prefix U, so candidates with prefix U (some maybe past the list) decide
+    // the last places: rank them by the exact key (d2 bits, original index) in a
+    // rescan and rewrite list places lo..K-1 (rare: a few per mille of the queries).
     int st = 0;  // 0 emit, 1 escalate, 2 exact path
-    bool amb_in = false, amb_b = false;
-    if (act) {
+    bool amb_b = on && (T[K - 1] >> kSlotBits) == (T[K] >> kSlotBits) && T[K - 1] != 0xffffffffu;
+    if (__any_sync(0xffffffffu, amb_b)) {
+        constexpr int KB = 4;  // places resolved in-kernel (more: the exact path)
+        const unsigned U = T[K - 1] >> kSlotBits;
+        int lo = 0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) lo += (T[r] >> kSlotBits) < U ? 1 : 0;
+        const int need = K - lo;
+        unsigned long long ek[KB];
+        int es[KB];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) {
+            ek[i] = ~0ull;
+            es[i] = 0;
+        }
+        const int cm = __reduce_max_sync(0xffffffffu, amb_b ? C : 0);
+        for (int c = 0; c < cm; ++c) {
+            const float4 p = cand[base + c];
+            const float dd = dist2(qp.x, qp.y, qp.z, p.x, p.y, p.z);
+            const bool take = amb_b && c < C && (__float_as_uint(dd) >> kSlotBits) == U;
+            const unsigned long long key =
+                take ? (((unsigned long long)__float_as_uint(dd) << 32) | (unsigned)__float_as_int(p.w)) : ~0ull;
+            // sorted insertion into the KB-list (no-op for ~0)
+            bool below = key < ek[KB - 1];
+#pragma unroll
+            for (int r = KB - 1; r > 0; --r) {
+                const bool sh = below && key < ek[r - 1];
+                const bool put = below && !sh;
+                const unsigned long long nk = sh ? ek[r - 1] : (put ? key : ek[r]);
+                const int ns = sh ? es[r - 1] : (put ? c : es[r]);
+                ek[r] = nk;
+                es[r] = ns;
+                below = sh;
+            }
+            if (below) {
+                ek[0] = key;
+                es[0] = c;
+            }
+        }
+        if (amb_b && need >= 1 && need <= KB) {
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int j2 = 0; j2 < KB; ++j2)
+                    if (j2 < need && r == lo + j2) T[r] = (U << kSlotBits) | (unsigned)(es[j2] + 1);
+            amb_b = false;
+        }
+    }
+    // (b) near-equal neighbours inside the list: their packed order must be the exact
+    // one; two passes of exact compare-exchange fix groups of up to three, anything
+    // left goes to the exact path
+    bool amb_in = false;
+    if (on) {
 #pragma unroll
         for (int r = 0; r < K - 1; ++r) amb_in |= (T[r] >> kSlotBits) == (T[r + 1] >> kSlotBits);
-        amb_b = (T[K - 1] >> kSlotBits) == (T[K] >> kSlotBits);
     }
-    if (__any_sync(0xffffffffu, amb_in && !amb_b)) {
-        // near-equal neighbours inside the list: their packed order must be the exact one
+    if (__any_sync(0xffffffffu, amb_in)) {
         bool bad = false;
-        if (amb_in && !amb_b) {
+        if (amb_in) {
+            for (int pass = 0; pass < 3; ++pass) {
+                bad = false;
 #pragma unroll
-            for (int r = 0; r < K - 1; ++r)
-                if ((T[r] >> kSlotBits) == (T[r + 1] >> kSlotBits))
-                    bad |= !exact_less(qp, cand[base + (int)(T[r] & kSlotMask) - 1],
-                                       cand[base + (int)(T[r + 1] & kSlotMask) - 1]);
+                for (int r = 0; r < K - 1; ++r)
+                    if ((T[r] >> kSlotBits) == (T[r + 1] >> kSlotBits) &&
+                        !exact_less(qp, cand[base + (int)(T[r] & kSlotMask) - 1],
+                                    cand[base + (int)(T[r + 1] & kSlotMask) - 1])) {
+                        if (pass < 2) {
+                            const unsigned t = T[r];
+                            T[r] = T[r + 1];
+                            T[r + 1] = t;
+                        }
+                        bad = true;
+                    }
+                if (!bad) break;
+            }
         }
         amb_in = bad;
     }
-    if (act) {
+    if (on) {
         const int bx = t_base[lt][0], by = t_base[lt][1], bz = t_base[lt][2];
         const float s = g0.cell;
         const float kth = __uint_as_float(T[K - 1] | kSlotMask);  // >= the K-th d2
         const QGeom G = make_geom(g0, qp.x, qp.y, qp.z);
-        const float mx = fminf(G.fx + (float)(G.cx - bx + 1) * s, (float)(bx + 3 - G.cx) * s - G.fx);
-        const float my = fminf(G.fy + (float)(G.cy - by + 1) * s, (float)(by + 3 - G.cy) * s - G.fy);
-        const float mz = fminf(G.fz + (float)(G.cz - bz + 1) * s, (float)(bz + 3 - G.cz) * s - G.fz);
-        const float m = fminf(mx, fminf(my, mz)) - g0.slack;
+        float m;
+        if (ROWS) {  // the 27-voxel cube around the query's voxel
+            m = cube_margin(G, s, g0.slack, 1);
+        } else {     // the tile's box
+            const float mx = fminf(G.fx + (float)(G.cx - bx + 1) * s, (float)(bx + 3 - G.cx) * s - G.fx);
+            const float my = fminf(G.fy + (float)(G.cy - by + 1) * s, (float)(by + 3 - G.cy) * s - G.fy);
+            const float mz = fminf(G.fz + (float)(G.cz - bz + 1) * s, (float)(bz + 3 - G.cz) * s - G.fz);
+            m = fminf(mx, fminf(my, mz)) - g0.slack;
+        }
         const bool full = T[K - 1] != 0xffffffffu;
         const bool fin = full && m > 0.0f && kth < m * m * kRel;
         st = !fin ? 1 : ((amb_in || amb_b) ? 2 : 0);
     }
-    push_warp(esc_count, esc_list, act && st == 1, (int)q);
-    push_warp2(exact_count, exact_list, act && st == 2, make_int2((int)q, 0));
-    if (!act || st != 0) return;
+    push_warp(esc_count, esc_list, on && st == 1, (int)qq);
+    push_warp2(exact_count, exact_list, on && st == 2, make_int2((int)qq, 0));
+    if (!on || st != 0) return;
     // (5) emit: original indices, exact d2, covariance of the K neighbours
     const int64_t row = __float_as_int(qp.w);
     const float4 p0 = cand[base + (int)(T[0] & kSlotMask) - 1];

@@ -87,27 +87,47 @@ def sharded_linearize(g, src, src_cov, index, tgt_cov, T, max_corr_dist=1.0, piv
     return g.combine_chunks(table, 1, num_chunks, 29)[0]
 
 
+class ShardPlan:
+    """This rank's part of a batch (fixed global chunking): its entries (b, c, lo, hi),
+    the device gather index of their rows in the batch arrays, the local entry
+    offsets and the global chunk rows b * num_chunks + c. Reusable while the batch's
+    layout is unchanged (bench.py builds it once)."""
+
+    def __init__(self, offsets, device, group=None, num_chunks: int = NUM_CHUNKS, reg_base=None):
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        offsets = np.asarray(offsets, dtype=np.int64)
+        self.B = len(offsets) - 1
+        self.num_chunks = num_chunks
+        base = offsets[:-1] if reg_base is None else np.asarray(reg_base, dtype=np.int64)
+        self.entries = registration_chunks(np.diff(offsets), rank, world, num_chunks)
+        lens = np.array([hi - lo for (_, _, lo, hi) in self.entries], dtype=np.int64)
+        self.loffs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        starts = np.array([base[b] + lo for (b, _, lo, _) in self.entries], dtype=np.int64)
+        n = int(self.loffs[-1])
+        # row i of entry e: starts[e] + (i - loffs[e])
+        idx = np.arange(n, dtype=np.int64) + np.repeat(starts - self.loffs[:-1], lens) if n else np.zeros(0, np.int64)
+        self.idx = torch.from_numpy(idx).to(device)
+        self.gid = np.array([b * num_chunks + c for (b, c, _, _) in self.entries], dtype=np.int32)
+        self.group = group
+
+
 def align_batched_sharded(g, src, src_cov, offsets, tgt, tgt_cov, T0s, group=None, num_chunks: int = NUM_CHUNKS,
-                          **params):
+                          reg_base=None, plan: ShardPlan | None = None, **params):
     """Batched LM alignment with the source points of every registration split into
     a fixed global chunking; this rank linearises its chunks (one batched launch
     per evaluation round), one NCCL all_reduce of the device chunk table per round
     combines them, and every rank runs the identical host LM. src / src_cov: the
-    full concatenated batch on this rank's GPU (only this rank's chunks are used).
-    Returns (T [B,4,4], infos)."""
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    offsets = np.asarray(offsets, dtype=np.int64)
-    B = len(offsets) - 1
-    entries = registration_chunks(np.diff(offsets), rank, world, num_chunks)
-    if entries:
-        idx = torch.cat([torch.arange(int(offsets[b]) + lo, int(offsets[b]) + hi, device=src.device)
-                         for (b, _, lo, hi) in entries])
-        src_l, cov_l = src[idx].contiguous(), src_cov[idx].contiguous()
+    batch's points on this rank's GPU (only this rank's chunks are used);
+    registration b has offsets[b+1] - offsets[b] points starting at row
+    reg_base[b] (default offsets[b]; registrations may share rows). Returns
+    (T [B,4,4], infos)."""
+    if plan is None:
+        plan = ShardPlan(offsets, src.device, group, num_chunks, reg_base)
+    if plan.idx.numel():
+        src_l, cov_l = src.index_select(0, plan.idx), src_cov.index_select(0, plan.idx)
     else:
         src_l = torch.zeros((0, 3), dtype=src.dtype, device=src.device)
         cov_l = torch.zeros((0, 6), dtype=src_cov.dtype, device=src_cov.device)
-    loffs = np.concatenate([[0], np.cumsum([hi - lo for (_, _, lo, hi) in entries])]).astype(np.int64)
-    gid = np.array([b * num_chunks + c for (b, c, _, _) in entries], dtype=np.int32)
-    return g.align_batched_sharded(src_l, cov_l, loffs, gid, num_chunks, B, tgt, tgt_cov, T0s,
-                                   allreduce=make_allreduce(group), **params)
+    return g.align_batched_sharded(src_l, cov_l, plan.loffs, plan.gid, plan.num_chunks, plan.B, tgt, tgt_cov, T0s,
+                                   allreduce=make_allreduce(plan.group), **params)

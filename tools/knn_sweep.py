@@ -1,6 +1,6 @@
 """Time the C3 map / scan self kNN(k=20)+cov for several cell sizes and library
 variants (GICP_LIB_VARIANT), one subprocess each.
-usage: python tools/knn_sweep.py cells=0.45,0.5 libs=default,variants/libgicp_x.so"""
+usage: python tools/knn_sweep.py cells=0.45,0.5 libs=default,variants/libgicp_x.so envs=A=1,A=0 (';'-separated sets)"""
 import os
 import subprocess
 import sys
@@ -33,9 +33,13 @@ for name, pts, c in (("map", mp, cell), ("scan", sc, 0.0)):
     os.environ.pop("GICP_DEBUG_STATS")
     print(f"RESULT {os.path.basename(os.environ.get('GICP_LIB_VARIANT', 'default'))} {name} cell={idx.cell_size:.3f} median {np.median(ts):.3f} ms min {np.min(ts):.3f}", flush=True)
 '''
+envs = [e for e in args.get("envs", "").split(";")]
 for lib in libs:
+  for es in envs:
+    extra = dict(kv.split("=", 1) for kv in es.split(",") if kv)
     for cell in cells:
-        env = dict(os.environ, ROOT=ROOT, CELL=cell)
+        env = dict(os.environ, ROOT=ROOT, CELL=cell, **extra)
+        print("ENV", es, flush=True)
         if lib != "default":
             env["GICP_LIB_VARIANT"] = os.path.join(ROOT, "paper_2308_07173_b200", lib)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
