@@ -695,6 +695,9 @@ namespace {
 struct BatchScratch {
     char* base = nullptr;
     int4* btab = nullptr;
+    int4* ctab = nullptr;   // a round's compacted block table (the active entries' blocks)
+    int2* clist = nullptr;  // per active entry: {its first block in btab, its compact start}
+    std::vector<int> eblk;  // host: first block of every entry in btab
     int64_t* offs = nullptr;
     Pose* poses = nullptr;
     LinScratch ls;
@@ -703,23 +706,34 @@ struct BatchScratch {
 
 // device scratch: block table, offsets, poses, per-registration counters (+1 for
 // the launch), block partials; `extra` bytes appended (16-B aligned) for the caller
-int batch_scratch(const int64_t* offsets, int B, size_t extra, cudaStream_t s, BatchScratch& bs, char** extra_p) {
+int batch_scratch(const int64_t* offsets, int B, size_t extra, cudaStream_t s, BatchScratch& bs, char** extra_p,
+                  int nposes = -1) {
+    if (nposes < B) nposes = B;
     std::vector<int4> tab;
     for (int b = 0; b < B; ++b) {
         const int64_t n = offsets[b + 1] - offsets[b];
         const int nbk = (int)((n + kLinPPB - 1) / kLinPPB);
-        for (int k = 0; k < nbk; ++k) tab.push_back(make_int4(b, k, nbk, 0));
+        for (int k = 0; k < nbk; ++k) tab.push_back(make_int4(b, k, nbk, (int)tab.size()));
     }
     bs.nb = (int64_t)tab.size();
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    bs.eblk.assign(B + 1, 0);
+    for (int b = 0, acc = 0; b <= B; ++b) {
+        bs.eblk[b] = acc;
+        if (b < B) acc += (int)((offsets[b + 1] - offsets[b] + kLinPPB - 1) / kLinPPB);
+    }
     const size_t o_tab = 0, o_offs = al(o_tab + tab.size() * sizeof(int4)), o_pose = al(o_offs + (B + 1) * 8),
-                 o_done = al(o_pose + (size_t)B * sizeof(Pose)), o_part = al(o_done + (B + 1) * sizeof(unsigned)),
-                 o_extra = al(o_part + linearize_partials_bytes(std::max<int64_t>(bs.nb, 1)));
+                 o_done = al(o_pose + (size_t)nposes * sizeof(Pose)), o_part = al(o_done + (B + 1) * sizeof(unsigned)),
+                 o_ctab = al(o_part + linearize_partials_bytes(std::max<int64_t>(bs.nb, 1))),
+                 o_clist = al(o_ctab + std::max<size_t>(tab.size(), 1) * sizeof(int4)),
+                 o_extra = al(o_clist + (size_t)(B + 1) * sizeof(int2));
     if (cudaMallocAsync((void**)&bs.base, o_extra + extra, s) != cudaSuccess) {
         cudaGetLastError();
         return set_error(GICP_ENOMEM, "batched linearize: scratch allocation failed");
     }
     bs.btab = (int4*)(bs.base + o_tab);
+    bs.ctab = (int4*)(bs.base + o_ctab);
+    bs.clist = (int2*)(bs.base + o_clist);
     bs.offs = (int64_t*)(bs.base + o_offs);
     bs.poses = (Pose*)(bs.base + o_pose);
     bs.ls.done = (unsigned*)(bs.base + o_done);
@@ -891,20 +905,31 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     char* ex = nullptr;
     // + the correspondence certificates paired with the two buffers (R27)
     const bool certs = GICP_ALIGN_CACHE && getenv("GICP_ALIGN_NOCACHE") == nullptr;
-    const size_t dev_extra = ds ? (size_t)std::max(E, 1) * (32 * sizeof(double) + sizeof(int)) + 512 : 0;
+    const size_t dev_extra = (ds ? (size_t)std::max(E, 1) * (32 * sizeof(double) + sizeof(int)) : 0) +
+                             (size_t)std::max(E, 1) * sizeof(int) + 768;
     if ((rc = batch_scratch(offsets, E,
                             2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
                                 (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + dev_extra,
-                            s, bs, &ex)))
+                            s, bs, &ex, B)))
         return rc;
     double* Ed = nullptr;  // device entry rows [E][32] (device sharding)
     int* gid_d = nullptr;
+    // entry -> registration (the poses go up per registration, not per entry)
+    int* ereg_d = (int*)(((uintptr_t)ex + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
+                          (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + 255) & ~(uintptr_t)255);
     if (ds) {
-        Ed = (double*)(((uintptr_t)ex + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
-                        (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + 255) & ~(uintptr_t)255);
+        Ed = (double*)(((uintptr_t)(ereg_d + std::max(E, 1)) + 255) & ~(uintptr_t)255);
         gid_d = (int*)(Ed + 32 * (size_t)std::max(E, 1));
         if (E > 0 &&
             (rc = check_cuda(cudaMemcpyAsync(gid_d, ds->gid, E * sizeof(int), cudaMemcpyHostToDevice, s), "H2D"))) {
+            cudaFreeAsync(bs.base, s);
+            return rc;
+        }
+    }
+    if (E > 0) {
+        std::vector<int> er(E);
+        for (int e = 0; e < E; ++e) er[e] = entry_reg ? entry_reg[e] : e;
+        if ((rc = check_cuda(cudaMemcpyAsync(ereg_d, er.data(), E * sizeof(int), cudaMemcpyHostToDevice, s), "H2D"))) {
             cudaFreeAsync(bs.base, s);
             return rc;
         }
@@ -924,7 +949,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     // host-mapped: entry rows [E][32] (device sharding: registration rows [B][32]) |
     // flag | pinned pose staging [E]
     const size_t rows = (size_t)(ds ? std::max(E, B) : E) * 32 * sizeof(double);
-    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)E * sizeof(Pose));
+    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)std::max(E, B) * sizeof(Pose) + (size_t)(E + 1) * sizeof(int2));
     if (!mb) {
         cudaFreeAsync(bs.base, s);
         return set_error(GICP_ENOMEM, "gicp_align_batched: host-mapped buffer");
@@ -963,31 +988,64 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     // rank calls `reduce` on every round (collectives stay matched) even when it
     // launches nothing.
     const double coarse_thr = coarse_threshold(tgt);
+    // GICP_DEBUG_ALIGN_HOST: rounds, their device-wait time and the host time between them
+    const bool host_trace = getenv("GICP_DEBUG_ALIGN_HOST") != nullptr;
+    using clk = std::chrono::steady_clock;
+    double t_wait = 0.0, t_total = 0.0;
+    int n_rounds = 0;
+    const auto t_begin = clk::now();
+    std::vector<char> eact(std::max(E, 1));
     auto round = [&](auto who, auto pose, int flags) -> int {
+        ++n_rounds;
         int n_active = 0;
-        for (int e = 0; e < E; ++e) {
-            const int b = reg(e);
-            const bool a = who(b) && offsets[e + 1] > offsets[e];  // an empty entry has no block
+        // one pose per registration (the kernel maps its entries through ereg)
+        for (int b = 0; b < B; ++b) {
+            const bool w = who(b);
+            pst[b].active = w;
+            if (!w) continue;
             const double* Tp;
             const double* pp;
             pose(b, Tp, pp);
-            pst[e] = make_pose(Tp, pp);
-            pst[e].active = a;
-            pst[e].cur = st[b].cur;
-            pst[e].coarse = st[b].disp > coarse_thr;  // per registration
-            n_active += a;
+            pst[b] = make_pose(Tp, pp);
+            pst[b].active = 1;
+            pst[b].cur = st[b].cur;
+            pst[b].coarse = st[b].disp > coarse_thr;  // per registration
+        }
+        for (int e = 0; e < E; ++e) {
+            eact[e] = pst[reg(e)].active && offsets[e + 1] > offsets[e];  // an empty entry has no block
+            n_active += eact[e];
         }
         int r = GICP_OK;
         if (n_active > 0) {
-            r = check_cuda(cudaMemcpyAsync(bs.poses, pst, E * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
+            r = check_cuda(cudaMemcpyAsync(bs.poses, pst, B * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
             if (r) return r;
             BatchView bv;
             bv.btab = bs.btab;
             bv.offs = bs.offs;
             bv.poses = bs.poses;
+            bv.ereg = ereg_d;
             bv.n_scans = E;
             bv.n_active = n_active;
             bv.out_stride = 32;
+            int64_t nbl = bs.nb;
+            if (n_active < E) {
+                // only the active entries' blocks are launched: their {first block,
+                // compact start} list goes up (pinned staging) and expands on the device
+                int2* cl = (int2*)(mb->h + rows + 256 + (size_t)std::max(E, B) * sizeof(Pose));
+                int nce = 0, acc = 0;
+                for (int e = 0; e < E; ++e)
+                    if (eact[e]) {
+                        cl[nce++] = make_int2(bs.eblk[e], acc);
+                        acc += bs.eblk[e + 1] - bs.eblk[e];
+                    }
+                cl[nce] = make_int2(0, acc);
+                r = check_cuda(cudaMemcpyAsync(bs.clist, cl, (nce + 1) * sizeof(int2), cudaMemcpyHostToDevice, s),
+                               "H2D");
+                if (!r) r = launch_compact_btab(bs.btab, bs.clist, nce, acc, bs.ctab, s);
+                if (r) return r;
+                bv.btab = bs.ctab;
+                nbl = acc;
+            }
             bs.ls.seq = ++seq;
             LinScratch lsr = bs.ls;
             if (ds) lsr.flag = nullptr;  // the combine kernel signals
@@ -995,12 +1053,12 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             const bool timed = kt.on && kt.used < KernelTiming::kCap;
             if (timed) cudaEventRecord(kt.e[2 * kt.used], s);
             r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags,
-                                      ds ? Ed : Hd, corrA, s, lsr, corrB, bv, bs.nb);
+                                      ds ? Ed : Hd, corrA, s, lsr, corrB, bv, nbl);
             if (timed) {
                 cudaEventRecord(kt.e[2 * kt.used + 1], s);
                 int64_t ap = 0;
                 for (int e = 0; e < E; ++e)
-                    if (pst[e].active) ap += offsets[e + 1] - offsets[e];
+                    if (eact[e]) ap += offsets[e + 1] - offsets[e];
                 kt.lpts[kt.used] = ap;
                 kt.kind[kt.used++] = (flags & kLinDual) ? 0 : ((flags & GICP_LIN_ERROR_ONLY) ? 2 : 1);
             }
@@ -1011,19 +1069,21 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             // device chunk table: zero, this rank's rows, allreduce, chunk-ordered combine
             const size_t tb = (size_t)B * ds->nc * 32 * sizeof(double);
             r = check_cuda(cudaMemsetAsync(ds->table, 0, tb, s), "memset");
-            if (!r && n_active > 0) r = launch_scatter_rows(Ed, E, gid_d, bs.poses, ds->table, s);
+            if (!r && n_active > 0) r = launch_scatter_rows(Ed, E, gid_d, ereg_d, bs.poses, bs.offs, ds->table, s);
             if (!r && ds->ar && ds->ar(ds->table, (int64_t)B * ds->nc * 32, ds->user, stream) != 0)
                 r = set_error(GICP_ECUDA, "gicp_align_batched_sharded: the allreduce callback failed");
             if (r) return r;
             bs.ls.seq = ++seq;
             r = launch_combine_chunks(ds->table, B, ds->nc, 32, Hd, bs.ls.flag, bs.ls.seq, s);
+            const auto w0 = clk::now();
             if (!r) r = wait_mapped(&mo, bs.ls.seq, s);
+            t_wait += std::chrono::duration<double, std::milli>(clk::now() - w0).count();
             if (r) return r;
             std::memcpy(Hr.data(), He, (size_t)B * 32 * sizeof(double));
             return GICP_OK;
         }
         for (int e = 0; e < E; ++e)  // rows of entries not launched this round are zero
-            if (!pst[e].active) std::memset(He + 32 * e, 0, 32 * sizeof(double));
+            if (!eact[e]) std::memset(He + 32 * e, 0, 32 * sizeof(double));
         if (reduce) {
             if (reduce(He, E, Hr.data(), B, user) != 0)
                 return set_error(GICP_ECUDA, "gicp_align_batched: the reduce callback failed");
@@ -1187,6 +1247,10 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
                 if (!st[b].done && st[b].relin == 2) keep(b);
         }
     }
+    t_total = std::chrono::duration<double, std::milli>(clk::now() - t_begin).count();
+    if (host_trace)
+        fprintf(stderr, "[gicp align_batched host] B=%d E=%d rounds=%d total %.2f ms, waiting on the device %.2f ms\n",
+                B, E, n_rounds, t_total, t_wait);
     cudaFreeAsync(bs.base, s);
     {
         KernelTiming& kt = kernel_timing();

@@ -237,6 +237,7 @@ struct BatchView {
     const int4* btab = nullptr;
     const int64_t* offs = nullptr;
     const Pose* poses = nullptr;
+    const int* ereg = nullptr;  // entry -> its pose (registration); nullptr: one pose per entry
     int n_scans = 1;
     int n_active = 1;
     int out_stride = 0;
@@ -298,10 +299,11 @@ int launch_linearize_vgicp(const float* src, const float* src_cov, int64_t ns, c
                            const double T[16], const double* pivot, int mode, int flags, int* base, double* out29,
                            cudaStream_t s, const LinScratch* pre = nullptr);
 // sharded linearisation (shard.cu): entry rows -> global chunk table, chunk-ordered combine
-int launch_scatter_rows(const double* rows, int E, const int* gid_dev, const Pose* poses_dev, double* table,
-                        cudaStream_t s);
+int launch_scatter_rows(const double* rows, int E, const int* gid_dev, const int* ereg_dev, const Pose* poses_dev,
+                        const int64_t* offs_dev, double* table, cudaStream_t s);
 int launch_combine_chunks(const double* table, int B, int nc, int width, double* out, volatile unsigned* flag,
                           unsigned seq, cudaStream_t s);
+int launch_compact_btab(const int4* btab, const int2* clist, int nce, int total, int4* ctab, cudaStream_t s);
 int sort_source(const float* src, const float* src_cov, int64_t ns, float cell, float* src_p, float* cov_p,
                 cudaStream_t s, const int64_t* offs = nullptr, int nseg = 1);
 

@@ -371,18 +371,20 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     // its point range; every registration is partitioned exactly like a single
     // launch over its own points, so its result is bitwise the single one
     int scan = 0, blk = blockIdx.x, nblk = gridDim.x;
+    int gblk = blockIdx.x;  // the block's slot in the partials (batched: its full-table index)
     int64_t p0 = 0, pend = ns;
     if (bv.btab) {
         const int4 e = bv.btab[blockIdx.x];
         scan = e.x;
         blk = e.y;
         nblk = e.z;
-        if (!bv.poses[scan].active) return;  // block-uniform: converged registration
+        gblk = e.w;
+        if (!bv.poses[bv.ereg ? bv.ereg[scan] : scan].active) return;  // block-uniform: converged registration
         p0 = bv.offs[scan];
         pend = bv.offs[scan + 1];
     }
     __shared__ Pose sP;
-    if (threadIdx.x == 0) sP = bv.btab ? bv.poses[scan] : P;
+    if (threadIdx.x == 0) sP = bv.btab ? bv.poses[bv.ereg ? bv.ereg[scan] : scan] : P;
     __syncthreads();
     // correspondence buffers: single launches use (corr, corr_old) as given; a
     // batched registration reads its current buffer (REUSE / DUAL's old) and
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
 #pragma unroll
             for (int w = 0; w < kLinBlock / 32; ++w) v += sh[w][c];
         }
-        partials[(int64_t)blockIdx.x * kNV + c] = v;
+        partials[(int64_t)gblk * kNV + c] = v;
     }
     // last block (of the registration): fixed-order sum of its block partials
     __shared__ bool last;
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     __syncthreads();
     if (!last) return;
     __threadfence();
-    partials += (int64_t)(blockIdx.x - blk) * kNV;  // the registration's first block
+    partials += (int64_t)(gblk - blk) * kNV;  // the registration's first block
     out29 += (int64_t)scan * bv.out_stride;
     // 29 components x 8 interleaved sub-sequences (block b goes to sub b % 8), the
     // loads of each thread batched 8 at a time (independent, in flight together),
