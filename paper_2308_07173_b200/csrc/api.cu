@@ -949,7 +949,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     // host-mapped: entry rows [E][32] (device sharding: registration rows [B][32]) |
     // flag | pinned pose staging [E]
     const size_t rows = (size_t)(ds ? std::max(E, B) : E) * 32 * sizeof(double);
-    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)std::max(E, B) * sizeof(Pose) + (size_t)(E + 1) * sizeof(int2));
+    MappedBatch* mb = mapped_batch(rows + 256 + (size_t)std::max(E, B) * sizeof(Pose) + 3 * (size_t)(E + 1) * sizeof(int2));
     if (!mb) {
         cudaFreeAsync(bs.base, s);
         return set_error(GICP_ENOMEM, "gicp_align_batched: host-mapped buffer");
@@ -965,11 +965,20 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     std::vector<double> Hr((size_t)B * 32, 0.0);  // registration rows of the last round
     const double* H = Hr.data();
 
+    // Per-registration state machine (each registration takes exactly the evaluation
+    // sequence of gicp_align on it alone; a round evaluates every unfinished
+    // registration once, whatever its next evaluation is, so slow registrations no
+    // longer hold the others in lockstep): FULL = linearise at T (initial, or after a
+    // trial accepted), DUAL = the speculative first trial of an iteration (the full
+    // linearisation at Tn plus e' with the current correspondences), TRIAL = e' alone
+    // at Tn (a later trial after a rejection).
+    enum { M_DONE = 0, M_FULL = 1, M_DUAL = 2, M_TRIAL = 3 };
     struct St {
         double T[16], piv[3], lin29[29], Tn[16], pn[3], delta[6], Hm[36], b[6];
         double lambda = -1.0, nu = 2.0, err = 0.0, e = 0.0;
         double disp = INFINITY;  // the last step's point motion (kLinCoarse)
-        int it = 0, converged = 0, done = 0, cur = 0, rc = GICP_OK, inner_ok = 0, accepted = 0, relin = 0;
+        int it = 0, converged = 0, cur = 0, rc = GICP_OK, inner = 0, mode = M_FULL;
+        int relin = 0;           // a FULL after an accepted trial (LM: test convergence after it)
         int64_t inl = 0;
     };
     std::vector<St> st(B);
@@ -979,97 +988,113 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         st[b].piv[1] = st[b].T[7];
         st[b].piv[2] = st[b].T[11];
         if (!reduce && !ds && !entry_reg && offsets[b + 1] == offsets[b]) {  // no points: no correspondences
-            st[b].done = 1;
+            st[b].mode = M_DONE;
             st[b].rc = GICP_EDEGENERATE;
         }
     }
-    // one evaluation round: `who` selects the registrations, pose(b) their pose;
-    // DUAL reads the current buffer as corr_old and writes the other one. Every
-    // rank calls `reduce` on every round (collectives stay matched) even when it
-    // launches nothing.
     const double coarse_thr = coarse_threshold(tgt);
     // GICP_DEBUG_ALIGN_HOST: rounds, their device-wait time and the host time between them
     const bool host_trace = getenv("GICP_DEBUG_ALIGN_HOST") != nullptr;
     using clk = std::chrono::steady_clock;
     double t_wait = 0.0, t_total = 0.0;
-    int n_rounds = 0;
+    int n_rounds = 0, n_launch = 0;
     const auto t_begin = clk::now();
     std::vector<char> eact(std::max(E, 1));
-    auto round = [&](auto who, auto pose, int flags) -> int {
+    // one round: every unfinished registration evaluated once; one launch per kind
+    // present (a compacted block table of that kind's entries), then the rows (the
+    // device chunk table + allreduce + combine when sharded). Every rank calls the
+    // collective on every round (collectives stay matched) even when it launches nothing.
+    auto round = [&]() -> int {
         ++n_rounds;
-        int n_active = 0;
-        // one pose per registration (the kernel maps its entries through ereg)
+        int n_any = 0;
         for (int b = 0; b < B; ++b) {
-            const bool w = who(b);
-            pst[b].active = w;
-            if (!w) continue;
-            const double* Tp;
-            const double* pp;
-            pose(b, Tp, pp);
-            pst[b] = make_pose(Tp, pp);
+            const St& q = st[b];
+            pst[b].active = q.mode != M_DONE;
+            if (q.mode == M_DONE) continue;
+            const bool trial = q.mode == M_DUAL || q.mode == M_TRIAL;
+            pst[b] = make_pose(trial ? q.Tn : q.T, trial ? q.pn : q.piv);
             pst[b].active = 1;
-            pst[b].cur = st[b].cur;
-            pst[b].coarse = st[b].disp > coarse_thr;  // per registration
+            pst[b].cur = q.cur;
+            pst[b].coarse = q.disp > coarse_thr;  // per registration
         }
-        for (int e = 0; e < E; ++e) {
-            eact[e] = pst[reg(e)].active && offsets[e + 1] > offsets[e];  // an empty entry has no block
-            n_active += eact[e];
-        }
+        for (int e = 0; e < E; ++e) n_any += pst[reg(e)].active && offsets[e + 1] > offsets[e];
         int r = GICP_OK;
-        if (n_active > 0) {
+        unsigned last_seq = 0;
+        if (n_any > 0) {
             r = check_cuda(cudaMemcpyAsync(bs.poses, pst, B * sizeof(Pose), cudaMemcpyHostToDevice, s), "H2D");
             if (r) return r;
-            BatchView bv;
-            bv.btab = bs.btab;
-            bv.offs = bs.offs;
-            bv.poses = bs.poses;
-            bv.ereg = ereg_d;
-            bv.n_scans = E;
-            bv.n_active = n_active;
-            bv.out_stride = 32;
-            int64_t nbl = bs.nb;
-            if (n_active < E) {
-                // only the active entries' blocks are launched: their {first block,
-                // compact start} list goes up (pinned staging) and expands on the device
-                int2* cl = (int2*)(mb->h + rows + 256 + (size_t)std::max(E, B) * sizeof(Pose));
-                int nce = 0, acc = 0;
-                for (int e = 0; e < E; ++e)
-                    if (eact[e]) {
-                        cl[nce++] = make_int2(bs.eblk[e], acc);
-                        acc += bs.eblk[e + 1] - bs.eblk[e];
-                    }
-                cl[nce] = make_int2(0, acc);
-                r = check_cuda(cudaMemcpyAsync(bs.clist, cl, (nce + 1) * sizeof(int2), cudaMemcpyHostToDevice, s),
-                               "H2D");
-                if (!r) r = launch_compact_btab(bs.btab, bs.clist, nce, acc, bs.ctab, s);
+            for (int kind = M_FULL; kind <= M_TRIAL; ++kind) {
+                int n_active = 0;
+                for (int e = 0; e < E; ++e) {
+                    eact[e] = offsets[e + 1] > offsets[e] && st[reg(e)].mode == kind;  // an empty entry has no block
+                    n_active += eact[e];
+                }
+                if (!n_active) continue;
+                const int flags = kind == M_FULL ? kLinCorrSpos
+                                  : kind == M_DUAL ? (kLinCorrSpos | kLinDual)
+                                                   : (kLinCorrSpos | GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY);
+                BatchView bv;
+                bv.btab = bs.btab;
+                bv.offs = bs.offs;
+                bv.poses = bs.poses;
+                bv.ereg = ereg_d;
+                bv.n_scans = E;
+                bv.n_active = n_active;
+                bv.out_stride = 32;
+                int64_t nbl = bs.nb;
+                if (n_active < E) {
+                    // only this kind's entries' blocks are launched: their {first block,
+                    // compact start} list goes up (pinned staging, one region per kind)
+                    // and expands on the device
+                    int2* cl = (int2*)(mb->h + rows + 256 + (size_t)std::max(E, B) * sizeof(Pose)) +
+                               (size_t)(kind - 1) * (E + 1);
+                    int nce = 0, acc = 0;
+                    for (int e = 0; e < E; ++e)
+                        if (eact[e]) {
+                            cl[nce++] = make_int2(bs.eblk[e], acc);
+                            acc += bs.eblk[e + 1] - bs.eblk[e];
+                        }
+                    cl[nce] = make_int2(0, acc);
+                    r = check_cuda(cudaMemcpyAsync(bs.clist, cl, (nce + 1) * sizeof(int2), cudaMemcpyHostToDevice, s),
+                                   "H2D");
+                    if (!r) r = launch_compact_btab(bs.btab, bs.clist, nce, acc, bs.ctab, s);
+                    if (r) return r;
+                    bv.btab = bs.ctab;
+                    nbl = acc;
+                }
+                bs.ls.seq = ++seq;
+                last_seq = bs.ls.seq;
+                LinScratch lsr = bs.ls;
+                if (ds) lsr.flag = nullptr;  // the combine kernel signals
+                KernelTiming& kt = kernel_timing();
+                const bool timed = kt.on && kt.used < KernelTiming::kCap;
+                if (timed) cudaEventRecord(kt.e[2 * kt.used], s);
+                ++n_launch;
+                r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags,
+                                          ds ? Ed : Hd, corrA, s, lsr, corrB, bv, nbl);
+                if (timed) {
+                    cudaEventRecord(kt.e[2 * kt.used + 1], s);
+                    int64_t ap = 0;
+                    for (int e = 0; e < E; ++e)
+                        if (eact[e]) ap += offsets[e + 1] - offsets[e];
+                    kt.lpts[kt.used] = ap;
+                    kt.kind[kt.used++] = kind == M_DUAL ? 0 : (kind == M_TRIAL ? 2 : 1);
+                }
                 if (r) return r;
-                bv.btab = bs.ctab;
-                nbl = acc;
             }
-            bs.ls.seq = ++seq;
-            LinScratch lsr = bs.ls;
-            if (ds) lsr.flag = nullptr;  // the combine kernel signals
-            KernelTiming& kt = kernel_timing();
-            const bool timed = kt.on && kt.used < KernelTiming::kCap;
-            if (timed) cudaEventRecord(kt.e[2 * kt.used], s);
-            r = launch_linearize_core(src_p, cov_p, ns, tgt, tgt_cov, pst[0], prm->max_corr_dist, flags,
-                                      ds ? Ed : Hd, corrA, s, lsr, corrB, bv, nbl);
-            if (timed) {
-                cudaEventRecord(kt.e[2 * kt.used + 1], s);
-                int64_t ap = 0;
-                for (int e = 0; e < E; ++e)
-                    if (eact[e]) ap += offsets[e + 1] - offsets[e];
-                kt.lpts[kt.used] = ap;
-                kt.kind[kt.used++] = (flags & kLinDual) ? 0 : ((flags & GICP_LIN_ERROR_ONLY) ? 2 : 1);
+            if (!ds) {
+                const auto w0 = clk::now();
+                r = wait_mapped(&mo, last_seq, s);
+                t_wait += std::chrono::duration<double, std::milli>(clk::now() - w0).count();
+                if (r) return r;
             }
-            if (!r && !ds) r = wait_mapped(&mo, bs.ls.seq, s);
-            if (r) return r;
         }
+        for (int e = 0; e < E; ++e) eact[e] = pst[reg(e)].active && offsets[e + 1] > offsets[e];
         if (ds) {
             // device chunk table: zero, this rank's rows, allreduce, chunk-ordered combine
             const size_t tb = (size_t)B * ds->nc * 32 * sizeof(double);
             r = check_cuda(cudaMemsetAsync(ds->table, 0, tb, s), "memset");
-            if (!r && n_active > 0) r = launch_scatter_rows(Ed, E, gid_d, ereg_d, bs.poses, bs.offs, ds->table, s);
+            if (!r && n_any > 0) r = launch_scatter_rows(Ed, E, gid_d, ereg_d, bs.poses, bs.offs, ds->table, s);
             if (!r && ds->ar && ds->ar(ds->table, (int64_t)B * ds->nc * 32, ds->user, stream) != 0)
                 r = set_error(GICP_ECUDA, "gicp_align_batched_sharded: the allreduce callback failed");
             if (r) return r;
@@ -1094,163 +1119,169 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         }
         return GICP_OK;
     };
-    auto at_T = [&](int b, const double*& Tp, const double*& pp) {
-        Tp = st[b].T;
-        pp = st[b].piv;
+    auto converged_step = [&](const St& q) {
+        const double mw = std::fmax(std::fabs(q.delta[0]), std::fmax(std::fabs(q.delta[1]), std::fabs(q.delta[2])));
+        const double mv = std::fmax(std::fabs(q.delta[3]), std::fmax(std::fabs(q.delta[4]), std::fabs(q.delta[5])));
+        return mw < prm->rot_eps && mv < prm->trans_eps;
     };
-    auto at_Tn = [&](int b, const double*& Tp, const double*& pp) {
-        Tp = st[b].Tn;
-        pp = st[b].pn;
-    };
-    auto keep = [&](int b) {  // take a full linearisation row: the other buffer becomes current
-        std::memcpy(st[b].lin29, H + 32 * b, sizeof(st[b].lin29));
-        st[b].cur ^= 1;
-    };
-    // initial linearisation of every registration
-    rc = round([&](int b) { return !st[b].done; }, at_T, kLinCorrSpos);
-    for (int b = 0; b < B && !rc; ++b)
-        if (!st[b].done) keep(b);
-    for (int it = 1; !rc && it <= prm->max_iter; ++it) {
-        bool any = false;
-        for (int b = 0; b < B; ++b) {
-            St& q = st[b];
-            if (q.done) continue;
-            q.it = it;
-            q.inl = (int64_t)q.lin29[28];
-            if (q.inl < 6) {
-                q.rc = GICP_EDEGENERATE;
-                q.done = 1;
+    // the next trial of an LM iteration (DUAL for the first, TRIAL after a rejection);
+    // ten solves / trials without an accepted step: a (numerical) minimum
+    auto try_trial = [&](St& q) {
+        while (q.inner < 10) {
+            double Hl[36], nb[6];
+            std::memcpy(Hl, q.Hm, sizeof(Hl));
+            for (int a = 0; a < 6; ++a) {
+                Hl[7 * a] += q.lambda;
+                nb[a] = -q.b[a];
+            }
+            if (!ldlt6(Hl, nb, q.delta)) {
+                q.lambda *= q.nu;
+                q.nu *= 2.0;
+                ++q.inner;
                 continue;
             }
-            for (int a = 0, o = 0; a < 6; ++a)
-                for (int c = a; c < 6; ++c, ++o) q.Hm[6 * a + c] = q.Hm[6 * c + a] = q.lin29[o];
-            for (int a = 0; a < 6; ++a) q.b[a] = q.lin29[21 + a];
-            q.e = q.lin29[27];
-            q.err = q.e;
-            for (int a = 0; a < 6; ++a) q.delta[a] = 0.0;
-            q.accepted = 0;
-            q.relin = 0;
-            any = true;
-            if (!prm->lm) {
-                double nb[6];
-                for (int a = 0; a < 6; ++a) nb[a] = -q.b[a];
-                if (!ldlt6(q.Hm, nb, q.delta)) {
-                    q.rc = GICP_EDEGENERATE;
-                    q.done = 1;
-                    continue;
-                }
-                double E[16];
-                pivoted_exp(q.delta, q.piv, E);
-                q.disp = step_displacement(q.delta);
-                mul44(E, q.T, q.T);
-            } else if (q.lambda < 0) {
-                double mx = 0.0;
-                for (int a = 0; a < 6; ++a) mx = std::fmax(mx, q.Hm[7 * a]);
-                q.lambda = 1e-9 * mx;
-            }
+            double Em[16];
+            pivoted_exp(q.delta, q.piv, Em);
+            q.disp = step_displacement(q.delta);
+            mul44(Em, q.T, q.Tn);
+            q.pn[0] = q.Tn[3];
+            q.pn[1] = q.Tn[7];
+            q.pn[2] = q.Tn[11];
+            q.mode = q.inner == 0 ? M_DUAL : M_TRIAL;
+            return;
         }
+        q.converged = 1;
+        q.mode = M_DONE;
+    };
+    // a new iteration from the linearisation at T (lin29)
+    auto start_iteration = [&](St& q) {
+        if (++q.it > prm->max_iter) {
+            q.it = prm->max_iter;
+            q.mode = M_DONE;
+            return;
+        }
+        q.inl = (int64_t)q.lin29[28];
+        if (q.inl < 6) {
+            q.rc = GICP_EDEGENERATE;
+            q.mode = M_DONE;
+            return;
+        }
+        for (int a = 0, o = 0; a < 6; ++a)
+            for (int c = a; c < 6; ++c, ++o) q.Hm[6 * a + c] = q.Hm[6 * c + a] = q.lin29[o];
+        for (int a = 0; a < 6; ++a) q.b[a] = q.lin29[21 + a];
+        q.e = q.lin29[27];
+        q.err = q.e;
+        for (int a = 0; a < 6; ++a) q.delta[a] = 0.0;
+        if (!prm->lm) {  // Gauss-Newton: the step, its convergence test, then re-linearise
+            double nb[6];
+            for (int a = 0; a < 6; ++a) nb[a] = -q.b[a];
+            if (!ldlt6(q.Hm, nb, q.delta)) {
+                q.rc = GICP_EDEGENERATE;
+                q.mode = M_DONE;
+                return;
+            }
+            double Em[16];
+            pivoted_exp(q.delta, q.piv, Em);
+            q.disp = step_displacement(q.delta);
+            mul44(Em, q.T, q.T);
+            if (converged_step(q)) {
+                q.converged = 1;
+                q.mode = M_DONE;
+                return;
+            }
+            q.piv[0] = q.T[3];
+            q.piv[1] = q.T[7];
+            q.piv[2] = q.T[11];
+            q.relin = 0;
+            q.mode = M_FULL;
+            return;
+        }
+        if (q.lambda < 0) {
+            double mx = 0.0;
+            for (int a = 0; a < 6; ++a) mx = std::fmax(mx, q.Hm[7 * a]);
+            q.lambda = 1e-9 * mx;
+        }
+        q.inner = 0;
+        try_trial(q);
+    };
+    auto accept = [&](St& q, double rho, double en) {
+        std::memcpy(q.T, q.Tn, sizeof(q.T));
+        std::memcpy(q.piv, q.pn, sizeof(q.piv));
+        const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);
+        q.lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
+        q.nu = 2.0;
+        q.err = en;
+    };
+    auto reject = [&](St& q) {
+        q.lambda *= q.nu;
+        q.nu *= 2.0;
+        ++q.inner;
+        try_trial(q);
+    };
+    while (!rc) {
+        bool any = false;
+        for (int b = 0; b < B; ++b) any |= st[b].mode != M_DONE;
         if (!any) break;
-        if (prm->lm) {
-            // inner trials in lockstep: round 0 is the speculative DUAL launch
-            for (int inner = 0; inner < 10 && !rc; ++inner) {
-                bool want = false;
-                for (int b = 0; b < B; ++b) {
-                    St& q = st[b];
-                    q.inner_ok = 0;
-                    if (q.done || q.accepted) continue;
-                    double Hl[36], nb[6];
-                    std::memcpy(Hl, q.Hm, sizeof(Hl));
-                    for (int a = 0; a < 6; ++a) {
-                        Hl[7 * a] += q.lambda;
-                        nb[a] = -q.b[a];
+        if ((rc = round())) break;
+        for (int b = 0; b < B; ++b) {
+            St& q = st[b];
+            const double* h = Hr.data() + 32 * b;
+            switch (q.mode) {
+                case M_FULL: {  // a linearisation at T: the other correspondence buffer becomes current
+                    std::memcpy(q.lin29, h, sizeof(q.lin29));
+                    q.cur ^= 1;
+                    if (q.relin && prm->lm && converged_step(q)) {
+                        q.converged = 1;
+                        q.mode = M_DONE;
+                        break;
                     }
-                    if (!ldlt6(Hl, nb, q.delta)) {
-                        q.lambda *= q.nu;
-                        q.nu *= 2.0;
-                        continue;
-                    }
-                    double E[16];
-                    pivoted_exp(q.delta, q.piv, E);
-                    q.disp = step_displacement(q.delta);
-                    mul44(E, q.T, q.Tn);
-                    q.pn[0] = q.Tn[3];
-                    q.pn[1] = q.Tn[7];
-                    q.pn[2] = q.Tn[11];
-                    q.inner_ok = 1;
-                    want = true;
+                    q.relin = 0;
+                    start_iteration(q);
+                    break;
                 }
-                if (!want) continue;
-                const bool spec = inner == 0;
-                rc = round([&](int b) { return st[b].inner_ok == 1; }, at_Tn,
-                           spec ? (kLinCorrSpos | kLinDual)
-                                : (kLinCorrSpos | GICP_LIN_REUSE_CORR | GICP_LIN_ERROR_ONLY));
-                if (rc) break;
-                for (int b = 0; b < B; ++b) {
-                    St& q = st[b];
-                    if (!q.inner_ok) continue;
-                    const double en = spec ? H[32 * b + 29] : H[32 * b + 27];
+                case M_DUAL: {
+                    const double en = h[29];
                     double den = 0.0;
                     for (int a = 0; a < 6; ++a) den += q.delta[a] * (q.lambda * q.delta[a] - q.b[a]);
                     const double rho = (q.e - en) / den;
-                    if (rho > 0) {
-                        std::memcpy(q.T, q.Tn, sizeof(q.T));
-                        std::memcpy(q.piv, q.pn, sizeof(q.piv));
-                        if (spec)
-                            keep(b);
-                        else
-                            q.relin = 1;
-                        const double f = 1.0 - std::pow(2.0 * rho - 1.0, 3);
-                        q.lambda *= (f > 1.0 / 3.0) ? f : 1.0 / 3.0;
-                        q.nu = 2.0;
-                        q.err = en;
-                        q.accepted = 1;
+                    if (rho > 0) {  // the speculative full linearisation at Tn is kept
+                        accept(q, rho, en);
+                        std::memcpy(q.lin29, h, sizeof(q.lin29));
+                        q.cur ^= 1;
+                        if (converged_step(q)) {
+                            q.converged = 1;
+                            q.mode = M_DONE;
+                        } else {
+                            start_iteration(q);
+                        }
                     } else {
-                        q.lambda *= q.nu;
-                        q.nu *= 2.0;
+                        reject(q);
                     }
+                    break;
                 }
+                case M_TRIAL: {
+                    const double en = h[27];
+                    double den = 0.0;
+                    for (int a = 0; a < 6; ++a) den += q.delta[a] * (q.lambda * q.delta[a] - q.b[a]);
+                    const double rho = (q.e - en) / den;
+                    if (rho > 0) {  // accepted: linearise at the new pose, then test convergence
+                        accept(q, rho, en);
+                        q.relin = 1;
+                        q.mode = M_FULL;
+                    } else {
+                        reject(q);
+                    }
+                    break;
+                }
+                default:
+                    break;
             }
-            if (rc) break;
-            // registrations accepted after a rejection: linearise at the new pose
-            rc = round([&](int b) { return !st[b].done && st[b].relin == 1; }, at_T, kLinCorrSpos);
-            if (rc) break;
-            for (int b = 0; b < B; ++b)
-                if (!st[b].done && st[b].relin) keep(b);
-        }
-        bool relin_gn = false;
-        for (int b = 0; b < B; ++b) {
-            St& q = st[b];
-            if (q.done || q.it != it) continue;
-            if (prm->lm && !q.accepted) {  // no step decreases the cost: a (numerical) minimum
-                q.converged = 1;
-                q.done = 1;
-                continue;
-            }
-            const double mw = std::fmax(std::fabs(q.delta[0]), std::fmax(std::fabs(q.delta[1]), std::fabs(q.delta[2])));
-            const double mv = std::fmax(std::fabs(q.delta[3]), std::fmax(std::fabs(q.delta[4]), std::fabs(q.delta[5])));
-            if (mw < prm->rot_eps && mv < prm->trans_eps) {
-                q.converged = 1;
-                q.done = 1;
-                continue;
-            }
-            if (!prm->lm) {
-                q.piv[0] = q.T[3];
-                q.piv[1] = q.T[7];
-                q.piv[2] = q.T[11];
-                q.relin = 2;
-                relin_gn = true;
-            }
-        }
-        if (relin_gn) {  // Gauss-Newton: linearise at the new poses
-            rc = round([&](int b) { return !st[b].done && st[b].relin == 2; }, at_T, kLinCorrSpos);
-            for (int b = 0; b < B && !rc; ++b)
-                if (!st[b].done && st[b].relin == 2) keep(b);
         }
     }
     t_total = std::chrono::duration<double, std::milli>(clk::now() - t_begin).count();
     if (host_trace)
-        fprintf(stderr, "[gicp align_batched host] B=%d E=%d rounds=%d total %.2f ms, waiting on the device %.2f ms\n",
-                B, E, n_rounds, t_total, t_wait);
+        fprintf(stderr, "[gicp align_batched host] B=%d E=%d rounds=%d launches=%d total %.2f ms, waiting on the device "
+                "%.2f ms\n", B, E, n_rounds, n_launch, t_total, t_wait);
     cudaFreeAsync(bs.base, s);
     {
         KernelTiming& kt = kernel_timing();
