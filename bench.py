@@ -62,6 +62,7 @@ WORKLOAD_C4 = ("C4 batched scan-to-map: 256 registrations (32 distinct 100k-poin
                "sharded over the GPUs (NCCL chunk-table allreduce per round)")
 WORKLOAD_C3 = "C3 scan-to-map: 100k-point scan vs 2M-point racetrack map, k=20, GICP to convergence"
 REF_SUB = 2000               # oracle sample: source points of one registration
+SCAN_WORKERS = int(os.environ.get("BENCH_SCAN_WORKERS", "4"))   # host threads issuing the scans' kNN/cov
 
 
 def peaks():
@@ -270,6 +271,9 @@ def run_c4(args, rank, world, local):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    from concurrent.futures import ThreadPoolExecutor
+    side = [torch.cuda.Stream(device=dev) for _ in range(SCAN_WORKERS)]
+    pool = ThreadPoolExecutor(max_workers=SCAN_WORKERS, initializer=lambda: torch.cuda.set_device(local))
 
     def step(map_src, scan_src, record=None):
         e = [ev() for _ in range(5)]
@@ -282,11 +286,25 @@ def run_c4(args, rank, world, local):
         _, _, cov_map = g.knn_cov_self(imap, K, EPS, with_nbr=True)
         g.attach_cov(imap, cov_map)
         e[1].record(stream)
-        for i in range(per):
-            sl = scan_src[i * N_SCAN:(i + 1) * N_SCAN]
-            isc = g.build_index(sl, 0.0)
-            g.knn_cov_self(isc, K, EPS, with_nbr=True, out=(None, None, cov_mine[i * N_SCAN:(i + 1) * N_SCAN]))
-            isc.free()
+        # the distinct scans' index + kNN/cov: latency-bound small clouds (host-synchronising
+        # index builds), so SCAN_WORKERS host threads run them on their own streams at once
+        start = torch.cuda.Event()
+        start.record(stream)
+
+        def scan_job(w):
+            sw = side[w]
+            sw.wait_event(start)
+            with torch.cuda.stream(sw):
+                for i in range(w, per, SCAN_WORKERS):
+                    sl = scan_src[i * N_SCAN:(i + 1) * N_SCAN]
+                    isc = g.build_index(sl, 0.0)
+                    g.knn_cov_self(isc, K, EPS, with_nbr=True, out=(None, None, cov_mine[i * N_SCAN:(i + 1) * N_SCAN]))
+                    isc.free()
+            done = torch.cuda.Event()
+            done.record(sw)
+            return done
+        for d in list(pool.map(scan_job, range(SCAN_WORKERS))):
+            stream.wait_event(d)
         if world > 1:
             dist.all_gather_into_tensor(cov_all, cov_mine)
         else:

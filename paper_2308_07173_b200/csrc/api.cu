@@ -1218,11 +1218,18 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         ++q.inner;
         try_trial(q);
     };
+    const bool dbg_rows = getenv("GICP_DEBUG_ALIGN") != nullptr;
     while (!rc) {
         bool any = false;
         for (int b = 0; b < B; ++b) any |= st[b].mode != M_DONE;
         if (!any) break;
         if ((rc = round())) break;
+        if (dbg_rows)
+            for (int b = 0; b < B; ++b)
+                if (st[b].mode != M_DONE)
+                    fprintf(stderr, "[gicp align_batched] round %d reg %d mode %d it %d: H00 %.9g b0 %.9g e %.9g n %.0f "
+                            "e' %.9g\n", n_rounds, b, st[b].mode, st[b].it, Hr[32 * b], Hr[32 * b + 21], Hr[32 * b + 27],
+                            Hr[32 * b + 28], Hr[32 * b + 29]);
         for (int b = 0; b < B; ++b) {
             St& q = st[b];
             const double* h = Hr.data() + 32 * b;

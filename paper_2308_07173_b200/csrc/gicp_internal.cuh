@@ -241,6 +241,7 @@ struct BatchView {
     int n_scans = 1;
     int n_active = 1;
     int out_stride = 0;
+    int queue = 0;  // DUAL+CERT: compact the uncertified searches per block (GICP_LIN_QUEUE=1)
 };
 
 struct LinScratch {

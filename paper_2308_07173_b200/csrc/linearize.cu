@@ -451,8 +451,64 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             int bj, ovf;
             float rho;
             LPROF(const long long t0 = clock64();)
-            nn_search<CERT>(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho,
-                      (sP.coarse && lvs.coarse_ok) ? 1 : 0);
+            if (DUAL && CERT && kTeam == 1 && kPPT == 1 && bv.queue) {
+                // block-level compaction of the points the certificates do not settle:
+                // their searches run densely (thread t searches queue entry t), instead
+                // of every warp with one uncertified lane paying a whole search
+                __shared__ int s_qn;
+                __shared__ int s_qt[kLinBlock];
+                __shared__ float4 s_qs[kLinBlock];
+                __shared__ unsigned long long s_best[kLinBlock];
+                __shared__ int s_bj[kLinBlock], s_ovf[kLinBlock];
+                __shared__ float s_rho[kLinBlock];
+                if (threadIdx.x == 0) s_qn = 0;
+                __syncthreads();
+                const bool need = active && !cached;
+                const unsigned qm = __ballot_sync(0xffffffffu, need);
+                const int ln = threadIdx.x & 31;
+                const int leader = qm ? __ffs(qm) - 1 : 0;
+                int qb = 0;
+                if (qm && ln == leader) qb = atomicAdd(&s_qn, __popc(qm));
+                qb = __shfl_sync(0xffffffffu, qb, leader);
+                if (need) {
+                    const int slot = qb + __popc(qm & ((1u << ln) - 1u));
+                    s_qt[slot] = threadIdx.x;
+                    s_qs[slot] = make_float4(sx, sy, sz, 0.f);
+                }
+                __syncthreads();
+                const int qn = s_qn;
+                const int t = threadIdx.x;
+                if ((t & ~31) < qn) {  // warp-uniform: the warps holding queue entries
+                    const bool has = t < qn;
+                    const float4 qs = has ? s_qs[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    unsigned long long b2;
+                    int j2, o2;
+                    float rr;
+                    nn_search<CERT>(pts, lvs, has, qs.x, qs.y, qs.z, r2, b2, j2, o2, tl, rr,
+                                    (sP.coarse && lvs.coarse_ok) ? 1 : 0);
+                    if (has) {
+                        const int ow = s_qt[t];
+                        s_best[ow] = b2;
+                        s_bj[ow] = j2;
+                        s_ovf[ow] = o2;
+                        s_rho[ow] = rr;
+                    }
+                }
+                __syncthreads();
+                best = kEmptyKey;
+                bj = -1;
+                ovf = 0;
+                rho = -1.0f;
+                if (need) {
+                    best = s_best[threadIdx.x];
+                    bj = s_bj[threadIdx.x];
+                    ovf = s_ovf[threadIdx.x];
+                    rho = s_rho[threadIdx.x];
+                }
+            } else {
+                nn_search<CERT>(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho,
+                                (sP.coarse && lvs.coarse_ok) ? 1 : 0);
+            }
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
@@ -657,6 +713,12 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
                           const BatchView& bv, int64_t nb) {
     volatile float r2v = max_corr_dist * max_corr_dist;  // fp32 product
     const float r2 = r2v;
+    // block-level compaction of the uncertified searches (GICP_LIN_QUEUE=1): measured
+    // slower on the C4 batch (dual launch 1.96 -> 2.13 ms: most launches have many
+    // uncertified points, so the extra barriers and shared-memory traffic do not pay)
+    static const bool queue = getenv("GICP_LIN_QUEUE") && atoi(getenv("GICP_LIN_QUEUE")) == 1;
+    BatchView bvq = bv;
+    bvq.queue = queue ? 1 : 0;
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];
@@ -687,7 +749,7 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
     const bool dual = (flags & kLinDual) && !reuse && !eonly;
 #define GICP_LIN_ARGS                                                                                            \
     src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
-        done, out29, flag, seq, bv, scr.cache_new, scr.cache_old
+        done, out29, flag, seq, bvq, scr.cache_new, scr.cache_old
 #define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
     // certificates (gicp_align: sorted source, sorted-position correspondences)
