@@ -403,6 +403,36 @@ int gicp_submap_query(gicp_submap sm, int center, int radius, int32_t* out, int6
 void gicp_submap_free(gicp_submap sm);
 
 
+/* ---------------------------------------------------------------------------
+ * Query sharding of the external kNN (config C5 across GPUs, SURVEY.md §8(e):
+ * "queries sharded by cell-sorted ranges, map replicated ... rank 0 builds and
+ * ncclBroadcasts the sorted float4 + cell table").
+ *
+ * gicp_knn_query_order -- perm (device int32 [m]) = the queries in the order the
+ *   index's voxel grid sorts them (the order gicp_knn processes them in; non-finite
+ *   queries last). A rank takes a contiguous range of it.
+ * gicp_knn_subset -- gicp_knn restricted to the queries ids (device int32 [n_ids],
+ *   indices into q [m][3]); rows ids[t] of nbr / d2 ([m][k], device) are written,
+ *   the others untouched. Rows are bitwise those of gicp_knn (the per-query result
+ *   does not depend on the other queries).
+ * gicp_index_export -- the index's metadata as an opaque host header
+ *   (GICP_INDEX_HEADER_BYTES) and its device buffers (pointers and byte sizes,
+ *   GICP_INDEX_MAX_BUFFERS; a NULL pointer / 0 bytes: absent). The buffers stay
+ *   owned by the index. Attached covariances / voxel statistics are not exported.
+ * gicp_index_import -- a new index (owning copies) from a header and device
+ *   buffers laid out as exported (e.g. received by a broadcast); synchronous.
+ * ------------------------------------------------------------------------- */
+#define GICP_INDEX_HEADER_BYTES 4096
+#define GICP_INDEX_MAX_BUFFERS 16
+int gicp_knn_query_order(gicp_index idx, const float* q, int64_t m, int32_t* perm, void* stream);
+int gicp_knn_subset(gicp_index idx, const float* q, int64_t m, const int32_t* ids, int64_t n_ids, int k, int32_t* nbr,
+                    float* d2, void* stream);
+int gicp_index_export(gicp_index idx, void* header /* host [GICP_INDEX_HEADER_BYTES] */,
+                      void** buffers /* host [GICP_INDEX_MAX_BUFFERS] */, int64_t* bytes /* host [..] */,
+                      int* n_buffers /* host */);
+int gicp_index_import(const void* header /* host */, const void* const* buffers /* host array of device pointers */,
+                      void* stream, gicp_index* out);
+
 /* gicp_align_timing -- opt-in diagnostics (bench.py's roofline): while enabled,
  * gicp_align and the batched aligns record CUDA events on their stream around every
  * linearisation launch of the calling thread. The call returns, per kind ([0]

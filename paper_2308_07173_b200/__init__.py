@@ -96,12 +96,18 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 _lib.gicp_align_batched_sharded.argtypes = [_P, _P, _P, _i32, _P, _i32, _i32, _P, _P, _P, ctypes.POINTER(AlignParams),
                                             _P, _P, ALLREDUCE_FN, _P, _P]
 _lib.gicp_combine_chunks.argtypes = [_P, _i32, _i32, _i32, _P, _P]
+_lib.gicp_knn_query_order.argtypes = [_P, _P, _i64, _P, _P]
+_lib.gicp_knn_subset.argtypes = [_P, _P, _i64, _P, _i64, _i32, _P, _P, _P]
+_lib.gicp_index_export.argtypes = [_P, _P, _P, _P, ctypes.POINTER(ctypes.c_int)]
+_lib.gicp_index_import.argtypes = [_P, _P, _P, ctypes.POINTER(_P)]
+INDEX_HEADER_BYTES, INDEX_MAX_BUFFERS = 4096, 16
 
 EXPORTS = ["gicp_last_error", "gicp_version", "gicp_build_index", "gicp_index_free", "gicp_get_index_info",
            "gicp_index_attach_cov",
            "gicp_knn", "gicp_knn_self", "gicp_covariances", "gicp_knn_cov_self", "gicp_linearize", "gicp_align",
            "gicp_linearize_batched", "gicp_align_batched", "gicp_align_batched_ex", "gicp_align_batched_sharded",
-           "gicp_combine_chunks", "gicp_covariances_kd",
+           "gicp_combine_chunks", "gicp_knn_query_order", "gicp_knn_subset", "gicp_index_export",
+           "gicp_index_import", "gicp_covariances_kd",
            "gicp_index_attach_voxels", "gicp_linearize_vgicp", "gicp_align_vgicp", "gicp_ground_filter",
            "gicp_cluster", "gicp_submap_build", "gicp_submap_query", "gicp_submap_free", "gicp_align_timing"]
 
@@ -426,6 +432,45 @@ def combine_chunks(table: torch.Tensor, B: int, num_chunks: int, width: int, out
     out = out if out is not None else torch.empty((B, width), dtype=torch.float64, device=table.device)
     _check(_lib.gicp_combine_chunks(_dptr(table), int(B), int(num_chunks), int(width), _dptr(out), _stream()))
     return out
+
+
+def knn_query_order(index: Index, q: torch.Tensor) -> torch.Tensor:
+    """gicp_knn_query_order: the queries' cell-sorted order (int32 device [m])."""
+    q = _pts(q, "q")
+    perm = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
+    _check(_lib.gicp_knn_query_order(index.handle, _dptr(q), q.shape[0], _dptr(perm), _stream()))
+    return perm
+
+
+def knn_subset(index: Index, q: torch.Tensor, ids: torch.Tensor, k: int, out):
+    """gicp_knn_subset: rows ids of out = (nbr int32 [m, k], d2 float32 [m, k])."""
+    q = _pts(q, "q")
+    ids = ids.to(torch.int32).contiguous()
+    nbr, d2 = out
+    _check(_lib.gicp_knn_subset(index.handle, _dptr(q), q.shape[0], _dptr(ids) if ids.numel() else None, ids.numel(),
+                                int(k), _dptr(nbr), _dptr(d2), _stream()))
+    return nbr, d2
+
+
+def index_export(index: Index):
+    """gicp_index_export: (header bytes, [(device pointer or 0, bytes)] * n)."""
+    hdr = (ctypes.c_ubyte * INDEX_HEADER_BYTES)()
+    ptrs = (ctypes.c_void_p * INDEX_MAX_BUFFERS)()
+    nbytes = (ctypes.c_int64 * INDEX_MAX_BUFFERS)()
+    nb = ctypes.c_int(0)
+    _check(_lib.gicp_index_export(index.handle, ctypes.cast(hdr, _P), ctypes.cast(ptrs, _P), ctypes.cast(nbytes, _P),
+                                  ctypes.byref(nb)))
+    return bytes(hdr), [(int(ptrs[i] or 0), int(nbytes[i])) for i in range(nb.value)]
+
+
+def index_import(header: bytes, buffers, device) -> Index:
+    """gicp_index_import from a header and device tensors (uint8) laid out as exported."""
+    hdr = (ctypes.c_ubyte * INDEX_HEADER_BYTES).from_buffer_copy(header)
+    ptrs = (ctypes.c_void_p * INDEX_MAX_BUFFERS)(*[(b.data_ptr() if b is not None and b.numel() else None)
+                                                   for b in buffers])
+    h = ctypes.c_void_p()
+    _check(_lib.gicp_index_import(ctypes.cast(hdr, _P), ctypes.cast(ptrs, _P), _stream(), ctypes.byref(h)))
+    return Index(h, torch.device(device))
 
 
 def attach_voxels(index: Index, cov: torch.Tensor):

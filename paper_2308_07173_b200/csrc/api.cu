@@ -318,6 +318,129 @@ GICP_API void gicp_index_free(gicp_index idx) {
     delete idx;
 }
 
+static int check_k(int k, int64_t n, const char* fn);
+
+// ---- index export / import (C5 sharding: one rank builds, the others receive) -----------
+namespace {
+struct IndexHeader {
+    unsigned magic;
+    int n_levels;
+    int64_t n, n_cells, n_tiles1;
+    int64_t hash_cap[kMaxLevels];
+    int64_t adj_cap[2];
+    Grid lv[kMaxLevels];  // hash pointers stored as slot offsets into hash_mem
+    int64_t bytes[GICP_INDEX_MAX_BUFFERS];
+};
+static_assert(sizeof(IndexHeader) <= GICP_INDEX_HEADER_BYTES, "index header");
+constexpr unsigned kIndexMagic = 0x47494350u;  // "GICP"
+}  // namespace
+
+GICP_API int gicp_index_export(gicp_index idx, void* header, void** buffers, int64_t* bytes, int* n_buffers) {
+    if (!idx || !header || !buffers || !bytes || !n_buffers) return set_error(GICP_EINVAL, "gicp_index_export: null pointer");
+    IndexHeader h{};
+    h.magic = kIndexMagic;
+    h.n_levels = idx->n_levels;
+    h.n = idx->n;
+    h.n_cells = idx->n_cells;
+    h.n_tiles1 = idx->tiles1 ? idx->n_tiles1 : -1;
+    int64_t total = 0;
+    for (int l = 0; l < kMaxLevels; ++l) {
+        h.hash_cap[l] = idx->hash_cap[l];
+        h.lv[l] = idx->lv[l];
+        h.lv[l].hash = (const HashEntry*)(intptr_t)(l < idx->n_levels ? idx->lv[l].hash - idx->hash_mem : 0);
+        if (l < idx->n_levels) total += idx->hash_cap[l];
+    }
+    h.adj_cap[0] = idx->adj_rng ? idx->adj_cap[0] : 0;
+    h.adj_cap[1] = idx->adj_rng1 ? idx->adj_cap[1] : 0;
+    void* b[GICP_INDEX_MAX_BUFFERS] = {idx->pts, idx->pts_orig, idx->hash_mem, idx->adj_oc, idx->adj_rng, idx->adj_oc1,
+                                       idx->adj_rng1, idx->tiles1, idx->tile_of};
+    const int64_t n = idx->n;
+    const int64_t sz[GICP_INDEX_MAX_BUFFERS] = {
+        n * 16, n * 16, total * (int64_t)sizeof(HashEntry), idx->adj_oc ? n * 8 : 0, h.adj_cap[0] * 8,
+        idx->adj_oc1 ? n * 8 : 0, h.adj_cap[1] * 8, idx->tiles1 ? (idx->n_tiles1 + 1) * 4 : 0,
+        idx->tile_of ? n * 4 : 0};
+    const int nb = 9;
+    for (int i = 0; i < nb; ++i) {
+        buffers[i] = sz[i] ? b[i] : nullptr;
+        bytes[i] = sz[i];
+        h.bytes[i] = sz[i];
+    }
+    *n_buffers = nb;
+    std::memset(header, 0, GICP_INDEX_HEADER_BYTES);
+    std::memcpy(header, &h, sizeof(h));
+    return GICP_OK;
+}
+
+GICP_API int gicp_index_import(const void* header, const void* const* buffers, void* stream, gicp_index* out) {
+    if (!header || !buffers || !out) return set_error(GICP_EINVAL, "gicp_index_import: null pointer");
+    IndexHeader h;
+    std::memcpy(&h, header, sizeof(h));
+    if (h.magic != kIndexMagic || h.n_levels < 1 || h.n_levels > kMaxLevels || h.n <= 0)
+        return set_error(GICP_EINVAL, "gicp_index_import: not an index header");
+    init_pool_once();
+    cudaStream_t s = (cudaStream_t)stream;
+    gicp_index_s* idx = new gicp_index_s();
+    idx->n = h.n;
+    idx->n_cells = h.n_cells;
+    idx->n_levels = h.n_levels;
+    idx->stream = s;
+    cudaGetDevice(&idx->device);
+    void** dst[9] = {(void**)&idx->pts, (void**)&idx->pts_orig, (void**)&idx->hash_mem, (void**)&idx->adj_oc,
+                     (void**)&idx->adj_rng, (void**)&idx->adj_oc1, (void**)&idx->adj_rng1, (void**)&idx->tiles1,
+                     (void**)&idx->tile_of};
+    for (int i = 0; i < 9; ++i) {
+        if (!h.bytes[i]) continue;
+        if (!buffers[i]) {
+            gicp_index_free(idx);
+            return set_error(GICP_EINVAL, "gicp_index_import: missing buffer");
+        }
+        if (cudaMallocAsync(dst[i], h.bytes[i], s) != cudaSuccess ||
+            cudaMemcpyAsync(*dst[i], buffers[i], h.bytes[i], cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+            cudaGetLastError();
+            gicp_index_free(idx);
+            return set_error(GICP_ENOMEM, "gicp_index_import: allocation / copy failed");
+        }
+        idx->device_bytes += h.bytes[i];
+    }
+    for (int l = 0; l < kMaxLevels; ++l) {
+        idx->hash_cap[l] = h.hash_cap[l];
+        idx->lv[l] = h.lv[l];
+        idx->lv[l].hash = l < h.n_levels ? idx->hash_mem + (intptr_t)h.lv[l].hash : nullptr;
+    }
+    idx->adj_cap[0] = h.adj_cap[0];
+    idx->adj_cap[1] = h.adj_cap[1];
+    idx->n_tiles1 = h.n_tiles1 >= 0 ? h.n_tiles1 : 0;
+    int rc = check_cuda(cudaStreamSynchronize(s), "gicp_index_import");
+    if (rc) {
+        gicp_index_free(idx);
+        return rc;
+    }
+    *out = idx;
+    return GICP_OK;
+}
+
+GICP_API int gicp_knn_query_order(gicp_index idx, const float* q, int64_t m, int32_t* perm, void* stream) {
+    if (!idx) return set_error(GICP_EINVAL, "gicp_knn_query_order: null index");
+    if (m < 0 || m >= (1ll << 31) - 1) return set_error(GICP_EINVAL, "gicp_knn_query_order: m out of range");
+    if (m == 0) return GICP_OK;
+    if (!q || !perm) return set_error(GICP_EINVAL, "gicp_knn_query_order: null pointer");
+    init_pool_once();
+    return launch_query_order(idx, q, m, perm, (cudaStream_t)stream);
+}
+
+GICP_API int gicp_knn_subset(gicp_index idx, const float* q, int64_t m, const int32_t* ids, int64_t n_ids, int k,
+                             int32_t* nbr, float* d2, void* stream) {
+    if (!idx) return set_error(GICP_EINVAL, "gicp_knn_subset: null index");
+    if (m < 0 || m >= (1ll << 31) - 1 || n_ids < 0 || n_ids > m)
+        return set_error(GICP_EINVAL, "gicp_knn_subset: m / n_ids out of range");
+    int rc = check_k(k, idx->n, "gicp_knn_subset");
+    if (rc) return rc;
+    if (n_ids == 0) return GICP_OK;
+    if (!q || !ids || !nbr || !d2) return set_error(GICP_EINVAL, "gicp_knn_subset: null pointer");
+    init_pool_once();
+    return launch_knn_subset(idx, q, ids, n_ids, k, nbr, d2, (cudaStream_t)stream);
+}
+
 GICP_API int gicp_index_attach_cov(gicp_index idx, const float* cov, void* stream) {
     if (!idx || !cov) return set_error(GICP_EINVAL, "gicp_index_attach_cov: null pointer");
     init_pool_once();

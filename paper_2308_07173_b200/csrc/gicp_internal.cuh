@@ -175,6 +175,7 @@ struct gicp_index_s {
     int device = 0;
     cudaStream_t stream = nullptr;  // build stream: device memory is pool-allocated on it
     int64_t device_bytes = 0;
+    int64_t adj_cap[2] = {0, 0};  // int2 entries of adj_rng / adj_rng1
 };
 
 namespace gicp {
@@ -187,6 +188,9 @@ int check_cuda(cudaError_t e, const char* what);
 int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gicp_index* out);
 int launch_knn_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, cudaStream_t s);
 int launch_knn(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, cudaStream_t s);
+int launch_knn_subset(const gicp_index_s* idx, const float* q, const int* ids, int64_t n_ids, int k, int32_t* nbr,
+                      float* d2, cudaStream_t s);
+int launch_query_order(const gicp_index_s* idx, const float* q, int64_t m, int* perm, cudaStream_t s);
 // kernel-descriptor weighted covariance parameters (gicp_cov_params, device copy)
 struct CovKD {
     int kind;

@@ -552,6 +552,7 @@ int build_index(const float* xyz, int64_t n, float cell_size, cudaStream_t s, gi
                 cudaGetLastError();
                 return fail(set_error(GICP_ENOMEM, "adjacency allocation failed"));
             }
+            idx->adj_cap[l] = 27 * nv;
             // per level: [2l] output counter, [1] overflow flag (shared)
             k_adjacency<<<grid_for(nv * 32, kAdjBlock), kAdjBlock, 0, s>>>(
                 idx->lv[l], 3 * l, (unsigned long long*)keys.p, l == 0 ? heads : heads1, nheads + l,

@@ -932,6 +932,36 @@ int run_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2,
     return run_queries<KCAP>(idx, nullptr, nullptr, idx->n, k, eps, nbr, d2, cov, s);
 }
 
+// the cell-sorted order of external queries (the order run_ext processes them in)
+int query_order(const gicp_index_s* idx, const float* q, int64_t m, int* perm, cudaStream_t s) {
+    Scratch keys_in, keys_out, vals_in, temp;
+    int rc;
+    if ((rc = keys_in.alloc(m * 8, s)) || (rc = keys_out.alloc(m * 8, s)) || (rc = vals_in.alloc(m * 4, s))) return rc;
+    auto bits_for = [](int d) {
+        int b = 0;
+        while ((1 << b) < d) ++b;
+        return b;
+    };
+    const Grid& g0 = idx->lv[0];
+    const int bits = std::max(1, 3 * std::max(bits_for(g0.nx), std::max(bits_for(g0.ny), bits_for(g0.nz))));
+    const unsigned long long empty = bits >= 64 ? kEmptyKey : (1ull << bits) - 1ull;
+    k_query_keys<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(q, m, g0, empty, (unsigned long long*)keys_in.p,
+                                                              (int*)vals_in.p);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned long long*)keys_in.p, (unsigned long long*)keys_out.p,
+                                    (int*)vals_in.p, perm, (int)m, 0, bits, s);
+    if ((rc = temp.alloc(tb, s))) return rc;
+    cub::DeviceRadixSort::SortPairs(temp.p, tb, (unsigned long long*)keys_in.p, (unsigned long long*)keys_out.p,
+                                    (int*)vals_in.p, perm, (int)m, 0, bits, s);
+    return check_cuda(cudaGetLastError(), "query order");
+}
+
+template <int KCAP>
+int run_subset(const gicp_index_s* idx, const float* q, const int* ids, int64_t n_ids, int k, int32_t* nbr, float* d2,
+               cudaStream_t s) {
+    return run_queries<KCAP>(idx, q, ids, n_ids, k, 0.f, nbr, d2, nullptr, s);
+}
+
 template <int KCAP>
 int run_ext(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, cudaStream_t s) {
     Scratch keys_in, keys_out, vals_in, perm, temp;
@@ -979,6 +1009,15 @@ int launch_knn_self(const gicp_index_s* idx, int k, float eps, int32_t* nbr, flo
 
 int launch_knn(const gicp_index_s* idx, const float* q, int64_t m, int k, int32_t* nbr, float* d2, cudaStream_t s) {
     GICP_KCAP_DISPATCH(k, (run_ext<KC>(idx, q, m, k, nbr, d2, s)));
+}
+
+int launch_knn_subset(const gicp_index_s* idx, const float* q, const int* ids, int64_t n_ids, int k, int32_t* nbr,
+                      float* d2, cudaStream_t s) {
+    GICP_KCAP_DISPATCH(k, (run_subset<KC>(idx, q, ids, n_ids, k, nbr, d2, s)));
+}
+
+int launch_query_order(const gicp_index_s* idx, const float* q, int64_t m, int* perm, cudaStream_t s) {
+    return query_order(idx, q, m, perm, s);
 }
 
 }  // namespace gicp

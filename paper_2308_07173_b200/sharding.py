@@ -131,3 +131,74 @@ def align_batched_sharded(g, src, src_cov, offsets, tgt, tgt_cov, T0s, group=Non
         cov_l = torch.zeros((0, 6), dtype=src_cov.dtype, device=src_cov.device)
     return g.align_batched_sharded(src_l, cov_l, plan.loffs, plan.gid, plan.num_chunks, plan.B, tgt, tgt_cov, T0s,
                                    allreduce=make_allreduce(plan.group), **params)
+
+
+# ---------------------------------------------------------------------------
+# Query sharding of the external kNN (config C5)
+# ---------------------------------------------------------------------------
+
+class _DevBytes:
+    """A uint8 view of a device allocation the library owns (for the collective)."""
+
+    def __init__(self, ptr: int, nbytes: int, device):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+        self.device = device
+
+
+def broadcast_index(g, index, src: int = 0, group=None, device=None):
+    """The index built once on rank `src` and broadcast to every rank (its header as a
+    host object, its device buffers over NCCL); the other ranks import owning copies.
+    `index` is the built index on `src` (ignored elsewhere). Returns this rank's index."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return index
+    if rank == src:
+        header, bufs = g.index_export(index)
+        meta = [header, [nb for _, nb in bufs]]
+    else:
+        meta = [None, None]
+    dist.broadcast_object_list(meta, src=src, group=group)
+    header, sizes = meta
+    dev = device if device is not None else (index.device if rank == src else torch.device("cuda"))
+    tensors = []
+    for i, nb in enumerate(sizes):
+        if nb == 0:
+            tensors.append(None)
+            continue
+        if rank == src:
+            t = torch.as_tensor(_DevBytes(bufs[i][0], nb, dev), device=dev)
+        else:
+            t = torch.empty(nb, dtype=torch.uint8, device=dev)
+        if dist.get_backend(group) == "nccl":
+            dist.broadcast(t, src=src, group=group)
+        else:  # gloo (CPU test runs): through host memory
+            h = t.cpu()
+            dist.broadcast(h, src=src, group=group)
+            t.copy_(h)
+        tensors.append(t)
+    if rank == src:
+        return index
+    return g.index_import(header, tensors, dev)
+
+
+def knn_sharded(g, index, q, k: int, group=None, gather: bool = False):
+    """External kNN with the queries sharded by contiguous ranges of their cell-sorted
+    order (gicp_knn_query_order; spatially coherent shards) over the ranks. Returns
+    (nbr, d2, ids): this rank's rows are filled (the others zero) unless gather, which
+    adds the shards together with one allreduce (exact: one contributor per row)."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    m = q.shape[0]
+    perm = g.knn_query_order(index, q)
+    lo, hi = (m * rank) // world, (m * (rank + 1)) // world
+    ids = perm[lo:hi].contiguous()
+    nbr = torch.zeros((m, k), dtype=torch.int32, device=q.device)
+    d2 = torch.zeros((m, k), dtype=torch.float32, device=q.device)
+    g.knn_subset(index, q, ids, k, (nbr, d2))
+    if gather and world > 1:
+        ar = make_allreduce(group)
+        ar_nbr = nbr.to(torch.float64)  # exact for indices < 2^53
+        ar(ar_nbr)
+        ar(d2)
+        nbr = ar_nbr.to(torch.int32)
+    return nbr, d2, ids

@@ -137,3 +137,64 @@ def test_sharded_linearize_world1():
     b = b.cpu().numpy()
     assert a[28] == b[28]
     assert np.allclose(a[:28], b[:28], rtol=1e-9, atol=1e-9 * np.abs(b[:28]).max())
+
+
+# --- C5: query sharding over cell-sorted ranges, the index broadcast from rank 0 ---
+
+def _c5_problem():
+    sys.path.insert(0, ROOT)
+    import gen
+    mp = gen.racetrack_map(300_000, 3)
+    sc, T = gen.scan(20_000, 700.0, 2001)
+    q = gen.apply_T(T, sc).astype(np.float32)
+    return mp, np.ascontiguousarray(q)
+
+
+def _c5_worker(rank, world, port, q_out):
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    import paper_2308_07173_b200 as g
+    from paper_2308_07173_b200 import sharding
+    mp, q = _c5_problem()
+    dev = torch.device("cuda:0")
+    idx = g.build_index(torch.from_numpy(mp).to(dev), 0.4) if rank == 0 else None
+    idx = sharding.broadcast_index(g, idx, src=0, device=dev)
+    qd = torch.from_numpy(q).to(dev)
+    nbr, d2, ids = sharding.knn_sharded(g, idx, qd, 32, gather=True)
+    q_out.put((rank, nbr.cpu().numpy(), d2.cpu().numpy(), ids.cpu().numpy()))
+    dist.destroy_process_group()
+
+
+def test_c5_query_sharding_with_broadcast_index():
+    """Rank 0 builds the map index and broadcasts it; each rank takes a contiguous
+    range of the cell-sorted queries; the gathered rows are bitwise gicp_knn's."""
+    sys.path.insert(0, ROOT)
+    import paper_2308_07173_b200 as g
+    mp, q = _c5_problem()
+    dev = torch.device("cuda:0")
+    idx = g.build_index(torch.from_numpy(mp).to(dev), 0.4)
+    qd = torch.from_numpy(q).to(dev)
+    ref_n, ref_d = g.knn(idx, qd, 32)
+    ref_n, ref_d = ref_n.cpu().numpy(), ref_d.cpu().numpy()
+    # export / import in one process: the copy answers identically
+    hdr, bufs = g.index_export(idx)
+    import paper_2308_07173_b200.sharding as sh
+    ts = [None if nb == 0 else torch.as_tensor(sh._DevBytes(p, nb, dev), device=dev).clone() for p, nb in bufs]
+    idx2 = g.index_import(hdr, ts, dev)
+    n2, d22 = g.knn(idx2, qd, 32)
+    assert np.array_equal(n2.cpu().numpy(), ref_n) and np.array_equal(d22.cpu().numpy(), ref_d)
+    ctx = mp_ctx = torch.multiprocessing.get_context("spawn")
+    qq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c5_worker, args=(r, 2, port, qq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (n, d, i)) for r, n, d, i in (qq.get(timeout=240) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        assert np.array_equal(res[r][0], ref_n) and np.array_equal(res[r][1], ref_d)
+    ids = np.sort(np.concatenate([res[0][2], res[1][2]]))
+    assert np.array_equal(ids, np.arange(len(q)))

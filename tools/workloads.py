@@ -99,9 +99,18 @@ def c5():
     ms_knn, _ = timed(lambda: g.knn(idx, qd, 32, out=(nbr, d2)))
     ms_cov, _ = timed(lambda: g.covariances(mpd, nbr, 1e-3, out=cov))
     m = q.shape[0]
+    # algorithmic bytes: 12 + 12k + 24 per external query plus 28 B per
+    # distinct map point the neighbour sets touch (16 B float4 + 12 B xyz for the covariance)
+    uniq = int(torch.unique(nbr).numel())
+    alg = m * (12 + 12 * 32 + 24) + 28 * uniq
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6650.0
+    ach = alg / ((ms_knn + ms_cov) * 1e-3) / 1e9
     print(json.dumps({"workload": "C5 20M multi-lap map, 1M queries, k=32", "index_build_ms": ms_build,
                       "knn_ms": ms_knn, "cov_ms": ms_cov, "knn_cov_pts_per_s": 1e3 * m / (ms_knn + ms_cov),
-                      "gen_s": gen_s}))
+                      "algorithmic_bytes": alg, "distinct_map_points": uniq, "achieved_GBps": ach,
+                      "roofline_frac": ach / peak, "gen_s": gen_s}))
 
 
 
