@@ -245,7 +245,6 @@ struct BatchView {
     int n_scans = 1;
     int n_active = 1;
     int out_stride = 0;
-    int queue = 0;  // DUAL+CERT: compact the uncertified searches per block (GICP_LIN_QUEUE=1)
 };
 
 struct LinScratch {

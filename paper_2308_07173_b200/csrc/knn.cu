@@ -563,14 +563,29 @@ struct Levels {
 // the tiled level-0 stage for self queries (knn_tile.cuh): K = 10 and 20 (the
 // configs' k); returns false when it does not apply (then the per-query kernel runs)
 bool launch_tile(const gicp_index_s* idx, int k, float eps, int32_t* nbr, float* d2, float* cov, int* counts,
-                 int* listA, int* listB, int2* exact, cudaStream_t s) {
+                 int* listA, int* listB, int2* exact, cudaStream_t s, const float* qext = nullptr,
+                 const int* perm = nullptr, int64_t m = 0) {
     static const bool off = getenv("GICP_KNN_TILE") && atoi(getenv("GICP_KNN_TILE")) == 0;
-    if (off || idx->tiles1 == nullptr || idx->tile_of == nullptr || idx->n == 0 || (k != 10 && k != 20)) return false;
+    if (off || idx->tiles1 == nullptr || idx->tile_of == nullptr || idx->n == 0) return false;
     // the staged boxes pay off on dense, even clouds (the C3 map: ~35 points per
     // level-1 voxel); sparse, uneven ones (a scan's 1/r^2 falloff) run per query
     if (idx->n < 24 * idx->n_tiles1) return false;
+    if (qext) {  // external queries in their cell-sorted order (perm)
+        if (!perm || m <= 0 || (k != 10 && k != 20 && k != 32)) return false;
+        const unsigned grid = (unsigned)((m + kTB - 1) / kTB);
+#define GICP_TILE_EXT(KK)                                                                                         \
+    k_knn_tile<KK, false, true><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, m, eps, nbr, \
+                                                     d2, nullptr, counts + 2, listA, counts + 0, exact, counts + 3,  \
+                                                     listB, qext, perm)
+        if (k == 32) GICP_TILE_EXT(32);
+        else if (k == 20) GICP_TILE_EXT(20);
+        else GICP_TILE_EXT(10);
+#undef GICP_TILE_EXT
+        return true;
+    }
+    if (perm || (k != 10 && k != 20)) return false;
     const unsigned grid = (unsigned)((idx->n + kTB - 1) / kTB);
-    static const bool rows = !(getenv("GICP_KNN_ROWS") && atoi(getenv("GICP_KNN_ROWS")) == 0);
+    static const bool rows = getenv("GICP_KNN_ROWS") && atoi(getenv("GICP_KNN_ROWS")) == 1;
 #define GICP_TILE_LAUNCH(KK, RR)                                                                                  \
     k_knn_tile<KK, RR><<<grid, kTB, 0, s>>>(idx->pts, idx->lv[0], idx->tiles1, idx->tile_of, idx->n, eps, nbr, d2, \
                                             cov, counts + 2, listA, counts + 0, exact, counts + 3, listB)
@@ -879,8 +894,7 @@ int run_queries(const gicp_index_s* idx, const float* qext, const int* perm, int
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = idx->lv[l < L ? l : L - 1];
     // level 0 over every query, then one launch that climbs the pyramid for the rest
     const AdjView adj{idx->adj_oc, idx->adj_rng, idx->adj_oc1, idx->adj_rng1};
-    if (qext == nullptr && perm == nullptr && L > 1 &&
-        launch_tile(idx, k, eps, nbr, d2, cov, counts, listA, listB, exact, s)) {
+    if (L > 1 && launch_tile(idx, k, eps, nbr, d2, cov, counts, listA, listB, exact, s, qext, perm, m)) {
         // tiles too dense to stage: the per-query level-0 kernel over their points
         k_knn_level<KCAP><<<some_blocks, kBlock, shmem, s>>>(src, adj, idx->lv[0], nullptr, m, listB, counts + 3, k, eps,
                                                              nbr, d2, cov, counts + 2, listA, counts + 0, exact, 0);

@@ -59,6 +59,23 @@ constexpr OuterCells make_outer_cells() {
     return o;
 }
 __constant__ OuterCells c_outer = make_outer_cells();
+// all 64 box cells, the tile's own 2x2x2 first (then nearest-first): external queries
+struct BoxCells {
+    signed char d[64][3];
+};
+constexpr BoxCells make_box_cells() {
+    BoxCells b{};
+    const OuterCells o = make_outer_cells();
+    for (int i = 0; i < 8; ++i) {
+        b.d[i][0] = (signed char)(i & 1);
+        b.d[i][1] = (signed char)((i >> 1) & 1);
+        b.d[i][2] = (signed char)(i >> 2);
+    }
+    for (int i = 0; i < 56; ++i)
+        for (int a = 0; a < 3; ++a) b.d[8 + i][a] = o.d[i][a];
+    return b;
+}
+__constant__ BoxCells c_box = make_box_cells();
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -125,29 +142,81 @@ __device__ __forceinline__ bool exact_less(const float4& q, const float4& a, con
 // voxels of the box, staged in (z, y, x) order so every row is contiguous) and the
 // stop rule uses that cube; the block's lanes are regrouped by the parity of their
 // voxel (the same relative rows), so a warp's lanes step through the same rows.
-template <int K, bool ROWS>
+// EXT: external queries (gicp_knn): the block's 128 queries are consecutive in their
+// cell-sorted order (perm); a "tile" is each distinct level-1 voxel of their (clamped)
+// cells, its whole 4x4x4 box probed and staged, the tile's own 2x2x2 first; rows go
+// to the queries' original indices, no covariance. Non-finite queries: per-query path.
+template <int K, bool ROWS, bool EXT = false>
 __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* __restrict__ pts, Grid g0,
                                                   const int* __restrict__ tiles, const int* __restrict__ tile_of,
                                                   int64_t n, float eps, int32_t* __restrict__ nbr,
                                                   float* __restrict__ d2out, float* __restrict__ cov,
                                                   int* __restrict__ esc_count, int* __restrict__ esc_list,
                                                   int* __restrict__ exact_count, int2* __restrict__ exact_list,
-                                                  int* __restrict__ fb_count, int* __restrict__ fb_list) {
+                                                  int* __restrict__ fb_count, int* __restrict__ fb_list,
+                                                  const float* __restrict__ qext = nullptr,
+                                                  const int* __restrict__ perm = nullptr) {
+    static_assert(!(ROWS && EXT), "external queries use the box scan");
     constexpr int NL = K + 1;
     __shared__ __align__(128) float4 cand[kBlkCap + kTileCap + 4];
     __shared__ unsigned buf[kTileBuf][kTB];
-    constexpr int NR = ROWS ? 64 : 57;  // staged ranges per tile
+    constexpr int NR = (ROWS || EXT) ? 64 : 57;  // staged ranges per tile
     __shared__ int2 rng[kBlkTiles][NR];
     __shared__ int cell_off[ROWS ? kBlkTiles : 1][65];  // ROWS: box cell starts in cand, then the end
     __shared__ int s_order[ROWS ? kTB : 1], s_pc[8];
+    __shared__ unsigned long long s_l1[EXT ? kTB : 1];
+    __shared__ int s_run[EXT ? kTB : 1], s_wst[kTB / 32];
     __shared__ int t_off[kBlkTiles], t_cnt[kBlkTiles], t_start[kBlkTiles], t_base[kBlkTiles][3];
     __shared__ __align__(8) unsigned long long bar;
     __shared__ int s_ta, s_nt, s_ok;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t q0 = (int64_t)blockIdx.x * kTB, q = q0 + tid;
-    const bool act = q < n;
-    if (tid == 0) {
-        mbar_init(&bar, 1);
+    const bool act = q < n;  // EXT: n = the number of queries
+    // EXT: this lane's query
+    int qid = (int)q;
+    float ex = 0.f, ey = 0.f, ez = 0.f;
+    bool efin = false;
+    if (EXT && act) {
+        qid = __ldg(perm + q);
+        ex = __ldg(qext + 3 * (int64_t)qid);
+        ey = __ldg(qext + 3 * (int64_t)qid + 1);
+        ez = __ldg(qext + 3 * (int64_t)qid + 2);
+        efin = isfinite(ex) && isfinite(ey) && isfinite(ez);
+    }
+    if (tid == 0) mbar_init(&bar, 1);
+    if constexpr (EXT) {
+        // runs of equal level-1 voxels (clamped cells, the sort's key) = the tiles
+        unsigned long long k1 = ~0ull;
+        int cx = 0, cy = 0, cz = 0;
+        if (efin) {
+            cx = min(max(cell_coord(ex, g0.ox, g0.inv_cell), 0), g0.nx - 1);
+            cy = min(max(cell_coord(ey, g0.oy, g0.inv_cell), 0), g0.ny - 1);
+            cz = min(max(cell_coord(ez, g0.oz, g0.inv_cell), 0), g0.nz - 1);
+            k1 = cell_key(cx >> 1, cy >> 1, cz >> 1);
+        }
+        s_l1[tid] = k1;
+        __syncthreads();
+        const bool st = efin && (tid == 0 || s_l1[tid - 1] != k1);
+        const unsigned bm = __ballot_sync(0xffffffffu, st);
+        if (lane == 0) s_wst[warp] = __popc(bm);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int w = 0; w < kTB / 32; ++w) {
+            if (w < warp) before += s_wst[w];
+            tot += s_wst[w];
+        }
+        const int r = before + __popc(bm & ((2u << lane) - 1u)) - 1;  // this lane's run
+        if (st && r < kBlkTiles) {
+            t_base[r][0] = cx & ~1;
+            t_base[r][1] = cy & ~1;
+            t_base[r][2] = cz & ~1;
+        }
+        s_run[tid] = r;
+        if (tid == 0) {
+            s_ta = 0;
+            s_nt = tot;
+        }
+    } else if (tid == 0) {
         const int ta = __ldg(tile_of + q0), tb = __ldg(tile_of + min(q0 + kTB, n) - 1);
         s_ta = ta;
         s_nt = tb - ta + 1;
@@ -155,21 +224,35 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     const int ta = s_ta, nt = s_nt;
-    auto fallback_all = [&]() { push_warp(fb_count, fb_list, act, (int)q); };
+    auto fallback_all = [&]() { push_warp(fb_count, fb_list, EXT ? (act && efin) : act, qid); };
+    if (EXT) push_warp(fb_count, fb_list, act && !efin, qid);  // non-finite: the per-query path
     if (nt > kBlkTiles) {  // sparse region: many tiny tiles
         fallback_all();
         return;
     }
     // (1) per tile (warp w: tiles w, w + 4): the ranges of its box
     for (int lt = warp; lt < nt; lt += kTB / 32) {
-        const int t = ta + lt;
-        const int s1 = __ldg(tiles + t), e1 = __ldg(tiles + t + 1);
-        const float4 f0 = __ldg(pts + s1);
-        const int bx = cell_coord(f0.x, g0.ox, g0.inv_cell) & ~1;
-        const int by = cell_coord(f0.y, g0.oy, g0.inv_cell) & ~1;
-        const int bz = cell_coord(f0.z, g0.oz, g0.inv_cell) & ~1;
+        int s1 = 0, e1 = 0, bx, by, bz;
+        if constexpr (EXT) {
+            bx = t_base[lt][0];
+            by = t_base[lt][1];
+            bz = t_base[lt][2];
+        } else {
+            const int t = ta + lt;
+            s1 = __ldg(tiles + t);
+            e1 = __ldg(tiles + t + 1);
+            const float4 f0 = __ldg(pts + s1);
+            bx = cell_coord(f0.x, g0.ox, g0.inv_cell) & ~1;
+            by = cell_coord(f0.y, g0.oy, g0.inv_cell) & ~1;
+            bz = cell_coord(f0.z, g0.oz, g0.inv_cell) & ~1;
+        }
         int2 ra, rb = make_int2(0, 0);
-        if constexpr (ROWS) {  // box cell ci = (z * 4 + y) * 4 + x, offsets -1..2 per axis
+        if constexpr (EXT) {  // all 64 box cells, the tile's own first
+            const signed char* d = c_box.d[lane];
+            const signed char* e = c_box.d[lane + 32];
+            ra = cell_lookup(g0, bx + d[0], by + d[1], bz + d[2]);
+            rb = cell_lookup(g0, bx + e[0], by + e[1], bz + e[2]);
+        } else if constexpr (ROWS) {  // box cell ci = (z * 4 + y) * 4 + x, offsets -1..2 per axis
             ra = cell_lookup(g0, bx - 1 + (lane & 3), by - 1 + ((lane >> 2) & 3), bz - 1 + (lane >> 4));
             const int c2 = lane + 32;
             rb = cell_lookup(g0, bx - 1 + (c2 & 3), by - 1 + ((c2 >> 2) & 3), bz - 1 + (c2 >> 4));
@@ -182,7 +265,7 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
             }
         }
         const int ca = max(ra.y - ra.x, 0), cb = max(rb.y - rb.x, 0);
-        if constexpr (ROWS) {
+        if constexpr (ROWS || EXT) {
             rng[lt][lane] = make_int2(ra.x, ca);
             rng[lt][32 + lane] = make_int2(rb.x, cb);
         } else {
@@ -191,8 +274,8 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
         }
         const int tot = __reduce_add_sync(0xffffffffu, ca + cb);
         if (lane == 0) {
-            if (!ROWS) rng[lt][0] = make_int2(s1, e1 - s1);
-            t_cnt[lt] = (ROWS ? 0 : e1 - s1) + tot;
+            if (!ROWS && !EXT) rng[lt][0] = make_int2(s1, e1 - s1);
+            t_cnt[lt] = ((ROWS || EXT) ? 0 : e1 - s1) + tot;
             t_start[lt] = s1;
             t_base[lt][0] = bx;
             t_base[lt][1] = by;
@@ -265,13 +348,13 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
     float4 qp = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nq = (int)min((int64_t)kTB, n - q0);
     const int me = ROWS ? (tid < nq ? s_order[tid] : tid) : tid;  // the lane's query (block-relative)
-    const int64_t qq = q0 + me;
-    const bool on = ROWS ? tid < nq : act;
+    const int64_t qq = EXT ? (int64_t)qid : q0 + me;               // its id in the lists / rows
+    const bool on = ROWS ? tid < nq : (EXT ? act && efin : act);
     if (on) {
-        lt = __ldg(tile_of + qq) - ta;
+        lt = EXT ? s_run[tid] : __ldg(tile_of + qq) - ta;
         base = t_off[lt];
         C = t_cnt[lt];
-        qp = ROWS ? __ldg(pts + qq) : cand[base + (int)(qq - t_start[lt])];
+        qp = EXT ? make_float4(ex, ey, ez, 0.f) : (ROWS ? __ldg(pts + qq) : cand[base + (int)(qq - t_start[lt])]);
     }
     unsigned T[NL];
     unsigned* col = &buf[0][tid];
@@ -323,7 +406,10 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
             }
         }
     } else {
-        constexpr net::Net sn = net::make_sort_net<kTileFirst, NL>();
+        // (K = 32: the list has 33 places and the first sort 32 keys; the last place
+        // starts empty)
+        constexpr int NF = NL < kTileFirst ? NL : kTileFirst;
+        constexpr net::Net sn = net::make_sort_net<kTileFirst, NF>();
         unsigned v[kTileFirst];
 #pragma unroll
         for (int i = 0; i < kTileFirst; ++i) {
@@ -335,7 +421,7 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
         }
         GICP_APPLY_NET(v, sn);
 #pragma unroll
-        for (int i = 0; i < NL; ++i) T[i] = v[sn.out[i]];
+        for (int i = 0; i < NL; ++i) T[i] = i < NF ? v[sn.out[i]] : 0xffffffffu;
     unsigned thr = T[NL - 1] | kSlotMask;
     const int cmax = __reduce_max_sync(0xffffffffu, C);
     for (int c = kTileFirst; c < cmax; c += 4) {
@@ -467,7 +553,7 @@ __global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* 
     push_warp2(exact_count, exact_list, on && st == 2, make_int2((int)qq, 0));
     if (!on || st != 0) return;
     // (5) emit: original indices, exact d2, covariance of the K neighbours
-    const int64_t row = __float_as_int(qp.w);
+    const int64_t row = EXT ? (int64_t)qid : (int64_t)__float_as_int(qp.w);
     const float4 p0 = cand[base + (int)(T[0] & kSlotMask) - 1];
     float sx = 0.f, sy = 0.f, sz = 0.f;
     // rows written 4 (K % 4 == 0), 2 or 1 values at a time as they are formed

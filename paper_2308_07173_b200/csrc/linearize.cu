@@ -24,6 +24,9 @@
 namespace gicp {
 namespace {
 
+#ifndef GICP_LIN_FLAT
+#define GICP_LIN_FLAT 0  // 1: flattened per-lane candidate stream in the level-0 cube stage
+#endif
 constexpr int kLinBlock = 256;
 constexpr int kPPT = 1;                       // points per team
 constexpr int kTeam = GICP_LIN_TEAM;          // lanes per point (adjacent lanes of a warp)
@@ -174,11 +177,56 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         // survives scan it together (inner loop = the longest surviving range).
         // Nearest-first order makes almost every voxel after the own one prunable.
         const int cnt = use_adj ? a1 - a0 : nr;
+#if GICP_LIN_FLAT
+        // flattened, per lane: one candidate stream over the lane's surviving voxels
+        // (the same voxels in the same order as the entry-major loop below, so the
+        // same result bitwise); the warp steps max over lanes of their stream length
+        // instead of the sum over entries of per-entry maxima
+        if (kTeam == 1) {
+            int ri = 0, pos = 0, end = 0;
+            int2 ne = make_int2(0, 0);
+            if (active && use_adj && cnt > 0) ne = __ldg(adj_rng + a0);
+            float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
+            while (true) {
+                while (active && pos == end && ri < cnt) {
+                    int2 r;
+                    float lb2;
+                    if (use_adj) {
+                        const int2 e = ne;
+                        if (ri + 1 < cnt) ne = __ldg(adj_rng + a0 + ri + 1);
+                        r = adj_range(e);
+                        lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
+                    } else {
+                        r = rl[ri];
+                        lb2 = lbl[ri];
+                    }
+                    ++ri;
+                    if (lb2 * kRel > bound()) {
+                        if (CERT) lbp = fminf(lbp, lb2);
+                        continue;
+                    }
+                    pos = r.x;
+                    end = r.y;
+                    if (pos < end) pn = __ldg(pts + pos);
+                }
+                const bool has = active && pos < end;
+                if (!__any_sync(0xffffffffu, has)) break;
+                if (has) {
+                    const float4 p = pn;
+                    if (pos + 1 < end) pn = __ldg(pts + pos + 1);
+                    consider_p(pos, p);
+                    ++pos;
+                }
+            }
+        }
+        const int kmax = kTeam == 1 ? 0 : __reduce_max_sync(0xffffffffu, active ? cnt : 0);
+#else
         const int kmax = __reduce_max_sync(0xffffffffu, active ? cnt : 0);
+#endif
         // the next entry is loaded one entry ahead; candidates go kUnroll at a time
         // (independent loads in flight together: the search is latency-bound)
         int2 ne = make_int2(0, 0);
-        if (use_adj && cnt > 0) ne = __ldg(adj_rng + a0);
+        if (use_adj && cnt > 0 && kmax > 0) ne = __ldg(adj_rng + a0);
         for (int k = 0; k < kmax; ++k) {
             int2 r = make_int2(0, 0);
             if (k < cnt) {
@@ -451,64 +499,8 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             int bj, ovf;
             float rho;
             LPROF(const long long t0 = clock64();)
-            if (DUAL && CERT && kTeam == 1 && kPPT == 1 && bv.queue) {
-                // block-level compaction of the points the certificates do not settle:
-                // their searches run densely (thread t searches queue entry t), instead
-                // of every warp with one uncertified lane paying a whole search
-                __shared__ int s_qn;
-                __shared__ int s_qt[kLinBlock];
-                __shared__ float4 s_qs[kLinBlock];
-                __shared__ unsigned long long s_best[kLinBlock];
-                __shared__ int s_bj[kLinBlock], s_ovf[kLinBlock];
-                __shared__ float s_rho[kLinBlock];
-                if (threadIdx.x == 0) s_qn = 0;
-                __syncthreads();
-                const bool need = active && !cached;
-                const unsigned qm = __ballot_sync(0xffffffffu, need);
-                const int ln = threadIdx.x & 31;
-                const int leader = qm ? __ffs(qm) - 1 : 0;
-                int qb = 0;
-                if (qm && ln == leader) qb = atomicAdd(&s_qn, __popc(qm));
-                qb = __shfl_sync(0xffffffffu, qb, leader);
-                if (need) {
-                    const int slot = qb + __popc(qm & ((1u << ln) - 1u));
-                    s_qt[slot] = threadIdx.x;
-                    s_qs[slot] = make_float4(sx, sy, sz, 0.f);
-                }
-                __syncthreads();
-                const int qn = s_qn;
-                const int t = threadIdx.x;
-                if ((t & ~31) < qn) {  // warp-uniform: the warps holding queue entries
-                    const bool has = t < qn;
-                    const float4 qs = has ? s_qs[t] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    unsigned long long b2;
-                    int j2, o2;
-                    float rr;
-                    nn_search<CERT>(pts, lvs, has, qs.x, qs.y, qs.z, r2, b2, j2, o2, tl, rr,
-                                    (sP.coarse && lvs.coarse_ok) ? 1 : 0);
-                    if (has) {
-                        const int ow = s_qt[t];
-                        s_best[ow] = b2;
-                        s_bj[ow] = j2;
-                        s_ovf[ow] = o2;
-                        s_rho[ow] = rr;
-                    }
-                }
-                __syncthreads();
-                best = kEmptyKey;
-                bj = -1;
-                ovf = 0;
-                rho = -1.0f;
-                if (need) {
-                    best = s_best[threadIdx.x];
-                    bj = s_bj[threadIdx.x];
-                    ovf = s_ovf[threadIdx.x];
-                    rho = s_rho[threadIdx.x];
-                }
-            } else {
-                nn_search<CERT>(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho,
-                                (sP.coarse && lvs.coarse_ok) ? 1 : 0);
-            }
+            nn_search<CERT>(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho,
+                            (sP.coarse && lvs.coarse_ok) ? 1 : 0);
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
@@ -713,12 +705,7 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
                           const BatchView& bv, int64_t nb) {
     volatile float r2v = max_corr_dist * max_corr_dist;  // fp32 product
     const float r2 = r2v;
-    // block-level compaction of the uncertified searches (GICP_LIN_QUEUE=1): measured
-    // slower on the C4 batch (dual launch 1.96 -> 2.13 ms: most launches have many
-    // uncertified points, so the extra barriers and shared-memory traffic do not pay)
-    static const bool queue = getenv("GICP_LIN_QUEUE") && atoi(getenv("GICP_LIN_QUEUE")) == 1;
-    BatchView bvq = bv;
-    bvq.queue = queue ? 1 : 0;
+    const BatchView& bvq = bv;
     Levels lvs;
     lvs.n = tgt->n_levels;
     for (int l = 0; l < kMaxLevels; ++l) lvs.lv[l] = tgt->lv[l < lvs.n ? l : lvs.n - 1];

@@ -127,6 +127,7 @@ constexpr int oe_sort(Net& t, const int* A, int n, int* out) {
 
 template <int N, int NOUT>
 constexpr Net make_sort_net() {
+    static_assert(NOUT <= N && N <= kMaxWires, "sort_net: NOUT <= N");
     Net t{};
     int A[kMaxWires] = {}, out[kMaxWires] = {};
     for (int i = 0; i < N; ++i) A[i] = i;
@@ -139,6 +140,7 @@ constexpr Net make_sort_net() {
 
 template <int M, int B, int NOUT>
 constexpr Net make_merge_net() {
+    static_assert(NOUT <= M + B && M + B <= kMaxWires, "merge_net: NOUT <= M + B");
     Net t{};
     int A[kMaxWires] = {}, Bw[kMaxWires] = {}, out[kMaxWires] = {};
     for (int i = 0; i < M; ++i) A[i] = i;
