@@ -54,6 +54,8 @@ def assert_cov_parity(cov_gpu, cov_ref, gap, eps=1e-3, masked_frac_max=None):
         w = np.linalg.eigvalsh(_full(cov_gpu[~m]))
         assert np.abs(w - np.array([eps, 1, 1])).max() <= 1e-4
     if masked_frac_max is not None:
+        # SURVEY §8 tolerances: report the masked fraction; < 1 % on the racetrack configs
+        print(f"masked (gap < 1e-2) fraction {(~m).mean():.4%} of {m.size} rows")
         assert (~m).mean() <= masked_frac_max
 
 
@@ -126,7 +128,7 @@ def test_knn_cov_racetrack_subset(orc, k):
     assert np.array_equal(hn[rows], on) and np.array_equal(hd[rows], od)
     assert np.array_equal(H(nbr2), hn) and np.array_equal(H(d22), hd)
     oc, gap, _ = orc.covariance(mp, on)
-    assert_cov_parity(H(cov)[rows], oc, gap, masked_frac_max=0.02)
+    assert_cov_parity(H(cov)[rows], oc, gap, masked_frac_max=0.01)
     # the standalone covariance kernel on the same neighbour table
     cov2 = g.covariances(D(mp), D(on))
     assert_cov_parity(H(cov2), oc, gap)
@@ -324,7 +326,7 @@ def test_c3_fullsize_sampled(orc):
     hn, hd, hc = H(nbr), H(d2), H(cov)
     assert np.array_equal(hn[rows], on) and np.array_equal(hd[rows], od)
     oc, gap, _ = orc.covariance(mp, on)
-    assert_cov_parity(hc[rows], oc, gap, masked_frac_max=0.02)
+    assert_cov_parity(hc[rows], oc, gap, masked_frac_max=0.01)
     # linearize of a source subsample against the full map; covariances are
     # generic SPD inputs from gen (no oracle input comes from the CUDA path)
     sub = rng.choice(len(sc), 1500, replace=False)
@@ -358,7 +360,7 @@ def test_c5_stress_sampled(orc):
     on, od = orc.knn(mp, q[rows], 32)
     assert np.array_equal(hn[rows], on) and np.array_equal(hd[rows], od)
     oc, gap, _ = orc.covariance(mp, on)
-    assert_cov_parity(hc[rows], oc, gap, masked_frac_max=0.05)
+    assert_cov_parity(hc[rows], oc, gap, masked_frac_max=0.01)
     idx.free()
 
 

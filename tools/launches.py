@@ -4,7 +4,7 @@ import sys
 from collections import defaultdict
 
 
-def main(path, top=30):
+def main(path, top=30, by_name=False):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
@@ -15,7 +15,7 @@ def main(path, top=30):
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     for r in rows[hi + 1:]:
         v = float(r[vi].replace(",", "")) * scale[r[ui]]
-        name = r[ki].split("(")[0].replace("gicp::<unnamed>::", "")[:60] + " " + r[gi]
+        name = r[ki].split("(")[0].replace("gicp::<unnamed>::", "")[:60] + ("" if by_name else " " + r[gi])
         agg[name][0] += 1
         agg[name][1] += v
         tot += v
@@ -26,4 +26,4 @@ def main(path, top=30):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], by_name="--by-name" in sys.argv[2:])
