@@ -563,6 +563,16 @@ static double coarse_threshold(const gicp_index_s* tgt) {
     if (const char* e = getenv("GICP_LIN_COARSE_THR")) return atof(e);  // experiments
     return 0.8 * (double)tgt->lv[0].cell;
 }
+// the split evaluation (linearize.cu: certificates, dense searches, terms) for the
+// certificate paths; GICP_LIN_SPLIT=0 (build flag) or the env GICP_LIN_FUSED keep
+// the fused kernel (the A/B and the bitwise check in tests/test_gpu_batched.py)
+#ifndef GICP_LIN_SPLIT
+#define GICP_LIN_SPLIT 1
+#endif
+static bool split_eval(int64_t n) {
+    static const bool fused = getenv("GICP_LIN_FUSED") != nullptr;
+    return GICP_LIN_SPLIT && !fused && n < (1ll << 30);
+}
 // |dv| + |dw| * 20 m (a typical range of the scan points): the step's point motion
 static double step_displacement(const double* d) {
     return std::sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]) + 20.0 * std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
@@ -587,7 +597,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     const int64_t nsa = ns > 0 ? ns : 1;
     const size_t lin_bytes = linearize_scratch_bytes(nsa);
     const size_t bytes = 512 + lin_bytes + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256 +
-                         (GICP_ALIGN_CACHE ? 2 * nsa * sizeof(float4) + 16 : 0);
+                         (GICP_ALIGN_CACHE ? 3 * nsa * sizeof(float4) + 64 : 0);
     char* scratch = nullptr;
     if (cudaMallocAsync((void**)&scratch, bytes, s) != cudaSuccess) {
         cudaGetLastError();
@@ -607,6 +617,10 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     if (GICP_ALIGN_CACHE && getenv("GICP_ALIGN_NOCACHE") == nullptr) {
         cache_a = (float4*)(((uintptr_t)(cov_p + 6 * nsa) + 15) & ~(uintptr_t)15);
         cache_b = cache_a + nsa;
+        if (split_eval(nsa)) {  // the split evaluation's search queue and counter
+            ls.queue = cache_b + nsa;
+            ls.qcount = (unsigned*)(ls.queue + nsa);
+        }
     }
     auto cache_of = [&](const int32_t* c) -> float4* { return c == corr_a ? cache_a : (c == corr_b ? cache_b : nullptr); };
     int rc0 = check_cuda(cudaMemsetAsync(ls.done, 0, sizeof(unsigned), s), "memset");
@@ -1032,14 +1046,14 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
                              (size_t)std::max(E, 1) * sizeof(int) + 768;
     if ((rc = batch_scratch(offsets, E,
                             2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
-                                (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + dev_extra,
+                                (certs ? 3 * nsa * sizeof(float4) + 64 : 0) + dev_extra,
                             s, bs, &ex, B)))
         return rc;
     double* Ed = nullptr;  // device entry rows [E][32] (device sharding)
     int* gid_d = nullptr;
     // entry -> registration (the poses go up per registration, not per entry)
     int* ereg_d = (int*)(((uintptr_t)ex + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
-                          (certs ? 2 * nsa * sizeof(float4) + 16 : 0) + 255) & ~(uintptr_t)255);
+                          (certs ? 3 * nsa * sizeof(float4) + 64 : 0) + 255) & ~(uintptr_t)255);
     if (ds) {
         Ed = (double*)(((uintptr_t)(ereg_d + std::max(E, 1)) + 255) & ~(uintptr_t)255);
         gid_d = (int*)(Ed + 32 * (size_t)std::max(E, 1));
@@ -1064,6 +1078,10 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
     if (certs) {  // cache_new pairs with corrA, cache_old with corrB; the kernel maps them per `cur`
         bs.ls.cache_new = (float4*)(((uintptr_t)(cov_p + 6 * nsa) + 15) & ~(uintptr_t)15);
         bs.ls.cache_old = bs.ls.cache_new + nsa;
+        if (split_eval(nsa)) {  // the split evaluation's search queue and counter
+            bs.ls.queue = bs.ls.cache_new + 2 * nsa;
+            bs.ls.qcount = (unsigned*)(bs.ls.queue + nsa);
+        }
     }
     if (ns > 0 && (rc = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s, bs.offs, E))) {
         cudaFreeAsync(bs.base, s);

@@ -259,6 +259,11 @@ struct LinScratch {
     // this launch's corr (written); nullptr: always search
     float4* cache_new = nullptr;
     const float4* cache_old = nullptr;
+    // optional split evaluation (GICP_LIN_SPLIT, with certificates): the queue of
+    // points that must search ({search point, i | flags}, one per source point) and
+    // its device counter
+    float4* queue = nullptr;
+    unsigned* qcount = nullptr;
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
 constexpr int kLinCoarse = 1 << 10;   // internal flag: single launches set Pose::coarse

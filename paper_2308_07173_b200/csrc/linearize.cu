@@ -24,9 +24,6 @@
 namespace gicp {
 namespace {
 
-#ifndef GICP_LIN_FLAT
-#define GICP_LIN_FLAT 0  // 1: flattened per-lane candidate stream in the level-0 cube stage
-#endif
 constexpr int kLinBlock = 256;
 constexpr int kPPT = 1;                       // points per team
 constexpr int kTeam = GICP_LIN_TEAM;          // lanes per point (adjacent lanes of a warp)
@@ -44,6 +41,9 @@ __device__ unsigned long long g_lprof[80];  // [0..3] stage counts, [4] max sear
 #define LPROF(x) x
 #else
 #define LPROF(x)
+#endif
+#ifndef GICP_LIN_WARM
+#define GICP_LIN_WARM 0
 #endif
 #ifndef GICP_LIN_UNROLL
 #define GICP_LIN_UNROLL 4
@@ -68,27 +68,37 @@ struct Levels {
 // in lockstep (no divergent per-voxel loops); the few points the stop rule (no
 // unsearched point below min(best, r2)) does not settle continue per lane:
 // coarser levels up to `ring_level`, then ring expansion there.
-template <bool CERT>
+// the 27 cells of a cube, own cell first, then faces, edges, corners (nearest
+// first): code = (dx + 1) + 3 (dy + 1) + 9 (dz + 1)
+__constant__ int c_cube27[27] = {13, 12, 14, 10, 16, 4, 22, 9, 11, 15, 17, 3, 5, 21, 23, 1, 7, 19, 25, 0, 2, 6, 8, 18, 20, 24, 26};
+
+template <bool CERT, int UNR = kUnroll>
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
                                           float qy, float qz, float r2, unsigned long long& best, int& bj,
-                                          int& overflow, const int t, float& rho, const int l0) {
+                                          int& overflow, const int t, float& rho, const int l0,
+                                          const unsigned long long warm = kEmptyKey, const int warm_j = -1) {
     // the key (d2 bits << 32 | original index) is kept as two words: the common
     // case (d2 larger) is one 32-bit compare, and only the sorted position of the
     // winner is tracked (its coordinates are loaded once, by the caller)
-    unsigned bh = 0xffffffffu, bo = 0xffffffffu;
+    // warm start (GICP_LIN_WARM): a real candidate's key (the previous
+    // correspondence at the new search point) bounds the search from the start;
+    // the minimum over all points is unchanged, the pruning is tighter
+    unsigned bh = (unsigned)(warm >> 32), bo = (unsigned)(warm & 0xffffffffu);
     overflow = 0;
-    bj = -1;
+    bj = warm_j;
     // certificate of the result for the next iteration (R27): the second-smallest
     // scanned d2 and the smallest lower bound of the voxels left unscanned
     unsigned sh2 = 0xffffffffu;
     float lbp = __int_as_float(0x7f800000);
     rho = -1.0f;
     auto bound = [&]() { return fminf(__uint_as_float(bh), r2); };
+    LPROF(int ncand = 0; int nvox = 0;)
     auto consider_p = [&](int j, const float4 p) {
+        LPROF(++ncand;)
         const unsigned h = __float_as_uint(dist2(qx, qy, qz, p.x, p.y, p.z));
         const unsigned o = __float_as_uint(p.w);
         const bool better = h < bh || (h == bh && o < bo);
-        if (CERT) sh2 = better ? bh : (h < sh2 ? h : sh2);
+        if (CERT) sh2 = better ? bh : ((h < sh2 && o != bo) ? h : sh2);  // (the warm key scanned again: skip)
         bh = better ? h : bh;
         bo = better ? o : bo;
         bj = better ? j : bj;
@@ -102,7 +112,10 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         const float d1 = sqrtf(__uint_as_float(bh)), dl = sqrtf(l2);
         rho = 0.5f * (dl - d1) - 1e-6f * (dl + d1) - 1e-6f;
     };
-    auto finish = [&]() { best = ((unsigned long long)bh << 32) | bo; };
+    auto finish = [&]() {
+        best = ((unsigned long long)bh << 32) | bo;
+        LPROF(if (ncand) atomicAdd(&g_lprof[75], (unsigned long long)ncand);)
+    };
     // the team's lanes split the level-0 candidates; their bests combine by a
     // butterfly min of the (d2 bits, original index) keys after every voxel
     auto team_min = [&]() {
@@ -126,9 +139,6 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         const int2* __restrict__ adj_rng = lvs.adj_rng[l0];
         const QGeom G = make_geom(g, qx, qy, qz);
         const float s = g.cell, slack = g.slack;
-        int2 rl[27];
-        float lbl[27];
-        int nr = 0;
         int a0 = 0, a1 = 0;
         bool use_adj = false;
         if (active && adj_oc != nullptr) {
@@ -143,86 +153,27 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
         const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
         const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
-        if (active && !use_adj) {
-            const float gxs[3] = {axis_gap(-1, G.fx, s, slack), 0.0f, axis_gap(1, G.fx, s, slack)};
-            const float gys[3] = {axis_gap(-1, G.fy, s, slack), 0.0f, axis_gap(1, G.fy, s, slack)};
-            const float gzs[3] = {axis_gap(-1, G.fz, s, slack), 0.0f, axis_gap(1, G.fz, s, slack)};
-#pragma unroll
-            for (int c = 0; c < 27; ++c) {
-                constexpr signed char off[27][3] = {
-                    {0, 0, 0},   {-1, 0, 0},  {1, 0, 0},   {0, -1, 0},  {0, 1, 0},   {0, 0, -1},  {0, 0, 1},
-                    {-1, -1, 0}, {1, -1, 0},  {-1, 1, 0},  {1, 1, 0},   {-1, 0, -1}, {1, 0, -1},  {-1, 0, 1},
-                    {1, 0, 1},   {0, -1, -1}, {0, 1, -1},  {0, -1, 1},  {0, 1, 1},   {-1, -1, -1}, {1, -1, -1},
-                    {-1, 1, -1}, {1, 1, -1},  {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
-                const int dx = off[c][0], dy = off[c][1], dz = off[c][2];
-                const int cx = G.cx + dx, cy = G.cy + dy, cz = G.cz + dz;
-                if ((unsigned)cx >= (unsigned)g.nx || (unsigned)cy >= (unsigned)g.ny || (unsigned)cz >= (unsigned)g.nz)
-                    continue;
-                const float lb2 =
-                    __fmaf_rn(gzs[dz + 1], gzs[dz + 1], __fmaf_rn(gys[dy + 1], gys[dy + 1], gxs[dx + 1] * gxs[dx + 1]));
-                if (lb2 * kRel > r2) {  // beyond the gate: cannot hold an inlier
-                    if (CERT) lbp = fminf(lbp, lb2);
-                    continue;
-                }
-                const unsigned long long key = cell_key(cx, cy, cz);
-                const int2 e = hash_find(g, key);
-                if (e.y <= e.x) continue;
-                rl[nr] = e;
-                lbl[nr] = lb2;
-                ++nr;
-            }
-        }
+        // a lane without an adjacency list (its own voxel is empty, or the index has
+        // none) probes the 27 cells in the entry loop itself, entry k = c_cube27[k]
+        // (no per-lane arrays: the search stays in registers)
+        auto probe = [&](int c, int& cx, int& cy, int& cz, float& lb2) {
+            const int code = c_cube27[c];
+            const int dx = (code % 3) - 1, dy = ((code / 3) % 3) - 1, dz = (code / 9) - 1;
+            cx = G.cx + dx;
+            cy = G.cy + dy;
+            cz = G.cz + dz;
+            const float gx = dx < 0 ? lox : (dx > 0 ? hix : 0.0f);
+            const float gy = dy < 0 ? loy : (dy > 0 ? hiy : 0.0f);
+            const float gz = dz < 0 ? loz : (dz > 0 ? hiz : 0.0f);
+            lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+            return (unsigned)cx < (unsigned)g.nx && (unsigned)cy < (unsigned)g.ny && (unsigned)cz < (unsigned)g.nz;
+        };
         // entry-major, warp-uniform: step k tests every lane's k-th voxel against
         // min(best, r2) (predicated: load, decode, bound) and the lanes whose voxel
         // survives scan it together (inner loop = the longest surviving range).
         // Nearest-first order makes almost every voxel after the own one prunable.
-        const int cnt = use_adj ? a1 - a0 : nr;
-#if GICP_LIN_FLAT
-        // flattened, per lane: one candidate stream over the lane's surviving voxels
-        // (the same voxels in the same order as the entry-major loop below, so the
-        // same result bitwise); the warp steps max over lanes of their stream length
-        // instead of the sum over entries of per-entry maxima
-        if (kTeam == 1) {
-            int ri = 0, pos = 0, end = 0;
-            int2 ne = make_int2(0, 0);
-            if (active && use_adj && cnt > 0) ne = __ldg(adj_rng + a0);
-            float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
-            while (true) {
-                while (active && pos == end && ri < cnt) {
-                    int2 r;
-                    float lb2;
-                    if (use_adj) {
-                        const int2 e = ne;
-                        if (ri + 1 < cnt) ne = __ldg(adj_rng + a0 + ri + 1);
-                        r = adj_range(e);
-                        lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
-                    } else {
-                        r = rl[ri];
-                        lb2 = lbl[ri];
-                    }
-                    ++ri;
-                    if (lb2 * kRel > bound()) {
-                        if (CERT) lbp = fminf(lbp, lb2);
-                        continue;
-                    }
-                    pos = r.x;
-                    end = r.y;
-                    if (pos < end) pn = __ldg(pts + pos);
-                }
-                const bool has = active && pos < end;
-                if (!__any_sync(0xffffffffu, has)) break;
-                if (has) {
-                    const float4 p = pn;
-                    if (pos + 1 < end) pn = __ldg(pts + pos + 1);
-                    consider_p(pos, p);
-                    ++pos;
-                }
-            }
-        }
-        const int kmax = kTeam == 1 ? 0 : __reduce_max_sync(0xffffffffu, active ? cnt : 0);
-#else
+        const int cnt = use_adj ? a1 - a0 : (active ? 27 : 0);
         const int kmax = __reduce_max_sync(0xffffffffu, active ? cnt : 0);
-#endif
         // the next entry is loaded one entry ahead; candidates go kUnroll at a time
         // (independent loads in flight together: the search is latency-bound)
         int2 ne = make_int2(0, 0);
@@ -231,37 +182,57 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             int2 r = make_int2(0, 0);
             if (k < cnt) {
                 float lb2;
+                bool inside = true;
+                int cx = 0, cy = 0, cz = 0;
                 if (use_adj) {
                     const int2 e = ne;
                     if (k + 1 < cnt) ne = __ldg(adj_rng + a0 + k + 1);
                     r = adj_range(e);
                     lb2 = adj_lb2((unsigned)e.y, lox, hix, loy, hiy, loz, hiz);
                 } else {
-                    r = rl[k];
-                    lb2 = lbl[k];
+                    inside = probe(k, cx, cy, cz, lb2);
                 }
-                if (lb2 * kRel > bound()) {
+                if (!inside) {
+                    r = make_int2(0, 0);
+                } else if (lb2 * kRel > bound()) {
                     r = make_int2(0, 0);
                     if (CERT) lbp = fminf(lbp, lb2);
+                } else if (!use_adj) {
+                    r = hash_find(g, cell_key(cx, cy, cz));
+                    if (r.y <= r.x) r = make_int2(0, 0);
                 }
             }
             const int len = r.y - r.x;
             const int lmax = __reduce_max_sync(0xffffffffu, len);
-            for (int j = 0; j < lmax; j += kUnroll * kTeam) {
-                float4 pv[kUnroll];
+            LPROF(nvox += len > 0;)
+            LPROF(if ((threadIdx.x & 31) == 0) atomicAdd(&g_lprof[77], (unsigned long long)lmax);)
+            for (int j = 0; j < lmax; j += UNR * kTeam) {
+                float4 pv[UNR];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < UNR; ++u) {
                     const int c = j + u * kTeam + t;
                     if (c < len) pv[u] = __ldg(pts + r.x + c);
                 }
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < UNR; ++u) {
                     const int c = j + u * kTeam + t;
                     if (c < len) consider_p(r.x + c, pv[u]);
                 }
             }
             if (kTeam > 1) team_min();
         }
+        LPROF({
+            const unsigned a = __reduce_add_sync(0xffffffffu, active ? (unsigned)ncand : 0u);
+            const unsigned v = __reduce_add_sync(0xffffffffu, active ? (unsigned)nvox : 0u);
+            const unsigned na = __reduce_add_sync(0xffffffffu, active ? 1u : 0u);
+            if ((threadIdx.x & 31) == 0) {
+                atomicAdd(&g_lprof[74], (unsigned long long)a);
+                atomicAdd(&g_lprof[76], (unsigned long long)v);
+                atomicAdd(&g_lprof[73], (unsigned long long)na);
+                atomicAdd(&g_lprof[78], 1ull);
+            }
+            ncand = 0;
+        })
         if (!active) { finish(); return; }
         const float m = cube_margin(G, s, slack, 1);
         if (m > 0.0f && bound() < m * m * kRel) {
@@ -403,7 +374,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // PREVIOUS correspondences corr_old at this T (LM's trial evaluation), values 29-30.
 // CERT: correspondence certificates (gicp_align, R27): read cache_old (DUAL) and
 // write cache_new; the other callers compile the tracking out
-template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS, bool DUAL, bool CERT>
+template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS, bool DUAL, bool CERT, bool PRE = false>
 __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
                                                          const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
@@ -440,7 +411,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     if (bv.btab) {
         int32_t* cur = sP.cur ? const_cast<int32_t*>(corr_old) : corr;
         int32_t* oth = sP.cur ? corr : const_cast<int32_t*>(corr_old);
-        corr = REUSE ? cur : oth;
+        corr = (REUSE && !PRE) ? cur : oth;  // PRE: this round's correspondences (k_lin_search)
         corr_old = cur;
         if (CERT) {  // the certificates follow their correspondence buffers
             float4* ccur = sP.cur ? const_cast<float4*>(cache_old) : cache_new;
@@ -495,12 +466,27 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                     cached = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc.w;
                 }
             }
+            LPROF(if (active) atomicAdd(&g_lprof[72], cached ? 1ull : 0ull);)
+            LPROF(if (active) atomicAdd(&g_lprof[79], 1ull);)
             unsigned long long best;
             int bj, ovf;
             float rho;
             LPROF(const long long t0 = clock64();)
+            unsigned long long warm = kEmptyKey;
+            int warm_j = -1;
+#if GICP_LIN_WARM
+            if (DUAL && SPOS && active && !cached) {
+                const int c = corr_old[i];
+                if (c >= 0 && c < nt) {
+                    const float4 q = __ldg(pts + c);
+                    warm = ((unsigned long long)__float_as_uint(dist2(sx, sy, sz, q.x, q.y, q.z)) << 32) |
+                           __float_as_uint(q.w);
+                    warm_j = c;
+                }
+            }
+#endif
             nn_search<CERT>(pts, lvs, active && !cached, sx, sy, sz, r2, best, bj, ovf, tl, rho,
-                            (sP.coarse && lvs.coarse_ok) ? 1 : 0);
+                            (sP.coarse && lvs.coarse_ok) ? 1 : 0, warm, warm_j);
             LPROF({
                 const unsigned dt = (unsigned)min(clock64() - t0, 0xffffffffll);
                 const unsigned mx = __reduce_max_sync(0xffffffffu, dt);
@@ -678,6 +664,128 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
     }
 }
 
+// ---------------------------------------------------------------------------
+// Split evaluation (GICP_LIN_SPLIT, the certificate paths of gicp_align and
+// gicp_align_batched): the fused kernel leaves most lanes of a searching warp idle
+// (64 % of the points keep a certified correspondence, the rest search for ~27
+// candidates in lockstep) and holds fp64 accumulators through the latency-bound
+// search. Instead: (S1) k_lin_cert checks the certificates and queues the points
+// that must search; (S2) k_lin_search runs those searches densely (32 searching
+// lanes per warp, a persistent grid at the occupancy the search alone needs);
+// (S3) k_linearize<PRE> accumulates the terms from the correspondences S1/S2 wrote.
+// Every point's search is the same call on the same inputs, and S3 sums the same
+// terms in the same order: the result is bitwise the fused kernel's.
+// ---------------------------------------------------------------------------
+
+// queue entry: the search point and w = i | coarse << 30 | (write base buffers) << 31
+template <bool DUAL>
+__global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict__ src, int64_t ns,
+                                                        const float4* __restrict__ pts, Pose P, float r2, int coarse_ok,
+                                                        int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
+                                                        BatchView bv, float4* __restrict__ cache_new,
+                                                        const float4* __restrict__ cache_old, float4* __restrict__ queue,
+                                                        unsigned* __restrict__ qcount) {
+    int scan = 0, blk = blockIdx.x;
+    int64_t p0 = 0, pend = ns;
+    if (bv.btab) {
+        const int4 e = bv.btab[blockIdx.x];
+        scan = e.x;
+        blk = e.y;
+        if (!bv.poses[bv.ereg ? bv.ereg[scan] : scan].active) return;
+        p0 = bv.offs[scan];
+        pend = bv.offs[scan + 1];
+    }
+    __shared__ Pose sP;
+    if (threadIdx.x == 0) sP = bv.btab ? bv.poses[bv.ereg ? bv.ereg[scan] : scan] : P;
+    __syncthreads();
+    unsigned wbase = 1u;  // single launches write (corr, cache_new)
+    if (bv.btab) {
+        int32_t* cur = sP.cur ? const_cast<int32_t*>(corr_old) : corr;
+        int32_t* oth = sP.cur ? corr : const_cast<int32_t*>(corr_old);
+        corr = oth;
+        corr_old = cur;
+        float4* ccur = sP.cur ? const_cast<float4*>(cache_old) : cache_new;
+        float4* coth = sP.cur ? cache_new : const_cast<float4*>(cache_old);
+        cache_new = coth;
+        cache_old = ccur;
+        wbase = sP.cur ? 1u : 0u;
+    }
+    const int64_t i = p0 + (int64_t)blk * kPPB + threadIdx.x;
+    const bool active = i < pend;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    bool cached = false;
+    if (active) {
+        const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
+        double pp[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            pp[a] = __fma_rn(sP.R[3 * a + 2], pz, __fma_rn(sP.R[3 * a + 1], py, __fma_rn(sP.R[3 * a], px, sP.t[a])));
+        sx = (float)pp[0];
+        sy = (float)pp[1];
+        sz = (float)pp[2];
+        if (DUAL && cache_old) {
+            const float4 cc = __ldg(cache_old + i);
+            if (cc.w > 0.0f) {
+                const double ex = (double)sx - cc.x, ey = (double)sy - cc.y, ez = (double)sz - cc.z;
+                cached = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc.w;
+            }
+            if (cached) {  // the certified pair: its distance at the new search point, the gate
+                const int bj = corr_old[i];
+                const float4 q = __ldg(pts + bj);
+                const bool inl = dist2(sx, sy, sz, q.x, q.y, q.z) < r2;
+                corr[i] = inl ? bj : -1;
+                cache_new[i] = cc;
+            }
+        }
+    }
+    const bool push = active && !cached;
+    const unsigned m = __ballot_sync(0xffffffffu, push);
+    if (m == 0u) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(qcount, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (push) {
+        const unsigned w = (unsigned)i | ((sP.coarse && coarse_ok) ? (1u << 30) : 0u) | (wbase << 31);
+        queue[base + __popc(m & ((1u << lane) - 1u))] = make_float4(sx, sy, sz, __uint_as_float(w));
+    }
+}
+
+#ifndef GICP_SEARCH_MINB
+#define GICP_SEARCH_MINB 4  // 64 registers: more warps spill, and measured slower (4: 1.64, 5: 2.04, 8: 2.22 ms)
+#endif
+#ifndef GICP_SEARCH_UNROLL
+#define GICP_SEARCH_UNROLL 2  // (4: 1.64, 2: 1.58, 8: 1.92 ms)
+#endif
+constexpr int kSearchBlock = 256;
+__global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
+    k_lin_search(const float4* __restrict__ pts, Levels lvs, int64_t nt, float r2, int32_t* __restrict__ corr_a,
+                 int32_t* __restrict__ corr_b, float4* __restrict__ cache_a, float4* __restrict__ cache_b,
+                 const float4* __restrict__ queue, const unsigned* __restrict__ qcount) {
+    const unsigned n = *qcount;
+    const int lane = threadIdx.x & 31;
+    const unsigned stride = gridDim.x * kSearchBlock;
+    for (unsigned w0 = blockIdx.x * kSearchBlock + (threadIdx.x & ~31u); w0 < n; w0 += stride) {
+        const unsigned k = w0 + lane;
+        const bool active = k < n;  // warp-uniform loop: every lane reaches the search
+        float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (active) e = __ldg(queue + k);
+        const unsigned w = __float_as_uint(e.w);
+        unsigned long long best;
+        int bj, ovf;
+        float rho;
+        nn_search<true, GICP_SEARCH_UNROLL>(pts, lvs, active, e.x, e.y, e.z, r2, best, bj, ovf, 0, rho, (w >> 30) & 1u);
+        if (active) {
+            if (ovf) nn_bruteforce(pts, nt, e.x, e.y, e.z, best, bj);
+            const float bd2 = __uint_as_float((unsigned)(best >> 32));
+            const bool inl = best != kEmptyKey && bd2 < r2;
+            const int64_t i = w & 0x3fffffffu;
+            (w >> 31 ? corr_a : corr_b)[i] = inl ? bj : -1;
+            (w >> 31 ? cache_a : cache_b)[i] = make_float4(e.x, e.y, e.z, (inl && !ovf) ? rho : -1.0f);
+        }
+    }
+}
+
 __global__ void k_zero29(double* out29) {
     if (threadIdx.x < 29) out29[threadIdx.x] = 0.0;
 }
@@ -750,7 +858,43 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
         GICP_LIN_GO(false, true, S, SP);  \
     else                             \
         GICP_LIN_GO(false, false, S, SP);
-    if (cert && dual) {
+    // split evaluation (S1 certificates, S2 dense searches, S3 terms) for the DUAL
+    // launches, where most points keep a certified correspondence; a full
+    // linearisation searches every point and stays fused (measured faster)
+    if (cert && dual && scr.queue) {
+        int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, sizeof(unsigned), s), "memset");
+        if (rc) return rc;
+        if (dual)
+            k_lin_cert<true><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
+                                                                 corr_old, bvq, scr.cache_new, scr.cache_old,
+                                                                 scr.queue, scr.qcount);
+        else
+            k_lin_cert<false><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
+                                                                  corr_old, bvq, scr.cache_new, scr.cache_old,
+                                                                  scr.queue, scr.qcount);
+        static int grid = 0;
+        if (grid == 0) {
+            int dev = 0, sms = 0, per = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#ifdef GICP_SEARCH_CARVEOUT
+            cudaFuncSetAttribute(k_lin_search, cudaFuncAttributePreferredSharedMemoryCarveout, GICP_SEARCH_CARVEOUT);
+#endif
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lin_search, kSearchBlock, 0);
+            grid = std::max(1, sms * std::max(per, 1));
+        }
+        // single launches: (corr, cache_new) are the written pair (w bit 31 = 1)
+        int32_t* ca = corr;
+        int32_t* cb = const_cast<int32_t*>(corr_old);
+        const unsigned g2 = (unsigned)std::min<int64_t>(grid, (ns + kSearchBlock - 1) / kSearchBlock);
+        k_lin_search<<<std::max(g2, 1u), kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
+                                                               const_cast<float4*>(scr.cache_old), scr.queue,
+                                                               scr.qcount);
+        if (dual)
+            k_linearize<true, false, true, true, true, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+        else
+            k_linearize<true, false, true, true, false, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+    } else if (cert && dual) {
         k_linearize<false, false, true, true, true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
     } else if (cert) {
         k_linearize<false, false, true, true, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
@@ -821,3 +965,16 @@ size_t linearize_scratch_bytes(int64_t ns) {
 }
 
 }  // namespace gicp
+
+#if GICP_LIN_PROF
+// diagnostics builds only (tools/lin_prof.py): read and optionally reset the counters
+GICP_API int gicp_debug_lin_prof(unsigned long long* out80, int reset) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out80, gicp::g_lprof, sizeof(gicp::g_lprof)) != cudaSuccess) return -1;
+    if (reset) {
+        static const unsigned long long z[80] = {};
+        cudaMemcpyToSymbol(gicp::g_lprof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

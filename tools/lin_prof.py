@@ -1,7 +1,7 @@
-"""A reduced C4 batch (N distinct scans x 8 hypotheses) aligned once through
-gicp_align_batched_sharded, the align inside cudaProfilerStart/Stop (ncu
---profile-from-start off -k regex:k_linearize --launch-skip S -c 1).
-usage: python tools/prof_c4.py [n_distinct]"""
+"""Search statistics of the batched align (needs the GICP_LIN_PROF=1 variant:
+python tools/build_variants.py lprof:-DGICP_LIN_PROF=1, run with
+GICP_LIB_VARIANT=.../libgicp_lprof.so). usage: python tools/lin_prof.py [n_distinct]"""
+import ctypes
 import os
 import sys
 
@@ -14,7 +14,7 @@ import gen
 import paper_2308_07173_b200 as g
 from paper_2308_07173_b200 import sharding
 
-nd = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+nd = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 scans = bench.gen_scans(list(range(nd)), min(nd, os.cpu_count() or 1))
 mp = gen.racetrack_map(2_000_000, 1)
 dev = torch.device("cuda:0")
@@ -32,18 +32,19 @@ _, T0 = bench.c4_poses()
 T0 = T0[:B]
 offsets = np.arange(B + 1, dtype=np.int64) * bench.N_SCAN
 plan = sharding.ShardPlan(offsets, dev, reg_base=(np.arange(B) // bench.N_HYP) * bench.N_SCAN)
-sharding.align_batched_sharded(g, sd, cs, offsets, imap, cm, T0, plan=plan)   # warm-up
-torch.cuda.synchronize()
-g.align_timing(True)
-torch.cuda.cudart().cudaProfilerStart()
+f = g._lib.gicp_debug_lin_prof
+f.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+buf = (ctypes.c_ulonglong * 80)()
+f(buf, 1)
 T, infos = sharding.align_batched_sharded(g, sd, cs, offsets, imap, cm, T0, plan=plan)
 torch.cuda.synchronize()
-torch.cuda.cudart().cudaProfilerStop()
-ms, n, pts = g.align_timing(False)
-if os.environ.get("PROF_SAVE"):
-    np.save(os.environ["PROF_SAVE"], np.asarray(T))
-print("iterations", [i.iterations for i in infos][:16], "launch ms", ms, "n", n, "pts", pts)
-for k in range(3):
-    if n[k]:
-        print(f"kind {k}: {ms[k] / n[k]:.3f} ms/launch, {pts[k] / n[k]:.0f} pts/launch, "
-              f"{80 * pts[k] / (ms[k] * 1e-3) / 1e9:.1f} GB/s")
+f(buf, 1)
+c = list(buf)
+print(f"points evaluated (searching kinds) {c[79]}, cached {c[72]} ({c[72] / max(c[79], 1):.3f})")
+print(f"level-0 searches {c[73]}: candidates/search {c[74] / max(c[73], 1):.1f}, voxels/search "
+      f"{c[76] / max(c[73], 1):.2f}; warp lockstep slots/warp-call {c[77] / max(c[78], 1):.1f} "
+      f"vs useful cands/warp-call {c[74] / max(c[78], 1):.1f} (lanes x)")
+print(f"stage 2 (coarser levels) entries {c[1]} ({c[1] / max(c[73], 1):.4f} of searches), "
+      f"cands/entry {c[75] / max(c[1], 1):.1f}; ring entries {c[2]}; overflow {c[3]}")
+print(f"search cycles/warp mean {c[5] / max(c[0], 1):.0f}, total cycles/warp mean {c[6] / max(c[78], 1):.0f}")
+print("search log2 hist", c[8:40])
