@@ -563,16 +563,12 @@ static double coarse_threshold(const gicp_index_s* tgt) {
     if (const char* e = getenv("GICP_LIN_COARSE_THR")) return atof(e);  // experiments
     return 0.8 * (double)tgt->lv[0].cell;
 }
-// the split evaluation (linearize.cu: certificates, dense searches, terms) for the
-// certificate paths; GICP_LIN_SPLIT=0 (build flag) or the env GICP_LIN_FUSED keep
-// the fused kernel (the A/B and the bitwise check in tests/test_gpu_batched.py)
+// the split evaluation's queue (linearize.cu: certificates, dense searches, terms)
+// for the certificate paths; GICP_LIN_SPLIT=0 (build flag) keeps every launch fused
 #ifndef GICP_LIN_SPLIT
 #define GICP_LIN_SPLIT 1
 #endif
-static bool split_eval(int64_t n) {
-    static const bool fused = getenv("GICP_LIN_FUSED") != nullptr;
-    return GICP_LIN_SPLIT && !fused && n < (1ll << 30);
-}
+static bool split_eval(int64_t n) { return GICP_LIN_SPLIT && n < (1ll << 30); }
 // |dv| + |dw| * 20 m (a typical range of the scan points): the step's point motion
 static double step_displacement(const double* d) {
     return std::sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]) + 20.0 * std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);

@@ -368,6 +368,116 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// the block's reduction and the launch's epilogue (shared by k_linearize and
+// k_lin_terms): warp butterfly + block tree into the block's partial row, the last
+// block of a registration sums its partials in a fixed order, the last
+// registration signals the launch
+template <bool ERROR_ONLY, bool DUAL>
+__device__ __forceinline__ void lin_block_finish(const double (&acc)[kNumAcc], const double cnt, const double eold27,
+                                                 const double cnt_old, const int scan, const int blk, const int nblk,
+                                                 const int gblk, double* __restrict__ partials,
+                                                 unsigned* __restrict__ done, double* __restrict__ out29,
+                                                 volatile unsigned* flag, const unsigned seq, const BatchView& bv) {
+    // warp tree
+    constexpr int NV = DUAL ? kNV : kNumAcc + 1;
+    __shared__ double sh[kLinBlock / 32][kNV];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (ERROR_ONLY) {
+        const double v = warp_sum(acc[27]), n = warp_sum(cnt);
+        if (lane == 0) {
+            sh[wid][27] = v;
+            sh[wid][kNumAcc] = n;
+        }
+    } else {
+        // butterfly reduce-scatter of the (up to) 32 values: at the stage of offset
+        // o a lane keeps the half of its values whose index bit matches its lane bit
+        // and adds its partner's copy of them, so after 5 stages lane L holds the
+        // warp sum of value L -- 31 exchanges instead of 5 per value (fixed order)
+        double val[32];
+#pragma unroll
+        for (int c = 0; c < kNumAcc; ++c) val[c] = acc[c];
+        val[kNumAcc] = cnt;
+        val[29] = DUAL ? eold27 : 0.0;
+        val[30] = DUAL ? cnt_old : 0.0;
+        val[31] = 0.0;
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool up = lane & h;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const double send = up ? val[i] : val[i + h];
+                const double keep = up ? val[i + h] : val[i];
+                val[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        if (lane < NV) sh[wid][lane] = val[0];
+    }
+    __syncthreads();
+    // block tree: thread c sums component c over the 8 warps in order
+    if (threadIdx.x < NV) {
+        const int c = threadIdx.x;
+        double v = 0.0;
+        if (!(ERROR_ONLY && c < 27)) {
+#pragma unroll
+            for (int w = 0; w < kLinBlock / 32; ++w) v += sh[w][c];
+        }
+        partials[(int64_t)gblk * kNV + c] = v;
+    }
+    // last block (of the registration): fixed-order sum of its block partials
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(done + scan, 1u) == (unsigned)nblk - 1u);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    partials += (int64_t)(gblk - blk) * kNV;  // the registration's first block
+    out29 += (int64_t)scan * bv.out_stride;
+    // 29 components x 8 interleaved sub-sequences (block b goes to sub b % 8), the
+    // loads of each thread batched 8 at a time (independent, in flight together),
+    // summed in a fixed order: deterministic and latency-tolerant
+    constexpr int kSub = 8;
+    __shared__ double part[kSub][kNV];
+    const int nb = nblk;
+    if (threadIdx.x < kSub * NV) {
+        const int c = threadIdx.x % NV, sub = threadIdx.x / NV;
+        double v = 0.0;
+        int b = sub;
+        for (; b + 7 * kSub < nb; b += 8 * kSub) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partials + (int64_t)(b + u * kSub) * kNV + c);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v += t[u];
+        }
+        for (; b < nb; b += kSub) v += __ldcg(partials + (int64_t)b * kNV + c);
+        part[sub][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        const int c = threadIdx.x;
+        double v = 0.0;
+#pragma unroll
+        for (int sub = 0; sub < kSub; ++sub) v += part[sub][c];
+        out29[c] = v;
+    }
+    if (threadIdx.x == 0) done[scan] = 0u;
+    if (bv.btab) {  // the last registration to finish signals the launch
+        __shared__ bool fin;
+        __threadfence_system();  // every lane's out row (possibly host-mapped) before the ticket
+        __syncthreads();
+        if (threadIdx.x == 0) fin = (atomicAdd(done + bv.n_scans, 1u) == (unsigned)bv.n_active - 1u);
+        __syncthreads();
+        if (!fin) return;
+        if (threadIdx.x == 0) done[bv.n_scans] = 0u;
+    }
+    if (flag) {  // out29 may be host-mapped: make it visible before the signal
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) *flag = seq;
+    }
+}
+
 // SORTED: target covariances from the index's sorted-order copy; SPOS: corr holds
 // sorted positions (internal to gicp_align) instead of original indices; DUAL
 // (gicp_align's speculative step): in the same pass also the cost e' with the
@@ -564,104 +674,104 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             atomicAdd(&g_lprof[40 + min(31, 31 - __clz(mx | 1))], 1ull);
         }
     })
-    // warp tree
-    constexpr int NV = DUAL ? kNV : kNumAcc + 1;
-    __shared__ double sh[kLinBlock / 32][kNV];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (ERROR_ONLY) {
-        const double v = warp_sum(acc[27]), n = warp_sum(cnt);
-        if (lane == 0) {
-            sh[wid][27] = v;
-            sh[wid][kNumAcc] = n;
+    lin_block_finish<ERROR_ONLY, DUAL>(acc, cnt, eold[27], cnt_old, scan, blk, nblk, gblk, partials, done, out29, flag,
+                                       seq, bv);
+}
+
+// Terms from given correspondences (gicp_align: the trial evaluation e' alone, and
+// PRE: the split evaluation's terms after k_lin_cert / k_lin_search; sorted
+// positions, sorted target covariances). The same per-point terms and reductions as
+// k_linearize, in the same order (bitwise the same result), but laid out for
+// latency: every load a point needs (its correspondence, chosen by the pose's `cur`
+// read directly, and that target point and covariance) is issued before the block
+// waits for its pose, whose copy into shared memory is spread over the first threads.
+template <bool ERROR_ONLY, bool DUAL, bool PRE>
+__global__ void __launch_bounds__(kLinBlock, 4)
+    k_lin_terms(const float* __restrict__ src, const float* __restrict__ src_cov, int64_t ns,
+                const float4* __restrict__ pts, int64_t nt, const float4* __restrict__ tgt_cov_sorted, Pose P,
+                const int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old, double* __restrict__ partials,
+                unsigned* __restrict__ done, double* __restrict__ out29, volatile unsigned* flag, unsigned seq,
+                BatchView bv) {
+    static_assert(sizeof(Pose) % 8 == 0 && sizeof(Pose) / 8 <= kLinBlock, "pose copy");
+    int scan = 0, blk = blockIdx.x, nblk = gridDim.x, gblk = blockIdx.x;
+    int64_t p0 = 0, pend = ns;
+    const Pose* gp = nullptr;  // (the kernel parameter P is not addressed: it would go to the stack)
+    if (bv.btab) {
+        const int4 e = bv.btab[blockIdx.x];
+        scan = e.x;
+        blk = e.y;
+        nblk = e.z;
+        gblk = e.w;
+        gp = bv.poses + (bv.ereg ? bv.ereg[scan] : scan);
+        p0 = bv.offs[scan];
+        pend = bv.offs[scan + 1];
+    }
+    __shared__ Pose sP;
+    if (gp == nullptr) {
+        if (threadIdx.x == 0) sP = P;
+    } else if (threadIdx.x < sizeof(Pose) / 8) {
+        reinterpret_cast<unsigned long long*>(&sP)[threadIdx.x] =
+            __ldg(reinterpret_cast<const unsigned long long*>(gp) + threadIdx.x);
+    }
+    const int64_t i = p0 + (int64_t)blk * kPPB + threadIdx.x;
+    const bool active = i < pend;
+    // batched: which buffer is current is the pose's `cur` (read directly: no wait
+    // for the shared copy); PRE reads the other buffer (this round's) as new and the
+    // current as old, REUSE the current alone. Single launches: corr is the written /
+    // reused buffer, corr_old the old one.
+    bool new_is_a = true;
+    if (bv.btab) {
+        const bool cur = __ldg(&gp->cur) != 0;
+        new_is_a = PRE ? cur : !cur;
+    }
+    const int32_t* cbuf = new_is_a ? corr : corr_old;
+    const int32_t* obuf = new_is_a ? corr_old : corr;
+    int cn = -1, co = -1;
+    double px = 0.0, py = 0.0, pz = 0.0;
+    float cp[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (active) {
+        cn = cbuf[i];
+        if (DUAL) co = obuf[i];
+        px = src[3 * i];
+        py = src[3 * i + 1];
+        pz = src[3 * i + 2];
+        load_cov6(src_cov, i, cp);
+    }
+    const bool vn = cn >= 0 && cn < nt, vo = DUAL && co >= 0 && co < nt;
+    const float4 q = __ldg(pts + (vn ? cn : 0));
+    float cq[6];
+    load_cov_sorted(tgt_cov_sorted, vn ? cn : 0, cq);
+    __syncthreads();
+    if (bv.btab && !sP.active) return;  // block-uniform: converged registration
+    double acc[kNumAcc];
+#pragma unroll
+    for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
+    double cnt = 0.0, cnt_old = 0.0, eold[kNumAcc];
+    eold[27] = 0.0;
+    if (active) {
+        double pp[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            pp[a] = __fma_rn(sP.R[3 * a + 2], pz, __fma_rn(sP.R[3 * a + 1], py, __fma_rn(sP.R[3 * a], px, sP.t[a])));
+        double e_new = 0.0;
+        if (vn) {
+            e_new = accumulate_point<ERROR_ONLY>(sP, pp, q.x, q.y, q.z, cp, cq, acc);
+            cnt += 1.0;
         }
-    } else {
-        // butterfly reduce-scatter of the (up to) 32 values: at the stage of offset
-        // o a lane keeps the half of its values whose index bit matches its lane bit
-        // and adds its partner's copy of them, so after 5 stages lane L holds the
-        // warp sum of value L -- 31 exchanges instead of 5 per value (fixed order)
-        double val[32];
-#pragma unroll
-        for (int c = 0; c < kNumAcc; ++c) val[c] = acc[c];
-        val[kNumAcc] = cnt;
-        val[29] = DUAL ? eold[27] : 0.0;
-        val[30] = DUAL ? cnt_old : 0.0;
-        val[31] = 0.0;
-#pragma unroll
-        for (int h = 16; h >= 1; h >>= 1) {
-            const bool up = lane & h;
-#pragma unroll
-            for (int i = 0; i < h; ++i) {
-                const double send = up ? val[i] : val[i + h];
-                const double keep = up ? val[i + h] : val[i];
-                val[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        if (vo) {  // the trial cost with the previous correspondences
+            if (vn && co == cn) {
+                eold[27] += e_new;  // the same pair at the same pose: the same term, bitwise
+            } else {
+                const float4 qo = __ldg(pts + co);
+                float cqo[6];
+                load_cov_sorted(tgt_cov_sorted, co, cqo);
+                accumulate_point<true>(sP, pp, qo.x, qo.y, qo.z, cp, cqo, eold);
             }
+            cnt_old += 1.0;
         }
-        if (lane < NV) sh[wid][lane] = val[0];
     }
-    __syncthreads();
-    // block tree: thread c sums component c over the 8 warps in order
-    if (threadIdx.x < NV) {
-        const int c = threadIdx.x;
-        double v = 0.0;
-        if (!(ERROR_ONLY && c < 27)) {
-#pragma unroll
-            for (int w = 0; w < kLinBlock / 32; ++w) v += sh[w][c];
-        }
-        partials[(int64_t)gblk * kNV + c] = v;
-    }
-    // last block (of the registration): fixed-order sum of its block partials
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = (atomicAdd(done + scan, 1u) == (unsigned)nblk - 1u);
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    partials += (int64_t)(gblk - blk) * kNV;  // the registration's first block
-    out29 += (int64_t)scan * bv.out_stride;
-    // 29 components x 8 interleaved sub-sequences (block b goes to sub b % 8), the
-    // loads of each thread batched 8 at a time (independent, in flight together),
-    // summed in a fixed order: deterministic and latency-tolerant
-    constexpr int kSub = 8;
-    __shared__ double part[kSub][kNV];
-    const int nb = nblk;
-    if (threadIdx.x < kSub * NV) {
-        const int c = threadIdx.x % NV, sub = threadIdx.x / NV;
-        double v = 0.0;
-        int b = sub;
-        for (; b + 7 * kSub < nb; b += 8 * kSub) {
-            double t[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partials + (int64_t)(b + u * kSub) * kNV + c);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v += t[u];
-        }
-        for (; b < nb; b += kSub) v += __ldcg(partials + (int64_t)b * kNV + c);
-        part[sub][c] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < NV) {
-        const int c = threadIdx.x;
-        double v = 0.0;
-#pragma unroll
-        for (int sub = 0; sub < kSub; ++sub) v += part[sub][c];
-        out29[c] = v;
-    }
-    if (threadIdx.x == 0) done[scan] = 0u;
-    if (bv.btab) {  // the last registration to finish signals the launch
-        __shared__ bool fin;
-        __threadfence_system();  // every lane's out row (possibly host-mapped) before the ticket
-        __syncthreads();
-        if (threadIdx.x == 0) fin = (atomicAdd(done + bv.n_scans, 1u) == (unsigned)bv.n_active - 1u);
-        __syncthreads();
-        if (!fin) return;
-        if (threadIdx.x == 0) done[bv.n_scans] = 0u;
-    }
-    if (flag) {  // out29 may be host-mapped: make it visible before the signal
-        __threadfence_system();
-        __syncthreads();
-        if (threadIdx.x == 0) *flag = seq;
-    }
+    lin_block_finish<ERROR_ONLY, DUAL>(acc, cnt, eold[27], cnt_old, scan, blk, nblk, gblk, partials, done, out29, flag,
+                                       seq, bv);
 }
 
 // ---------------------------------------------------------------------------
@@ -715,7 +825,11 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
     float sx = 0.f, sy = 0.f, sz = 0.f;
     bool cached = false;
     if (active) {
+        // the point, its certificate and its previous correspondence: independent
+        // loads, issued together
         const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
+        const float4 cc = (DUAL && cache_old) ? __ldg(cache_old + i) : make_float4(0.f, 0.f, 0.f, -1.f);
+        const int bj = (DUAL && cache_old) ? corr_old[i] : 0;
         double pp[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
@@ -724,13 +838,11 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
         sy = (float)pp[1];
         sz = (float)pp[2];
         if (DUAL && cache_old) {
-            const float4 cc = __ldg(cache_old + i);
             if (cc.w > 0.0f) {
                 const double ex = (double)sx - cc.x, ey = (double)sy - cc.y, ez = (double)sz - cc.z;
                 cached = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc.w;
             }
             if (cached) {  // the certified pair: its distance at the new search point, the gate
-                const int bj = corr_old[i];
                 const float4 q = __ldg(pts + bj);
                 const bool inl = dist2(sx, sy, sz, q.x, q.y, q.z) < r2;
                 corr[i] = inl ? bj : -1;
@@ -758,14 +870,23 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
 #define GICP_SEARCH_UNROLL 2  // (4: 1.64, 2: 1.58, 8: 1.92 ms)
 #endif
 constexpr int kSearchBlock = 256;
+#ifndef GICP_SPLIT_MIN
+#define GICP_SPLIT_MIN (1 << 20)
+#endif
+constexpr int64_t kSplitMinPoints = GICP_SPLIT_MIN;
 __global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
     k_lin_search(const float4* __restrict__ pts, Levels lvs, int64_t nt, float r2, int32_t* __restrict__ corr_a,
                  int32_t* __restrict__ corr_b, float4* __restrict__ cache_a, float4* __restrict__ cache_b,
                  const float4* __restrict__ queue, const unsigned* __restrict__ qcount) {
-    const unsigned n = *qcount;
+    // qcount[0]: queue length; qcount[1]: the next unclaimed entry (each warp claims
+    // 32 at a time: dynamic balance, and warps in flight work on neighbouring entries)
+    const unsigned n = qcount[0];
     const int lane = threadIdx.x & 31;
-    const unsigned stride = gridDim.x * kSearchBlock;
-    for (unsigned w0 = blockIdx.x * kSearchBlock + (threadIdx.x & ~31u); w0 < n; w0 += stride) {
+    for (;;) {
+        unsigned w0 = 0;
+        if (lane == 0) w0 = atomicAdd(const_cast<unsigned*>(qcount) + 1, 32u);
+        w0 = __shfl_sync(0xffffffffu, w0, 0);
+        if (w0 >= n) break;
         const unsigned k = w0 + lane;
         const bool active = k < n;  // warp-uniform loop: every lane reaches the search
         float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -845,6 +966,8 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
 #define GICP_LIN_ARGS                                                                                            \
     src, src_cov, ns, tgt->pts, tgt->pts_orig, lvs, tgt->n, tgt_cov, tgt->cov_sorted, P, r2, corr, corr_old, partials, \
         done, out29, flag, seq, bvq, scr.cache_new, scr.cache_old
+#define GICP_TERMS_ARGS                                                                                           \
+    src, src_cov, ns, tgt->pts, tgt->n, tgt->cov_sorted, P, corr, corr_old, partials, done, out29, flag, seq, bvq
 #define GICP_LIN_GO(R, E, S, SP) k_linearize<R, E, S, SP, false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
 #define GICP_LIN_DUAL(S, SP) k_linearize<false, false, S, SP, true, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS)
     // certificates (gicp_align: sorted source, sorted-position correspondences)
@@ -858,11 +981,17 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
         GICP_LIN_GO(false, true, S, SP);  \
     else                             \
         GICP_LIN_GO(false, false, S, SP);
-    // split evaluation (S1 certificates, S2 dense searches, S3 terms) for the DUAL
-    // launches, where most points keep a certified correspondence; a full
-    // linearisation searches every point and stays fused (measured faster)
-    if (cert && dual && scr.queue) {
-        int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, sizeof(unsigned), s), "memset");
+    // split evaluation (S1 certificates, S2 dense searches, S3 terms) for the
+    // certificate launches over many points (C4, 9M points a launch: dual 1.97 ->
+    // 1.39 ms, full 0.62 -> 0.53 ms); a single 100k-point scan (C3) stays fused: its
+    // three extra launches and the memset cost more than the denser search saves
+    // (C3 align 1.30 -> 1.56 ms split)
+    // GICP_LIN_SPLIT_MIN (points, env, read per launch): the threshold; tests force
+    // either path to check that they agree bitwise
+    int64_t split_min = kSplitMinPoints;
+    if (const char* e = getenv("GICP_LIN_SPLIT_MIN")) split_min = atoll(e);
+    if (cert && scr.queue && ns >= split_min) {
+        int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, 2 * sizeof(unsigned), s), "memset");
         if (rc) return rc;
         if (dual)
             k_lin_cert<true><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
@@ -891,9 +1020,9 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
                                                                const_cast<float4*>(scr.cache_old), scr.queue,
                                                                scr.qcount);
         if (dual)
-            k_linearize<true, false, true, true, true, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+            k_lin_terms<false, true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_TERMS_ARGS);
         else
-            k_linearize<true, false, true, true, false, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
+            k_lin_terms<false, false, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_TERMS_ARGS);
     } else if (cert && dual) {
         k_linearize<false, false, true, true, true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_LIN_ARGS);
     } else if (cert) {
@@ -905,6 +1034,11 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
             GICP_LIN_DUAL(true, false);
         else
             GICP_LIN_DUAL(false, false);
+    } else if (spos && reuse) {  // given correspondences (the trial evaluation)
+        if (eonly)
+            k_lin_terms<true, false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_TERMS_ARGS);
+        else
+            k_lin_terms<false, false, false><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_TERMS_ARGS);
     } else if (spos) {
         GICP_LIN_RE(true, true)
     } else if (sorted) {
@@ -916,6 +1050,7 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
 #undef GICP_LIN_RE
 #undef GICP_LIN_GO
 #undef GICP_LIN_ARGS
+#undef GICP_TERMS_ARGS
     return check_cuda(cudaGetLastError(), "linearize launch");
 }
 

@@ -142,3 +142,25 @@ def test_align_batched_certificates_bitwise(problem, monkeypatch):
     assert np.array_equal(np.asarray(Ta), np.asarray(Tb))
     assert [(i.iterations, i.converged, i.error, i.inliers) for i in ia] == \
         [(i.iterations, i.converged, i.error, i.inliers) for i in ib]
+
+
+@pytest.mark.parametrize("single", [False, True])
+def test_split_evaluation_bitwise(problem, monkeypatch, single):
+    """The split evaluation (k_lin_cert -> k_lin_search -> k_lin_terms, used for
+    launches of >= 1M points) and the fused k_linearize give bitwise the same
+    aligns: forced on (GICP_LIN_SPLIT_MIN=0) against forced off."""
+    p = problem
+    def run():
+        if single:
+            b = int(np.argmax(np.diff(p["offs"])))
+            lo, hi = p["offs"][b], p["offs"][b + 1]
+            T, i = g.align(p["src"][lo:hi], p["covs"][b], p["im"], p["cm"], p["T0"][b])
+            return [T], [i]
+        return g.align_batched(p["src"], p["cov"], p["offs"], p["im"], p["cm"], p["T0"], allow_degenerate=True)
+    monkeypatch.setenv("GICP_LIN_SPLIT_MIN", "0")
+    Ta, ia = run()
+    monkeypatch.setenv("GICP_LIN_SPLIT_MIN", str(1 << 40))
+    Tb, ib = run()
+    assert np.array_equal(np.asarray(Ta), np.asarray(Tb))
+    assert [(i.iterations, i.converged, i.error, i.inliers) for i in ia] == \
+        [(i.iterations, i.converged, i.error, i.inliers) for i in ib]

@@ -22,5 +22,7 @@ for r in rows:
         tot_i += i
         tot_s += smp
 print(f"total warp instr/item {tot_i / n:.1f}, samples {tot_s}")
-for i, smp, f, ln, src in sorted(res, key=lambda t: -t[0])[:top]:
+import os
+key = (lambda t: -t[1]) if os.environ.get("BY_STALL") else (lambda t: -t[0])
+for i, smp, f, ln, src in sorted(res, key=key)[:top]:
     print(f"{i / n:8.2f}/item {100 * smp / max(tot_s, 1):5.1f}% stall  {f}:{ln}  {src.strip()[:70]}")
