@@ -12,12 +12,11 @@ namespace gicp {
 
 constexpr int kLinAcc = 28;  // H(21) b(6) e(1)
 
-// per-pair terms for the residual d (fp32) at the transformed point pp, added
-// to the fp64 acc (times w when WEIGHTED: the voxel size N of VGICP)
-template <bool ERROR_ONLY, bool WEIGHTED = false>
-__device__ __forceinline__ double accumulate_terms(const Pose& P, const double pp[3], const float dx, const float dy,
-                                                 const float dz, const float cp[6], const float cq[6],
-                                                 double acc[kLinAcc], const double w = 1.0) {
+// per-pair terms for the residual d (fp32) at the transformed point pp: t[0..26]
+// = H (21), b (6) (not written when ERROR_ONLY), returns the cost term e (fp32)
+template <bool ERROR_ONLY>
+__device__ __forceinline__ float point_terms(const Pose& P, const double pp[3], const float dx, const float dy,
+                                             const float dz, const float cp[6], const float cq[6], float t[27]) {
     // A = C^q + R C^p R^T
     const float* R = P.Rf;
     const float C[9] = {cp[0], cp[1], cp[2], cp[1], cp[3], cp[4], cp[2], cp[4], cp[5]};
@@ -46,9 +45,7 @@ __device__ __forceinline__ double accumulate_terms(const Pose& P, const double p
     const float mdx = M00 * dx + M01 * dy + M02 * dz;
     const float mdy = M01 * dx + M11 * dy + M12 * dz;
     const float mdz = M02 * dx + M12 * dy + M22 * dz;
-    const double et =
-        WEIGHTED ? w * (double)(dx * mdx + dy * mdy + dz * mdz) : (double)(dx * mdx + dy * mdy + dz * mdz);
-    acc[27] += et;
+    const float et = dx * mdx + dy * mdy + dz * mdz;
     if (ERROR_ONLY) return et;
     // lever arm about the pivot (fp64 difference, then fp32)
     const float px = (float)(pp[0] - P.c[0]), py = (float)(pp[1] - P.c[1]), pz = (float)(pp[2] - P.c[2]);
@@ -75,8 +72,25 @@ __device__ __forceinline__ double accumulate_terms(const Pose& P, const double p
     const float v[27] = {H00, H01, H02, H03, H04, H05, H11, H12, H13, H14, H15, H22,   H23,   H24,
                          H25, M00, M01, M02, M11, M12, M22, b0,  b1,  b2,  -mdx, -mdy, -mdz};
 #pragma unroll
-    for (int c = 0; c < 27; ++c) acc[c] += WEIGHTED ? w * (double)v[c] : (double)v[c];
-    return et;  // the cost term this pair added
+    for (int c = 0; c < 27; ++c) t[c] = v[c];
+    return et;
+}
+
+// the same terms added to the fp64 acc (times w when WEIGHTED: the voxel size N of
+// VGICP); returns the cost term this pair added
+template <bool ERROR_ONLY, bool WEIGHTED = false>
+__device__ __forceinline__ double accumulate_terms(const Pose& P, const double pp[3], const float dx, const float dy,
+                                                 const float dz, const float cp[6], const float cq[6],
+                                                 double acc[kLinAcc], const double w = 1.0) {
+    float t[27];
+    const float e = point_terms<ERROR_ONLY>(P, pp, dx, dy, dz, cp, cq, t);
+    const double et = WEIGHTED ? w * (double)e : (double)e;
+    acc[27] += et;
+    if constexpr (!ERROR_ONLY) {
+#pragma unroll
+        for (int c = 0; c < 27; ++c) acc[c] += WEIGHTED ? w * (double)t[c] : (double)t[c];
+    }
+    return et;
 }
 
 

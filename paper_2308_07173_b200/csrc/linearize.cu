@@ -42,6 +42,9 @@ __device__ unsigned long long g_lprof[80];  // [0..3] stage counts, [4] max sear
 #else
 #define LPROF(x)
 #endif
+#ifndef GICP_LIN_MINB
+#define GICP_LIN_MINB 4  // blocks per SM the fused / terms kernels are compiled for
+#endif
 #ifndef GICP_LIN_WARM
 #define GICP_LIN_WARM 0
 #endif
@@ -352,15 +355,21 @@ __device__ __forceinline__ void load_cov6(const float* __restrict__ c, int64_t r
     o[5] = d.y;
 }
 
-// per-point terms of one inlier, accumulated into fp64 acc[28]
+
+// the terms of one pair as fp32 values (one point per thread: every fp64 sum of the
+// reduction starts from these exact values); returns e
 template <bool ERROR_ONLY>
-__device__ __forceinline__ double accumulate_point(const Pose& P, const double pp[3], float qx, float qy, float qz,
-                                                   const float cp[6], const float cq[6], double acc[kNumAcc]) {
+__device__ __forceinline__ float point_terms_at(const Pose& P, const double pp[3], float qx, float qy, float qz,
+                                                const float cp[6], const float cq[6], float t[27]) {
     const float dx = (float)((double)qx - pp[0]);
     const float dy = (float)((double)qy - pp[1]);
     const float dz = (float)((double)qz - pp[2]);
-    return accumulate_terms<ERROR_ONLY>(P, pp, dx, dy, dz, cp, cq, acc);
+    return point_terms<ERROR_ONLY>(P, pp, dx, dy, dz, cp, cq, t);
 }
+
+// a thread's values (one point): [0, 27) H and b, 27 e, 28 count, 29 e' (DUAL),
+// 30 its count; 0.0f + x, as the fp64 accumulators 0.0 + x were (signed zeros)
+constexpr int kTV = 32;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -373,8 +382,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // block of a registration sums its partials in a fixed order, the last
 // registration signals the launch
 template <bool ERROR_ONLY, bool DUAL>
-__device__ __forceinline__ void lin_block_finish(const double (&acc)[kNumAcc], const double cnt, const double eold27,
-                                                 const double cnt_old, const int scan, const int blk, const int nblk,
+__device__ __forceinline__ void lin_block_finish(const float (&tv)[kTV], const int scan, const int blk, const int nblk,
                                                  const int gblk, double* __restrict__ partials,
                                                  unsigned* __restrict__ done, double* __restrict__ out29,
                                                  volatile unsigned* flag, const unsigned seq, const BatchView& bv) {
@@ -383,7 +391,7 @@ __device__ __forceinline__ void lin_block_finish(const double (&acc)[kNumAcc], c
     __shared__ double sh[kLinBlock / 32][kNV];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (ERROR_ONLY) {
-        const double v = warp_sum(acc[27]), n = warp_sum(cnt);
+        const double v = warp_sum((double)tv[27]), n = warp_sum((double)tv[28]);
         if (lane == 0) {
             sh[wid][27] = v;
             sh[wid][kNumAcc] = n;
@@ -393,15 +401,20 @@ __device__ __forceinline__ void lin_block_finish(const double (&acc)[kNumAcc], c
         // o a lane keeps the half of its values whose index bit matches its lane bit
         // and adds its partner's copy of them, so after 5 stages lane L holds the
         // warp sum of value L -- 31 exchanges instead of 5 per value (fixed order)
-        double val[32];
+        // (the first stage exchanges the fp32 values and adds them in fp64: the
+        // same sums as from fp64 copies, half the registers)
+        double val[16];
+        {
+            const bool up = lane & 16;
 #pragma unroll
-        for (int c = 0; c < kNumAcc; ++c) val[c] = acc[c];
-        val[kNumAcc] = cnt;
-        val[29] = DUAL ? eold27 : 0.0;
-        val[30] = DUAL ? cnt_old : 0.0;
-        val[31] = 0.0;
+            for (int i = 0; i < 16; ++i) {
+                const float send = up ? tv[i] : tv[i + 16];
+                const float keep = up ? tv[i + 16] : tv[i];
+                val[i] = (double)keep + (double)__shfl_xor_sync(0xffffffffu, send, 16);
+            }
+        }
 #pragma unroll
-        for (int h = 16; h >= 1; h >>= 1) {
+        for (int h = 8; h >= 1; h >>= 1) {
             const bool up = lane & h;
 #pragma unroll
             for (int i = 0; i < h; ++i) {
@@ -485,7 +498,7 @@ __device__ __forceinline__ void lin_block_finish(const double (&acc)[kNumAcc], c
 // CERT: correspondence certificates (gicp_align, R27): read cache_old (DUAL) and
 // write cache_new; the other callers compile the tracking out
 template <bool REUSE, bool ERROR_ONLY, bool SORTED, bool SPOS, bool DUAL, bool CERT, bool PRE = false>
-__global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
+__global__ void __launch_bounds__(kLinBlock, GICP_LIN_MINB) k_linearize(const float* __restrict__ src, const float* __restrict__ src_cov,
                                                          int64_t ns, const float4* __restrict__ pts,
                                                          const float4* __restrict__ pts_orig, Levels lvs, int64_t nt,
                                                          const float* __restrict__ tgt_cov,
@@ -530,12 +543,10 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             cache_old = ccur;
         }
     }
-    double acc[kNumAcc];
+    static_assert(kPPT == 1, "one point per thread: its terms are the fp32 values tv");
+    float tv[kTV];
 #pragma unroll
-    for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
-    double cnt = 0.0, cnt_old = 0.0;
-    double eold[kNumAcc];
-    eold[27] = 0.0;
+    for (int c = 0; c < kTV; ++c) tv[c] = 0.0f;
     const int tl = (int)(threadIdx.x % kTeam);  // lane within the point's team
     const int64_t base = p0 + (int64_t)blk * kPPB + threadIdx.x / kTeam;
 #pragma unroll 1
@@ -637,20 +648,26 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
         // lane 0 of the team adds the new pair, the last lane the DUAL trial term
         const bool do_new = tl == 0, do_old = DUAL && tl == kTeam - 1;
         if ((do_new && orig >= 0) || do_old) load_cov6(src_cov, i, cp);
-        double e_new = 0.0;
+        float e_new = 0.0f;
         if (do_new && orig >= 0) {
             if (SORTED)
                 load_cov_sorted(tgt_cov_sorted, spos, cq);
             else
                 load_cov6(tgt_cov, orig, cq);
-            e_new = accumulate_point<ERROR_ONLY>(sP, pp, qx, qy, qz, cp, cq, acc);
-            cnt += 1.0;
+            float t[27];
+            e_new = point_terms_at<ERROR_ONLY>(sP, pp, qx, qy, qz, cp, cq, t);
+            if (!ERROR_ONLY) {
+#pragma unroll
+                for (int c = 0; c < 27; ++c) tv[c] = 0.0f + t[c];
+            }
+            tv[27] = 0.0f + e_new;
+            tv[28] = 1.0f;
         }
         if (do_old) {  // the trial cost with the previous correspondences
             const int c = corr_old[i];
             if (c >= 0 && c < nt) {
                 if (kTeam == 1 && orig >= 0 && c == (SPOS ? spos : orig)) {
-                    eold[27] += e_new;  // the same pair at the same pose: the same term, bitwise
+                    tv[29] = 0.0f + e_new;  // the same pair at the same pose: the same term, bitwise
                 } else {
                     const float4 q = SPOS ? __ldg(pts + c) : __ldg(pts_orig + c);
                     const int so = SPOS ? c : __float_as_int(q.w);
@@ -659,9 +676,10 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
                         load_cov_sorted(tgt_cov_sorted, so, cq);
                     else
                         load_cov6(tgt_cov, oo, cq);
-                    accumulate_point<true>(sP, pp, q.x, q.y, q.z, cp, cq, eold);
+                    float t[27];
+                    tv[29] = 0.0f + point_terms_at<true>(sP, pp, q.x, q.y, q.z, cp, cq, t);
                 }
-                cnt_old += 1.0;
+                tv[30] = 1.0f;
             }
         }
     }
@@ -674,8 +692,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
             atomicAdd(&g_lprof[40 + min(31, 31 - __clz(mx | 1))], 1ull);
         }
     })
-    lin_block_finish<ERROR_ONLY, DUAL>(acc, cnt, eold[27], cnt_old, scan, blk, nblk, gblk, partials, done, out29, flag,
-                                       seq, bv);
+    lin_block_finish<ERROR_ONLY, DUAL>(tv, scan, blk, nblk, gblk, partials, done, out29, flag, seq, bv);
 }
 
 // Terms from given correspondences (gicp_align: the trial evaluation e' alone, and
@@ -686,7 +703,7 @@ __global__ void __launch_bounds__(kLinBlock, 4) k_linearize(const float* __restr
 // read directly, and that target point and covariance) is issued before the block
 // waits for its pose, whose copy into shared memory is spread over the first threads.
 template <bool ERROR_ONLY, bool DUAL, bool PRE>
-__global__ void __launch_bounds__(kLinBlock, 4)
+__global__ void __launch_bounds__(kLinBlock, GICP_LIN_MINB)
     k_lin_terms(const float* __restrict__ src, const float* __restrict__ src_cov, int64_t ns,
                 const float4* __restrict__ pts, int64_t nt, const float4* __restrict__ tgt_cov_sorted, Pose P,
                 const int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old, double* __restrict__ partials,
@@ -743,35 +760,38 @@ __global__ void __launch_bounds__(kLinBlock, 4)
     load_cov_sorted(tgt_cov_sorted, vn ? cn : 0, cq);
     __syncthreads();
     if (bv.btab && !sP.active) return;  // block-uniform: converged registration
-    double acc[kNumAcc];
+    float tv[kTV];
 #pragma unroll
-    for (int c = 0; c < kNumAcc; ++c) acc[c] = 0.0;
-    double cnt = 0.0, cnt_old = 0.0, eold[kNumAcc];
-    eold[27] = 0.0;
+    for (int c = 0; c < kTV; ++c) tv[c] = 0.0f;
     if (active) {
         double pp[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
             pp[a] = __fma_rn(sP.R[3 * a + 2], pz, __fma_rn(sP.R[3 * a + 1], py, __fma_rn(sP.R[3 * a], px, sP.t[a])));
-        double e_new = 0.0;
+        float e_new = 0.0f;
         if (vn) {
-            e_new = accumulate_point<ERROR_ONLY>(sP, pp, q.x, q.y, q.z, cp, cq, acc);
-            cnt += 1.0;
+            float t[27];
+            e_new = point_terms_at<ERROR_ONLY>(sP, pp, q.x, q.y, q.z, cp, cq, t);
+            if (!ERROR_ONLY) {
+#pragma unroll
+                for (int c = 0; c < 27; ++c) tv[c] = 0.0f + t[c];
+            }
+            tv[27] = 0.0f + e_new;
+            tv[28] = 1.0f;
         }
         if (vo) {  // the trial cost with the previous correspondences
             if (vn && co == cn) {
-                eold[27] += e_new;  // the same pair at the same pose: the same term, bitwise
+                tv[29] = 0.0f + e_new;  // the same pair at the same pose: the same term, bitwise
             } else {
                 const float4 qo = __ldg(pts + co);
-                float cqo[6];
+                float cqo[6], t[27];
                 load_cov_sorted(tgt_cov_sorted, co, cqo);
-                accumulate_point<true>(sP, pp, qo.x, qo.y, qo.z, cp, cqo, eold);
+                tv[29] = 0.0f + point_terms_at<true>(sP, pp, qo.x, qo.y, qo.z, cp, cqo, t);
             }
-            cnt_old += 1.0;
+            tv[30] = 1.0f;
         }
     }
-    lin_block_finish<ERROR_ONLY, DUAL>(acc, cnt, eold[27], cnt_old, scan, blk, nblk, gblk, partials, done, out29, flag,
-                                       seq, bv);
+    lin_block_finish<ERROR_ONLY, DUAL>(tv, scan, blk, nblk, gblk, partials, done, out29, flag, seq, bv);
 }
 
 // ---------------------------------------------------------------------------
