@@ -593,7 +593,7 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
     const int64_t nsa = ns > 0 ? ns : 1;
     const size_t lin_bytes = linearize_scratch_bytes(nsa);
     const size_t bytes = 512 + lin_bytes + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 256 +
-                         (GICP_ALIGN_CACHE ? 3 * nsa * sizeof(float4) + 64 : 0);
+                         (GICP_ALIGN_CACHE ? 4 * nsa * sizeof(float4) + 64 : 0);
     char* scratch = nullptr;
     if (cudaMallocAsync((void**)&scratch, bytes, s) != cudaSuccess) {
         cudaGetLastError();
@@ -615,7 +615,8 @@ GICP_API int gicp_align(const float* src, const float* src_cov, int64_t ns, gicp
         cache_b = cache_a + nsa;
         if (split_eval(nsa)) {  // the split evaluation's search queue and counter
             ls.queue = cache_b + nsa;
-            ls.qcount = (unsigned*)(ls.queue + nsa);
+            ls.queue2 = ls.queue + nsa;
+            ls.qcount = (unsigned*)(ls.queue2 + nsa);
         }
     }
     auto cache_of = [&](const int32_t* c) -> float4* { return c == corr_a ? cache_a : (c == corr_b ? cache_b : nullptr); };
@@ -1042,14 +1043,14 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
                              (size_t)std::max(E, 1) * sizeof(int) + 768;
     if ((rc = batch_scratch(offsets, E,
                             2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
-                                (certs ? 3 * nsa * sizeof(float4) + 64 : 0) + dev_extra,
+                                (certs ? 4 * nsa * sizeof(float4) + 64 : 0) + dev_extra,
                             s, bs, &ex, B)))
         return rc;
     double* Ed = nullptr;  // device entry rows [E][32] (device sharding)
     int* gid_d = nullptr;
     // entry -> registration (the poses go up per registration, not per entry)
     int* ereg_d = (int*)(((uintptr_t)ex + 2 * nsa * sizeof(int32_t) + nsa * 9 * sizeof(float) + 64 +
-                          (certs ? 3 * nsa * sizeof(float4) + 64 : 0) + 255) & ~(uintptr_t)255);
+                          (certs ? 4 * nsa * sizeof(float4) + 64 : 0) + 255) & ~(uintptr_t)255);
     if (ds) {
         Ed = (double*)(((uintptr_t)(ereg_d + std::max(E, 1)) + 255) & ~(uintptr_t)255);
         gid_d = (int*)(Ed + 32 * (size_t)std::max(E, 1));
@@ -1076,7 +1077,8 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
         bs.ls.cache_old = bs.ls.cache_new + nsa;
         if (split_eval(nsa)) {  // the split evaluation's search queue and counter
             bs.ls.queue = bs.ls.cache_new + 2 * nsa;
-            bs.ls.qcount = (unsigned*)(bs.ls.queue + nsa);
+            bs.ls.queue2 = bs.ls.queue + nsa;
+            bs.ls.qcount = (unsigned*)(bs.ls.queue2 + nsa);
         }
     }
     if (ns > 0 && (rc = sort_source(src, src_cov, ns, tgt->lv[0].cell, src_p, cov_p, s, bs.offs, E))) {

@@ -263,7 +263,8 @@ struct LinScratch {
     // points that must search ({search point, i | flags}, one per source point) and
     // its device counter
     float4* queue = nullptr;
-    unsigned* qcount = nullptr;
+    float4* queue2 = nullptr;    // the points the first search pass leaves to the full search
+    unsigned* qcount = nullptr;  // [4]: queue length, its claim counter, queue2 length, its claim counter
 };
 constexpr int kLinCorrSpos = 1 << 8;  // internal flag: corr holds sorted positions
 constexpr int kLinCoarse = 1 << 10;   // internal flag: single launches set Pose::coarse

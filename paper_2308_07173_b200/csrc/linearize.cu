@@ -45,6 +45,16 @@ __device__ unsigned long long g_lprof[80];  // [0..3] stage counts, [4] max sear
 #ifndef GICP_LIN_MINB
 #define GICP_LIN_MINB 4  // blocks per SM the fused / terms kernels are compiled for
 #endif
+#ifndef GICP_LIN_STREAM
+#define GICP_LIN_STREAM 0  // 1: per-point streams (source, certificates, correspondences, queue) evict-first
+#endif
+#if GICP_LIN_STREAM
+#define LDS_(p) __ldcs(p)
+#define STS_(p, v) __stcs((p), (v))
+#else
+#define LDS_(p) (*(p))
+#define STS_(p, v) (*(p) = (v))
+#endif
 #ifndef GICP_LIN_WARM
 #define GICP_LIN_WARM 0
 #endif
@@ -75,7 +85,11 @@ struct Levels {
 // first): code = (dx + 1) + 3 (dy + 1) + 9 (dz + 1)
 __constant__ int c_cube27[27] = {13, 12, 14, 10, 16, 4, 22, 9, 11, 15, 17, 3, 5, 21, 23, 1, 7, 19, 25, 0, 2, 6, 8, 18, 20, 24, 26};
 
-template <bool CERT, int UNR = kUnroll>
+// LEAN (k_lin_search's first pass): only the level-0 cube through adjacency lists;
+// a lane whose own voxel has no list, or whose cube does not settle the search,
+// returns overflow = 2 untouched otherwise and is searched again in full (the
+// result is the same exact minimum: the full search repeats the same stage 1)
+template <bool CERT, int UNR = kUnroll, bool LEAN = false>
 __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const Levels& lvs, bool active, float qx,
                                           float qy, float qz, float r2, unsigned long long& best, int& bj,
                                           int& overflow, const int t, float& rho, const int l0,
@@ -153,6 +167,10 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 a1 = oc.x + oc.y;
             }
         }
+        if (LEAN && active && !use_adj) {  // no adjacency list: the full search
+            overflow = 2;
+            active = false;
+        }
         const float lox = axis_gap(-1, G.fx, s, slack), hix = axis_gap(1, G.fx, s, slack);
         const float loy = axis_gap(-1, G.fy, s, slack), hiy = axis_gap(1, G.fy, s, slack);
         const float loz = axis_gap(-1, G.fz, s, slack), hiz = axis_gap(1, G.fz, s, slack);
@@ -187,7 +205,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 float lb2;
                 bool inside = true;
                 int cx = 0, cy = 0, cz = 0;
-                if (use_adj) {
+                if (LEAN || use_adj) {
                     const int2 e = ne;
                     if (k + 1 < cnt) ne = __ldg(adj_rng + a0 + k + 1);
                     r = adj_range(e);
@@ -200,7 +218,7 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
                 } else if (lb2 * kRel > bound()) {
                     r = make_int2(0, 0);
                     if (CERT) lbp = fminf(lbp, lb2);
-                } else if (!use_adj) {
+                } else if (!LEAN && !use_adj) {
                     r = hash_find(g, cell_key(cx, cy, cz));
                     if (r.y <= r.x) r = make_int2(0, 0);
                 }
@@ -248,6 +266,11 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
             finish();
             return;
         }
+    }
+    if constexpr (LEAN) {  // the cube did not settle it: the full search
+        overflow = 2;
+        finish();
+        return;
     }
     // (2) per lane: coarser levels' cubes up to ring_level, then rings there
     LPROF(atomicAdd(&g_lprof[1], 1ull);)
@@ -342,6 +365,17 @@ __device__ __forceinline__ void load_cov_sorted(const float4* __restrict__ c8, i
     o[3] = a.w;
     o[4] = b.x;
     o[5] = b.y;
+}
+
+__device__ __forceinline__ void load_cov6_stream(const float* __restrict__ c, int64_t row, float o[6]) {
+    const float2* p = reinterpret_cast<const float2*>(c + row * 6);
+    const float2 a = LDS_(p), b = LDS_(p + 1), d = LDS_(p + 2);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = b.x;
+    o[3] = b.y;
+    o[4] = d.x;
+    o[5] = d.y;
 }
 
 __device__ __forceinline__ void load_cov6(const float* __restrict__ c, int64_t row, float o[6]) {
@@ -747,12 +781,12 @@ __global__ void __launch_bounds__(kLinBlock, GICP_LIN_MINB)
     double px = 0.0, py = 0.0, pz = 0.0;
     float cp[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (active) {
-        cn = cbuf[i];
-        if (DUAL) co = obuf[i];
-        px = src[3 * i];
-        py = src[3 * i + 1];
-        pz = src[3 * i + 2];
-        load_cov6(src_cov, i, cp);
+        cn = LDS_(cbuf + i);
+        if (DUAL) co = LDS_(obuf + i);
+        px = LDS_(src + 3 * i);
+        py = LDS_(src + 3 * i + 1);
+        pz = LDS_(src + 3 * i + 2);
+        load_cov6_stream(src_cov, i, cp);
     }
     const bool vn = cn >= 0 && cn < nt, vo = DUAL && co >= 0 && co < nt;
     const float4 q = __ldg(pts + (vn ? cn : 0));
@@ -847,9 +881,9 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
     if (active) {
         // the point, its certificate and its previous correspondence: independent
         // loads, issued together
-        const double px = src[3 * i], py = src[3 * i + 1], pz = src[3 * i + 2];
-        const float4 cc = (DUAL && cache_old) ? __ldg(cache_old + i) : make_float4(0.f, 0.f, 0.f, -1.f);
-        const int bj = (DUAL && cache_old) ? corr_old[i] : 0;
+        const double px = LDS_(src + 3 * i), py = LDS_(src + 3 * i + 1), pz = LDS_(src + 3 * i + 2);
+        const float4 cc = (DUAL && cache_old) ? LDS_(cache_old + i) : make_float4(0.f, 0.f, 0.f, -1.f);
+        const int bj = (DUAL && cache_old) ? LDS_(corr_old + i) : 0;
         double pp[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
@@ -865,8 +899,8 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
             if (cached) {  // the certified pair: its distance at the new search point, the gate
                 const float4 q = __ldg(pts + bj);
                 const bool inl = dist2(sx, sy, sz, q.x, q.y, q.z) < r2;
-                corr[i] = inl ? bj : -1;
-                cache_new[i] = cc;
+                STS_(corr + i, inl ? bj : -1);
+                STS_(cache_new + i, cc);
             }
         }
     }
@@ -879,7 +913,7 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
     base = __shfl_sync(0xffffffffu, base, leader);
     if (push) {
         const unsigned w = (unsigned)i | ((sP.coarse && coarse_ok) ? (1u << 30) : 0u) | (wbase << 31);
-        queue[base + __popc(m & ((1u << lane) - 1u))] = make_float4(sx, sy, sz, __uint_as_float(w));
+        STS_(queue + base + __popc(m & ((1u << lane) - 1u)), make_float4(sx, sy, sz, __uint_as_float(w)));
     }
 }
 
@@ -887,42 +921,61 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
 #define GICP_SEARCH_MINB 4  // 64 registers: more warps spill, and measured slower (4: 1.64, 5: 2.04, 8: 2.22 ms)
 #endif
 #ifndef GICP_SEARCH_UNROLL
-#define GICP_SEARCH_UNROLL 2  // (4: 1.64, 2: 1.58, 8: 1.92 ms)
+#define GICP_SEARCH_UNROLL 4  // with the lean first pass (dual launch): 4: 1.12, 2: 1.15 ms
 #endif
 constexpr int kSearchBlock = 256;
 #ifndef GICP_SPLIT_MIN
 #define GICP_SPLIT_MIN (1 << 20)
 #endif
 constexpr int64_t kSplitMinPoints = GICP_SPLIT_MIN;
+// LEAN: the first pass over the queue (qcount[0] entries, claimed through
+// qcount[1]); points it cannot settle go to queue2 (qcount[2], claimed through
+// qcount[3]) for the full search (LEAN = false)
+template <bool LEAN>
 __global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
     k_lin_search(const float4* __restrict__ pts, Levels lvs, int64_t nt, float r2, int32_t* __restrict__ corr_a,
                  int32_t* __restrict__ corr_b, float4* __restrict__ cache_a, float4* __restrict__ cache_b,
-                 const float4* __restrict__ queue, const unsigned* __restrict__ qcount) {
-    // qcount[0]: queue length; qcount[1]: the next unclaimed entry (each warp claims
-    // 32 at a time: dynamic balance, and warps in flight work on neighbouring entries)
-    const unsigned n = qcount[0];
+                 const float4* __restrict__ queue, float4* __restrict__ queue2, unsigned* __restrict__ qcount) {
+    // each warp claims 32 entries at a time: dynamic balance, and warps in flight
+    // work on neighbouring entries
+    const unsigned n = LEAN ? qcount[0] : qcount[2];
+    unsigned* claim = qcount + (LEAN ? 1 : 3);
+    const float4* q = LEAN ? queue : queue2;
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned w0 = 0;
-        if (lane == 0) w0 = atomicAdd(const_cast<unsigned*>(qcount) + 1, 32u);
+        if (lane == 0) w0 = atomicAdd(claim, 32u);
         w0 = __shfl_sync(0xffffffffu, w0, 0);
         if (w0 >= n) break;
         const unsigned k = w0 + lane;
         const bool active = k < n;  // warp-uniform loop: every lane reaches the search
         float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (active) e = __ldg(queue + k);
+        if (active) e = LDS_(q + k);
         const unsigned w = __float_as_uint(e.w);
         unsigned long long best;
         int bj, ovf;
         float rho;
-        nn_search<true, GICP_SEARCH_UNROLL>(pts, lvs, active, e.x, e.y, e.z, r2, best, bj, ovf, 0, rho, (w >> 30) & 1u);
+        nn_search<true, GICP_SEARCH_UNROLL, LEAN>(pts, lvs, active, e.x, e.y, e.z, r2, best, bj, ovf, 0, rho,
+                                                  (w >> 30) & 1u);
+        if (LEAN) {  // the unsettled: to the full search
+            const bool push = active && ovf == 2;
+            const unsigned m = __ballot_sync(0xffffffffu, push);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                unsigned base = 0;
+                if (lane == leader) base = atomicAdd(qcount + 2, (unsigned)__popc(m));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (push) queue2[base + __popc(m & ((1u << lane) - 1u))] = e;
+            }
+            if (push) continue;
+        }
         if (active) {
             if (ovf) nn_bruteforce(pts, nt, e.x, e.y, e.z, best, bj);
             const float bd2 = __uint_as_float((unsigned)(best >> 32));
             const bool inl = best != kEmptyKey && bd2 < r2;
             const int64_t i = w & 0x3fffffffu;
-            (w >> 31 ? corr_a : corr_b)[i] = inl ? bj : -1;
-            (w >> 31 ? cache_a : cache_b)[i] = make_float4(e.x, e.y, e.z, (inl && !ovf) ? rho : -1.0f);
+            STS_((w >> 31 ? corr_a : corr_b) + i, inl ? bj : -1);
+            STS_((w >> 31 ? cache_a : cache_b) + i, make_float4(e.x, e.y, e.z, (inl && !ovf) ? rho : -1.0f));
         }
     }
 }
@@ -1011,7 +1064,7 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
     int64_t split_min = kSplitMinPoints;
     if (const char* e = getenv("GICP_LIN_SPLIT_MIN")) split_min = atoll(e);
     if (cert && scr.queue && ns >= split_min) {
-        int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, 2 * sizeof(unsigned), s), "memset");
+        int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, 4 * sizeof(unsigned), s), "memset");
         if (rc) return rc;
         if (dual)
             k_lin_cert<true><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
@@ -1021,24 +1074,26 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
             k_lin_cert<false><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
                                                                   corr_old, bvq, scr.cache_new, scr.cache_old,
                                                                   scr.queue, scr.qcount);
-        static int grid = 0;
+        static int grid = 0, grid2 = 0;
         if (grid == 0) {
-            int dev = 0, sms = 0, per = 0;
+            int dev = 0, sms = 0, per = 0, per2 = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#ifdef GICP_SEARCH_CARVEOUT
-            cudaFuncSetAttribute(k_lin_search, cudaFuncAttributePreferredSharedMemoryCarveout, GICP_SEARCH_CARVEOUT);
-#endif
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lin_search, kSearchBlock, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lin_search<true>, kSearchBlock, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_lin_search<false>, kSearchBlock, 0);
             grid = std::max(1, sms * std::max(per, 1));
+            grid2 = std::max(1, sms * std::max(per2, 1));
         }
         // single launches: (corr, cache_new) are the written pair (w bit 31 = 1)
         int32_t* ca = corr;
         int32_t* cb = const_cast<int32_t*>(corr_old);
         const unsigned g2 = (unsigned)std::min<int64_t>(grid, (ns + kSearchBlock - 1) / kSearchBlock);
-        k_lin_search<<<std::max(g2, 1u), kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
-                                                               const_cast<float4*>(scr.cache_old), scr.queue,
-                                                               scr.qcount);
+        k_lin_search<true><<<std::max(g2, 1u), kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
+                                                                     const_cast<float4*>(scr.cache_old), scr.queue,
+                                                                     scr.queue2, scr.qcount);
+        k_lin_search<false><<<(unsigned)std::min<int64_t>(grid2, std::max<int64_t>(1, g2)), kSearchBlock, 0, s>>>(
+            tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new, const_cast<float4*>(scr.cache_old), scr.queue,
+            scr.queue2, scr.qcount);
         if (dual)
             k_lin_terms<false, true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_TERMS_ARGS);
         else
