@@ -124,10 +124,13 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     // rho = half the gap between the best distance and every other point's lower
     // bound, minus a rounding margin: a search point that moved less than rho keeps
     // this nearest neighbour (distances change by at most the move)
+    // The certificate also keeps the pair inside the gate: rho <= (r - d1) minus the
+    // same rounding margin, so a carried pair is an inlier without re-measuring it
+    // (k_lin_cert then needs no load of the target point)
     auto certify = [&](float m2) {
         const float l2 = fminf(fminf(__uint_as_float(sh2), lbp * kRel), m2);
-        const float d1 = sqrtf(__uint_as_float(bh)), dl = sqrtf(l2);
-        rho = 0.5f * (dl - d1) - 1e-6f * (dl + d1) - 1e-6f;
+        const float d1 = sqrtf(__uint_as_float(bh)), dl = sqrtf(l2), r = sqrtf(r2);
+        rho = fminf(0.5f * (dl - d1) - 1e-6f * (dl + d1) - 1e-6f, (r - d1) - 1e-6f * (r + d1) - 1e-6f);
     };
     auto finish = [&]() {
         best = ((unsigned long long)bh << 32) | bo;
@@ -896,21 +899,32 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
                 const double ex = (double)sx - cc.x, ey = (double)sy - cc.y, ez = (double)sz - cc.z;
                 cached = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc.w;
             }
-            if (cached) {  // the certified pair: its distance at the new search point, the gate
-                const float4 q = __ldg(pts + bj);
-                const bool inl = dist2(sx, sy, sz, q.x, q.y, q.z) < r2;
-                STS_(corr + i, inl ? bj : -1);
+            if (cached) {  // the certified pair (inside the gate by construction of rho)
+                STS_(corr + i, bj);
                 STS_(cache_new + i, cc);
             }
         }
     }
+    // one queue reservation per block (the counter is a single address: per-warp
+    // atomics serialise at the L2); the warps' slots follow in warp order
     const bool push = active && !cached;
     const unsigned m = __ballot_sync(0xffffffffu, push);
-    if (m == 0u) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(qcount, (unsigned)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ unsigned wcnt[kLinBlock / 32], bbase;
+    if (lane == 0) wcnt[wid] = (unsigned)__popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+#pragma unroll
+        for (int w = 0; w < kLinBlock / 32; ++w) {
+            const unsigned c = wcnt[w];
+            wcnt[w] = tot;
+            tot += c;
+        }
+        bbase = tot ? atomicAdd(qcount, tot) : 0u;
+    }
+    __syncthreads();
+    const unsigned base = bbase + wcnt[wid];
     if (push) {
         const unsigned w = (unsigned)i | ((sP.coarse && coarse_ok) ? (1u << 30) : 0u) | (wbase << 31);
         STS_(queue + base + __popc(m & ((1u << lane) - 1u)), make_float4(sx, sy, sz, __uint_as_float(w)));
@@ -924,6 +938,9 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
 #define GICP_SEARCH_UNROLL 4  // with the lean first pass (dual launch): 4: 1.12, 2: 1.15 ms
 #endif
 constexpr int kSearchBlock = 256;
+#ifndef GICP_SEARCH_CLAIM
+#define GICP_SEARCH_CLAIM 32  // queue entries a warp claims at a time (128: C4 dual 1.12 -> 1.20 ms)
+#endif
 #ifndef GICP_SPLIT_MIN
 #define GICP_SPLIT_MIN (1 << 20)
 #endif
@@ -942,13 +959,22 @@ __global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
     unsigned* claim = qcount + (LEAN ? 1 : 3);
     const float4* q = LEAN ? queue : queue2;
     const int lane = threadIdx.x & 31;
+    // (a claim covers kClaim entries, walked 32 at a time: fewer atomics on the one
+    // counter address)
+    constexpr unsigned kClaim = GICP_SEARCH_CLAIM;
+    unsigned w0 = 0, wend = 0;
     for (;;) {
-        unsigned w0 = 0;
-        if (lane == 0) w0 = atomicAdd(claim, 32u);
-        w0 = __shfl_sync(0xffffffffu, w0, 0);
-        if (w0 >= n) break;
+        if (w0 >= wend) {
+            unsigned c = 0;
+            if (lane == 0) c = atomicAdd(claim, kClaim);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if (c >= n) break;
+            w0 = c;
+            wend = min(c + kClaim, n);
+        }
         const unsigned k = w0 + lane;
-        const bool active = k < n;  // warp-uniform loop: every lane reaches the search
+        w0 += 32;
+        const bool active = k < wend;  // warp-uniform loop: every lane reaches the search
         float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
         if (active) e = LDS_(q + k);
         const unsigned w = __float_as_uint(e.w);
