@@ -941,6 +941,13 @@ constexpr int kSearchBlock = 256;
 #ifndef GICP_SEARCH_CLAIM
 #define GICP_SEARCH_CLAIM 32  // queue entries a warp claims at a time (128: C4 dual 1.12 -> 1.20 ms)
 #endif
+#ifndef GICP_FULL_PER_WARP
+#define GICP_FULL_PER_WARP 32
+#endif
+#ifndef GICP_COOP_MAX
+#define GICP_COOP_MAX 16384  // queue2 sizes searched a warp per point (larger: per lane)
+#endif
+constexpr unsigned kCoopMax = GICP_COOP_MAX;
 #ifndef GICP_SPLIT_MIN
 #define GICP_SPLIT_MIN (1 << 20)
 #endif
@@ -952,16 +959,22 @@ template <bool LEAN>
 __global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
     k_lin_search(const float4* __restrict__ pts, Levels lvs, int64_t nt, float r2, int32_t* __restrict__ corr_a,
                  int32_t* __restrict__ corr_b, float4* __restrict__ cache_a, float4* __restrict__ cache_b,
-                 const float4* __restrict__ queue, float4* __restrict__ queue2, unsigned* __restrict__ qcount) {
+                 const float4* __restrict__ queue, float4* __restrict__ queue2, unsigned* __restrict__ qcount,
+                 unsigned max_coop) {
     // each warp claims 32 entries at a time: dynamic balance, and warps in flight
     // work on neighbouring entries
     const unsigned n = LEAN ? qcount[0] : qcount[2];
+    if (!LEAN && n <= max_coop) return;  // a small queue2: k_lin_search_coop takes it
     unsigned* claim = qcount + (LEAN ? 1 : 3);
     const float4* q = LEAN ? queue : queue2;
     const int lane = threadIdx.x & 31;
     // (a claim covers kClaim entries, walked 32 at a time: fewer atomics on the one
     // counter address)
-    constexpr unsigned kClaim = GICP_SEARCH_CLAIM;
+    // The full pass takes kPer entries per warp: its points diverge (per-lane coarse
+    // levels and rings), so a warp of 32 would serialise them; its queue is small
+    // (~3 % of the searches) and the grid has warps to spare.
+    constexpr unsigned kPer = LEAN ? 32u : GICP_FULL_PER_WARP;
+    constexpr unsigned kClaim = LEAN ? GICP_SEARCH_CLAIM : kPer;
     unsigned w0 = 0, wend = 0;
     for (;;) {
         if (w0 >= wend) {
@@ -972,8 +985,8 @@ __global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
             w0 = c;
             wend = min(c + kClaim, n);
         }
-        const unsigned k = w0 + lane;
-        w0 += 32;
+        const unsigned k = w0 + (lane < (int)kPer ? lane : 0x40000000);
+        w0 += kPer;
         const bool active = k < wend;  // warp-uniform loop: every lane reaches the search
         float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
         if (active) e = LDS_(q + k);
@@ -1002,6 +1015,189 @@ __global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
             const int64_t i = w & 0x3fffffffu;
             STS_((w >> 31 ? corr_a : corr_b) + i, inl ? bj : -1);
             STS_((w >> 31 ? cache_a : cache_b) + i, make_float4(e.x, e.y, e.z, (inl && !ovf) ? rho : -1.0f));
+        }
+    }
+}
+
+// The full pass for a SMALL queue2 (the common case: ~3 % of a dual launch's
+// searches): one point per warp, the 32 lanes probing cells and scanning candidates
+// together, so a point's chain of dependent probes (27 cells, then rings of 98+) is
+// ~4 rounds deep instead of ~125 (the per-lane pass is latency-bound on that chain).
+// Same exact minimum (d2 bits, original index) and the same stop rules as
+// nn_search; the certificate is issued at the cube exit only, like nn_search.
+__global__ void __launch_bounds__(kSearchBlock)
+    k_lin_search_coop(const float4* __restrict__ pts, Levels lvs, int64_t nt, float r2, int32_t* __restrict__ corr_a,
+                      int32_t* __restrict__ corr_b, float4* __restrict__ cache_a, float4* __restrict__ cache_b,
+                      const float4* __restrict__ queue2, unsigned* __restrict__ qcount, unsigned max_coop) {
+    const unsigned n = qcount[2];
+    if (n > max_coop) return;  // a large queue: the per-lane pass (k_lin_search<false>) takes it
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned k = 0;
+        if (lane == 0) k = atomicAdd(qcount + 3, 1u);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= n) break;
+        const float4 e = __ldg(queue2 + k);
+        const unsigned w = __float_as_uint(e.w);
+        const int l0 = (int)((w >> 30) & 1u);
+        const float qx = e.x, qy = e.y, qz = e.z;
+        unsigned bh = 0xffffffffu, bo = 0xffffffffu, sh2 = 0xffffffffu;
+        int bj = -1;
+        float lbp = __int_as_float(0x7f800000);
+        auto consider = [&](int j) {
+            const float4 p = __ldg(pts + j);
+            const unsigned h = __float_as_uint(dist2(qx, qy, qz, p.x, p.y, p.z));
+            const unsigned o = __float_as_uint(p.w);
+            const bool better = h < bh || (h == bh && o < bo);
+            sh2 = better ? bh : (h < sh2 ? h : sh2);
+            bh = better ? h : bh;
+            bo = better ? o : bo;
+            bj = better ? j : bj;
+        };
+        // warp minimum of the best keys (every lane gets it); the bound for pruning
+        auto wmin_h = [&]() {
+            unsigned h = bh;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) h = min(h, __shfl_xor_sync(0xffffffffu, h, o));
+            return h;
+        };
+        auto bound = [&]() { return fminf(__uint_as_float(wmin_h()), r2); };
+        auto scan = [&](int2 r) {
+            for (int j = r.x + lane; j < r.y; j += 32) consider(j);
+        };
+        // cooperative cube at level l: lane c < 27 probes cell c_cube27[c]; cells then
+        // taken in that (nearest-first) order, pruned against the warp's bound
+        auto cube = [&](int l, bool track) {
+            const Grid& g = lvs.lv[l];
+            const QGeom G = make_geom(g, qx, qy, qz);
+            const float s = g.cell, slack = g.slack;
+            int2 rc = make_int2(0, 0);
+            float lbc = 0.0f;
+            bool in = false;
+            if (lane < 27) {
+                const int code = c_cube27[lane];
+                const int dx = (code % 3) - 1, dy = ((code / 3) % 3) - 1, dz = (code / 9) - 1;
+                const int cx = G.cx + dx, cy = G.cy + dy, cz = G.cz + dz;
+                in = (unsigned)cx < (unsigned)g.nx && (unsigned)cy < (unsigned)g.ny && (unsigned)cz < (unsigned)g.nz;
+                const float gx = axis_gap(dx, G.fx, s, slack), gy = axis_gap(dy, G.fy, s, slack),
+                            gz = axis_gap(dz, G.fz, s, slack);
+                lbc = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                if (in && !(lbc * kRel > r2)) rc = hash_find(g, cell_key(cx, cy, cz));
+            }
+            for (int c = 0; c < 27; ++c) {
+                const bool ci = __shfl_sync(0xffffffffu, in, c);
+                if (!ci) continue;
+                const float lb = __shfl_sync(0xffffffffu, lbc, c);
+                if (lb * kRel > bound()) {
+                    if (track) lbp = fminf(lbp, lb);
+                    continue;
+                }
+                const int2 r = make_int2(__shfl_sync(0xffffffffu, rc.x, c), __shfl_sync(0xffffffffu, rc.y, c));
+                if (r.y > r.x) scan(r);
+            }
+            return G;
+        };
+        float rho = -1.0f;
+        int ovf = 0;
+        bool done = false;
+        {
+            const Grid& g = lvs.lv[l0];
+            const QGeom G = cube(l0, true);
+            const float m = cube_margin(G, g.cell, g.slack, 1);
+            const unsigned wb = wmin_h();
+            const float bnd = fminf(__uint_as_float(wb), r2);
+            const bool whole = G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 &&
+                               G.cz >= g.nz - 2;
+            if ((m > 0.0f && bnd < m * m * kRel) || whole) {
+                done = true;
+                if (wb != 0xffffffffu) {  // certificate: second-smallest scanned, pruned bounds, outside
+                    // the second smallest over the warp: the winner's own second, the others' bests
+                    unsigned wo = bh == wb ? bo : 0xffffffffu;
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) wo = min(wo, __shfl_xor_sync(0xffffffffu, wo, o));
+                    unsigned s2 = (bh == wb && bo == wo) ? sh2 : bh;
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) s2 = min(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+                    const float m2 = whole ? __int_as_float(0x7f800000) : m * m * kRel;
+                    const float l2 = fminf(fminf(__uint_as_float(s2), lbp * kRel), m2);
+                    const float d1 = sqrtf(__uint_as_float(wb)), dl = sqrtf(l2), rr = sqrtf(r2);
+                    rho = fminf(0.5f * (dl - d1) - 1e-6f * (dl + d1) - 1e-6f, (rr - d1) - 1e-6f * (rr + d1) - 1e-6f);
+                }
+            }
+        }
+        const int ring_level = max(lvs.ring_level, l0);
+        for (int l = l0 + 1; !done && l <= ring_level; ++l) {
+            const Grid& g = lvs.lv[l];
+            const QGeom G = cube(l, false);
+            const float m = cube_margin(G, g.cell, g.slack, 1);
+            if ((m > 0.0f && bound() < m * m * kRel) ||
+                (G.cx <= 1 && G.cx >= g.nx - 2 && G.cy <= 1 && G.cy >= g.ny - 2 && G.cz <= 1 && G.cz >= g.nz - 2))
+                done = true;
+        }
+        if (!done) {  // rings at ring_level, 32 cells probed at a time
+            const Grid& g = lvs.lv[ring_level];
+            const QGeom G = make_geom(g, qx, qy, qz);
+            const float s = g.cell, slack = g.slack;
+            const int R0 = max(max(max(-G.cx, G.cx - (g.nx - 1)), max(-G.cy, G.cy - (g.ny - 1))),
+                               max(-G.cz, G.cz - (g.nz - 1)));
+            for (int R = max(2, R0);; ++R) {
+                if (R > max(R0, 1) + kMaxRing) {
+                    ovf = 1;
+                    break;
+                }
+                const int side = 2 * R + 1, cells = side * side * side;
+                for (int c0 = 0; c0 < cells; c0 += 32) {
+                    const float bnd = bound();
+                    const int c = c0 + lane;
+                    int2 rc = make_int2(0, 0);
+                    if (c < cells) {
+                        const int dx = c % side - R, dy = (c / side) % side - R, dz = c / (side * side) - R;
+                        if (max(max(abs(dx), abs(dy)), abs(dz)) == R) {
+                            const float gx = axis_gap(dx, G.fx, s, slack), gy = axis_gap(dy, G.fy, s, slack),
+                                        gz = axis_gap(dz, G.fz, s, slack);
+                            const float lb2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, gx * gx));
+                            if (!(lb2 * kRel > bnd)) rc = cell_lookup(g, G.cx + dx, G.cy + dy, G.cz + dz);
+                        }
+                    }
+                    unsigned m = __ballot_sync(0xffffffffu, rc.y > rc.x);
+                    while (m) {
+                        const int src = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int2 r = make_int2(__shfl_sync(0xffffffffu, rc.x, src), __shfl_sync(0xffffffffu, rc.y, src));
+                        scan(r);
+                    }
+                }
+                const float mR = cube_margin(G, s, slack, R);
+                if (mR > 0.0f && bound() < mR * mR * kRel) break;
+                if (G.cx - R <= 0 && G.cx + R >= g.nx - 1 && G.cy - R <= 0 && G.cy + R >= g.ny - 1 && G.cz - R <= 0 &&
+                    G.cz + R >= g.nz - 1)
+                    break;
+            }
+        }
+        // the winner: the warp's minimum key and its sorted position
+        unsigned long long key = ((unsigned long long)bh << 32) | bo;
+        int kj = bj;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, key, o);
+            const int pj = __shfl_xor_sync(0xffffffffu, kj, o);
+            if (pk < key) {
+                key = pk;
+                kj = pj;
+            }
+        }
+        if (lane == 0) {
+            unsigned long long best = key;
+            int j = kj;
+            if (ovf) {
+                nn_bruteforce(pts, nt, qx, qy, qz, best, j);
+                rho = -1.0f;
+            }
+            const float bd2 = __uint_as_float((unsigned)(best >> 32));
+            const bool inl = best != kEmptyKey && bd2 < r2;
+            const int64_t i = w & 0x3fffffffu;
+            STS_((w >> 31 ? corr_a : corr_b) + i, inl ? j : -1);
+            STS_((w >> 31 ? cache_a : cache_b) + i, make_float4(qx, qy, qz, (inl && !ovf) ? rho : -1.0f));
         }
     }
 }
@@ -1116,10 +1312,23 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
         const unsigned g2 = (unsigned)std::min<int64_t>(grid, (ns + kSearchBlock - 1) / kSearchBlock);
         k_lin_search<true><<<std::max(g2, 1u), kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
                                                                      const_cast<float4*>(scr.cache_old), scr.queue,
-                                                                     scr.queue2, scr.qcount);
-        k_lin_search<false><<<(unsigned)std::min<int64_t>(grid2, std::max<int64_t>(1, g2)), kSearchBlock, 0, s>>>(
-            tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new, const_cast<float4*>(scr.cache_old), scr.queue,
-            scr.queue2, scr.qcount);
+                                                                     scr.queue2, scr.qcount, 0u);
+        // the unsettled points: cooperatively (a warp per point) while few, per lane
+        // otherwise (each kernel exits at once when the queue is the other's)
+        const unsigned g3 = (unsigned)std::min<int64_t>(grid2, std::max<int64_t>(1, g2));
+        k_lin_search<false><<<g3, kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
+                                                        const_cast<float4*>(scr.cache_old), scr.queue, scr.queue2,
+                                                        scr.qcount, kCoopMax);
+        k_lin_search_coop<<<g3, kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
+                                                      const_cast<float4*>(scr.cache_old), scr.queue2, scr.qcount,
+                                                      kCoopMax);
+        static const bool dbg = getenv("GICP_DEBUG_SPLIT") != nullptr;  // diagnostics: queue sizes
+        if (dbg) {
+            unsigned q[4];
+            cudaMemcpyAsync(q, scr.qcount, sizeof(q), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "[gicp split] points %lld queue %u full-search %u\n", (long long)ns, q[0], q[2]);
+        }
         if (dual)
             k_lin_terms<false, true, true><<<(unsigned)nb, kLinBlock, 0, s>>>(GICP_TERMS_ARGS);
         else
