@@ -117,8 +117,13 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
         LPROF(++ncand;)
         const unsigned h = __float_as_uint(dist2(qx, qy, qz, p.x, p.y, p.z));
         const unsigned o = __float_as_uint(p.w);
-        const bool better = h < bh || (h == bh && o < bo);
+        // (d2 bits, original index) as one 64-bit compare
+        const bool better = (((unsigned long long)h << 32) | o) < (((unsigned long long)bh << 32) | bo);
+#if GICP_LIN_WARM
         if (CERT) sh2 = better ? bh : ((h < sh2 && o != bo) ? h : sh2);  // (the warm key scanned again: skip)
+#else
+        if (CERT) sh2 = better ? bh : min(h, sh2);  // (stage 1 scans every point once)
+#endif
         bh = better ? h : bh;
         bo = better ? o : bo;
         bj = better ? j : bj;
@@ -132,6 +137,12 @@ __device__ __forceinline__ void nn_search(const float4* __restrict__ pts, const 
     // (k_lin_cert then needs no load of the target point)
     auto certify = [&](float m2) {
         const float l2 = fminf(fminf(__uint_as_float(sh2), lbp * kRel), m2);
+        LPROF({
+            atomicAdd(&g_lprof[64], 1ull);
+            if (l2 == __uint_as_float(sh2)) atomicAdd(&g_lprof[65], 1ull);
+            else if (l2 == lbp * kRel) atomicAdd(&g_lprof[66], 1ull);
+            else atomicAdd(&g_lprof[67], 1ull);
+        })
         const float d1 = sqrtf(__uint_as_float(bh)), dl = sqrtf(l2), r = sqrtf(r2);
         rho = fminf(0.5f * (dl - d1) - 1e-6f * (dl + d1) - 1e-6f, (r - d1) - 1e-6f * (r + d1) - 1e-6f);
     };

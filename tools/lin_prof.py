@@ -48,3 +48,4 @@ print(f"stage 2 (coarser levels) entries {c[1]} ({c[1] / max(c[73], 1):.4f} of s
       f"cands/entry {c[75] / max(c[1], 1):.1f}; ring entries {c[2]}; overflow {c[3]}")
 print(f"search cycles/warp mean {c[5] / max(c[0], 1):.0f}, total cycles/warp mean {c[6] / max(c[78], 1):.0f}")
 print("search log2 hist", c[8:40])
+print(f"certificates {c[64]}: limited by the second-nearest {c[65]}, by a pruned voxel {c[66]}, by the cube {c[67]}")
