@@ -30,7 +30,10 @@
 
 constexpr int kTB = 128;        // queries (threads) per block: consecutive sorted positions
 constexpr int kBlkTiles = 12;   // tiles a block may stage (sparser blocks: per-query kernel)
-constexpr int kBlkCap = 1536;   // staged points per block (+ kTileCap of padding: unclamped reads)
+#ifndef GICP_TILE_BLKCAP
+#define GICP_TILE_BLKCAP 1280  // (1536: 1.141 ms, 1280 + minBlocks 5: 1.109 ms, 1024: 1.12-1.13 ms on the C3 map)
+#endif
+constexpr int kBlkCap = GICP_TILE_BLKCAP;  // staged points per block (+ kTileCap of padding: unclamped reads)
 constexpr int kSlotBits = 9;    // low key bits holding the candidate's slot + 1
 constexpr unsigned kSlotMask = (1u << kSlotBits) - 1u;
 constexpr int kTileCap = (int)kSlotMask;  // staged points per tile (slot + 1 fits the slot bits)
@@ -136,7 +139,7 @@ __device__ __forceinline__ bool exact_less(const float4& q, const float4& a, con
 }
 
 #ifndef GICP_TILE_MINB
-#define GICP_TILE_MINB 1
+#define GICP_TILE_MINB 5
 #endif
 // ROWS: each lane scans only the 27 voxels around its own (nine x-rows of three
 // voxels of the box, staged in (z, y, x) order so every row is contiguous) and the
