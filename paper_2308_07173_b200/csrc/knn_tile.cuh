@@ -150,7 +150,7 @@ __device__ __forceinline__ bool exact_less(const float4& q, const float4& a, con
 // cells, its whole 4x4x4 box probed and staged, the tile's own 2x2x2 first; rows go
 // to the queries' original indices, no covariance. Non-finite queries: per-query path.
 template <int K, bool ROWS, bool EXT = false>
-__global__ void __launch_bounds__(kTB, GICP_TILE_MINB) k_knn_tile(const float4* __restrict__ pts, Grid g0,
+__global__ void __launch_bounds__(kTB, K <= 20 ? GICP_TILE_MINB : 4) k_knn_tile(const float4* __restrict__ pts, Grid g0,
                                                   const int* __restrict__ tiles, const int* __restrict__ tile_of,
                                                   int64_t n, float eps, int32_t* __restrict__ nbr,
                                                   float* __restrict__ d2out, float* __restrict__ cov,

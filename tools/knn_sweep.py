@@ -15,7 +15,7 @@ sys.path.insert(0, os.environ["ROOT"])
 import gen, paper_2308_07173_b200 as g
 cell = float(os.environ["CELL"])
 sc, mp, T, T0 = gen.config_c3()
-for name, pts, c in (("map", mp, cell), ("scan", sc, 0.0)):
+for name, pts, c in (("map", mp, cell), ("scan", sc, float(os.environ.get("SCAN_CELL", "0")))):
     if name == "scan" and os.environ.get("SCAN", "1") == "0": continue
     idx = g.build_index(torch.from_numpy(np.array(pts)).cuda(), c)
     n = len(pts)
