@@ -62,7 +62,7 @@ WORKLOAD_C4 = ("C4 batched scan-to-map: 256 registrations (32 distinct 100k-poin
                "sharded over the GPUs (NCCL chunk-table allreduce per round)")
 WORKLOAD_C3 = "C3 scan-to-map: 100k-point scan vs 2M-point racetrack map, k=20, GICP to convergence"
 REF_SUB = 2000               # oracle sample: source points of one registration
-X
+SCAN_WORKERS = int(os.environ.get("BENCH_SCAN_WORKERS", "8"))   # host threads issuing the scans' kNN/cov
 
 
 def peaks():
