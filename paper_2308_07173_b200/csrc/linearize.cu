@@ -1299,6 +1299,9 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
     // either path to check that they agree bitwise
     int64_t split_min = kSplitMinPoints;
     if (const char* e = getenv("GICP_LIN_SPLIT_MIN")) split_min = atoll(e);
+    // GICP_LIN_COOP_MAX (env): the largest full-search queue searched a warp per point
+    unsigned coop_max = kCoopMax;
+    if (const char* e = getenv("GICP_LIN_COOP_MAX")) coop_max = (unsigned)atoll(e);
     if (cert && scr.queue && ns >= split_min) {
         int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, 4 * sizeof(unsigned), s), "memset");
         if (rc) return rc;
@@ -1332,10 +1335,10 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
         const unsigned g3 = (unsigned)std::min<int64_t>(grid2, std::max<int64_t>(1, g2));
         k_lin_search<false><<<g3, kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
                                                         const_cast<float4*>(scr.cache_old), scr.queue, scr.queue2,
-                                                        scr.qcount, kCoopMax);
+                                                        scr.qcount, coop_max);
         k_lin_search_coop<<<g3, kSearchBlock, 0, s>>>(tgt->pts, lvs, tgt->n, r2, ca, cb, scr.cache_new,
                                                       const_cast<float4*>(scr.cache_old), scr.queue2, scr.qcount,
-                                                      kCoopMax);
+                                                      coop_max);
         static const bool dbg = getenv("GICP_DEBUG_SPLIT") != nullptr;  // diagnostics: queue sizes
         if (dbg) {
             unsigned q[4];

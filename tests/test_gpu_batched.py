@@ -144,12 +144,15 @@ def test_align_batched_certificates_bitwise(problem, monkeypatch):
         [(i.iterations, i.converged, i.error, i.inliers) for i in ib]
 
 
-@pytest.mark.parametrize("single", [False, True])
-def test_split_evaluation_bitwise(problem, monkeypatch, single):
+@pytest.mark.parametrize("single,coop", [(False, True), (False, False), (True, True)])
+def test_split_evaluation_bitwise(problem, monkeypatch, single, coop):
     """The split evaluation (k_lin_cert -> k_lin_search -> k_lin_terms, used for
     launches of >= 1M points) and the fused k_linearize give bitwise the same
-    aligns: forced on (GICP_LIN_SPLIT_MIN=0) against forced off."""
+    aligns: forced on (GICP_LIN_SPLIT_MIN=0) against forced off; the unsettled
+    points searched a warp per point (k_lin_search_coop) or per lane
+    (GICP_LIN_COOP_MAX=0: k_lin_search<false>)."""
     p = problem
+    monkeypatch.setenv("GICP_LIN_COOP_MAX", "16384" if coop else "0")
     def run():
         if single:
             b = int(np.argmax(np.diff(p["offs"])))
