@@ -15,6 +15,9 @@ method's values happens in the library.
 """
 from __future__ import annotations
 
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -131,6 +134,110 @@ def align_batched_sharded(g, src, src_cov, offsets, tgt, tgt_cov, T0s, group=Non
         cov_l = torch.zeros((0, 6), dtype=src_cov.dtype, device=src_cov.device)
     return g.align_batched_sharded(src_l, cov_l, plan.loffs, plan.gid, plan.num_chunks, plan.B, tgt, tgt_cov, T0s,
                                    allreduce=make_allreduce(plan.group), **params)
+
+
+class _RoundRobinGate:
+    """Orders the per-round collectives of concurrently aligned groups: group k may
+    enqueue its allreduce only on its turn; turns go round-robin over the groups
+    still aligning. Every rank runs the same groups with the same round counts
+    (their rows are bitwise equal), so every rank enqueues the same sequence of
+    collectives on the one communicator."""
+
+    def __init__(self, n):
+        self.n, self.turn, self.done = n, 0, [False] * n
+        self.cv = threading.Condition()
+
+    def _advance(self):
+        for step in range(1, self.n + 1):
+            t = (self.turn + step) % self.n
+            if not self.done[t]:
+                self.turn = t
+                break
+        self.cv.notify_all()
+
+    def run(self, k, fn):
+        with self.cv:
+            while self.turn != k:
+                self.cv.wait()
+            try:
+                fn()
+            finally:
+                self._advance()
+
+    def finish(self, k):
+        with self.cv:
+            self.done[k] = True
+            if self.turn == k:
+                self._advance()
+            self.cv.notify_all()
+
+
+class ConcurrentAlign:
+    """The batch's registrations split into `n_groups` contiguous groups, each aligned
+    by `align_batched_sharded` on its own host thread and CUDA stream, so one group's
+    kernels run while another's host LM decides its next round (the GPU no longer
+    idles at every round's host turn-around). Per registration the result is bitwise
+    the single batched call's (every registration is evaluated exactly as alone).
+    With a process group, the groups' chunk-table allreduces are issued in a fixed
+    round-robin order (_RoundRobinGate) on the one communicator."""
+
+    def __init__(self, offsets, device, n_groups: int, group=None, num_chunks: int = NUM_CHUNKS, reg_base=None):
+        offsets = np.asarray(offsets, dtype=np.int64)
+        B = len(offsets) - 1
+        base = offsets[:-1] if reg_base is None else np.asarray(reg_base, dtype=np.int64)
+        n_groups = max(1, min(int(n_groups), B))
+        cuts = [round(k * B / n_groups) for k in range(n_groups + 1)]
+        self.ranges = [(cuts[k], cuts[k + 1]) for k in range(n_groups) if cuts[k + 1] > cuts[k]]
+        self.plans = []
+        for lo, hi in self.ranges:
+            sub = offsets[lo:hi + 1] - offsets[lo]
+            self.plans.append(ShardPlan(sub, device, group, num_chunks, base[lo:hi]))
+        self.streams = [torch.cuda.Stream(device=device) for _ in self.ranges]
+        dev_index = torch.device(device).index
+        self.pool = ThreadPoolExecutor(max_workers=len(self.ranges),
+                                       initializer=lambda: torch.cuda.set_device(dev_index))
+        self.group = group
+
+    def __call__(self, g, src, src_cov, tgt, tgt_cov, T0s, **params):
+        T0s = np.asarray(T0s, dtype=np.float64)
+        caller = torch.cuda.current_stream(src.device)
+        ready = torch.cuda.Event()
+        ready.record(caller)
+        collective = make_allreduce(self.group) is not None
+        gate = _RoundRobinGate(len(self.ranges)) if collective else None
+
+        def job(k):
+            lo, hi = self.ranges[k]
+            plan, st = self.plans[k], self.streams[k]
+            try:
+                st.wait_event(ready)
+                with torch.cuda.stream(st):
+                    ar = make_allreduce(plan.group)
+                    if gate is not None and ar is not None:
+                        inner = ar
+
+                        def ar(table, _inner=inner, _k=k):
+                            gate.run(_k, lambda: _inner(table))
+                    if plan.idx.numel():
+                        src_l, cov_l = src.index_select(0, plan.idx), src_cov.index_select(0, plan.idx)
+                    else:
+                        src_l = torch.zeros((0, 3), dtype=src.dtype, device=src.device)
+                        cov_l = torch.zeros((0, 6), dtype=src_cov.dtype, device=src_cov.device)
+                    T, infos = g.align_batched_sharded(src_l, cov_l, plan.loffs, plan.gid, plan.num_chunks, plan.B,
+                                                       tgt, tgt_cov, T0s[lo:hi], allreduce=ar, **params)
+                    done = torch.cuda.Event()
+                    done.record(st)
+                return np.asarray(T), infos, done
+            finally:
+                if gate is not None:
+                    gate.finish(k)
+
+        out = list(self.pool.map(job, range(len(self.ranges))))
+        for _, _, done in out:
+            caller.wait_event(done)
+        T = np.concatenate([o[0] for o in out])
+        infos = [i for o in out for i in o[1]]
+        return T, infos
 
 
 # ---------------------------------------------------------------------------

@@ -50,14 +50,18 @@ def _problem(scans=None):
     return g, im, cm, torch.cat(srcs).contiguous(), torch.cat(covs).contiguous(), offs, np.array(T0)
 
 
-def _worker(rank, world, port, q, tiny=False):
+def _worker(rank, world, port, q, tiny=False, groups=1):
     import torch.distributed as dist
     # file rendezvous: no TCP port to race for (a bind/close/reuse port probe is racy)
     dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     sys.path.insert(0, ROOT)
     from paper_2308_07173_b200 import sharding
     g, im, cm, src, cov, offs, T0 = _problem(TINY if tiny else None)
-    Ts, infos = sharding.align_batched_sharded(g, src, cov, offs, im, cm, T0)
+    if groups > 1:  # concurrent groups, their allreduces in round-robin order
+        conc = sharding.ConcurrentAlign(offs, src.device, groups)
+        Ts, infos = conc(g, src, cov, im, cm, T0)
+    else:
+        Ts, infos = sharding.align_batched_sharded(g, src, cov, offs, im, cm, T0)
     q.put((rank, Ts, [(i.iterations, i.converged, i.error, i.inliers) for i in infos]))
     dist.destroy_process_group()
 
@@ -70,11 +74,11 @@ def _free_port():
     return os.path.join(d, "rendezvous")
 
 
-def _run(world, tiny=False):
+def _run(world, tiny=False, groups=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, tiny)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, tiny, groups)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict((r, (T, inf)) for r, T, inf in (q.get(timeout=240) for _ in range(world)))
@@ -100,6 +104,18 @@ def test_sharded_align_world2_is_bitwise_world1():
         c = (np.trace(T1[b][:3, :3] @ Tu[b][:3, :3].T) - 1) / 2
         assert np.arccos(min(1.0, c)) <= 1e-4
         assert i1[b][3] > 0 and abs(i1[b][3] - iu[b].inliers) <= 0.001 * iu[b].inliers
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_concurrent_groups_are_bitwise_the_single_call(world):
+    """sharding.ConcurrentAlign (bench.py's timed steps): the batch split into
+    concurrent groups, each its own host thread and stream, the groups' per-round
+    allreduces ordered round-robin on the one process group; every pose and info
+    bitwise the single batched call's."""
+    r1 = _run(1)
+    rg = _run(world, groups=2)
+    for r in range(world):
+        assert np.array_equal(rg[r][0], r1[0][0]) and rg[r][1] == r1[0][1]
 
 
 def test_sharded_align_with_an_idle_rank():
