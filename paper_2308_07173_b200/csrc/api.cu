@@ -569,6 +569,12 @@ static double coarse_threshold(const gicp_index_s* tgt) {
 #define GICP_LIN_SPLIT 1
 #endif
 static bool split_eval(int64_t n) { return GICP_LIN_SPLIT && n < (1ll << 30); }
+// the batched align's deferred reduction (linearize.cu k_lin_reduce): the kernels skip
+// the per-block fence + ticket; GICP_LIN_INLINE_REDUCE (env) keeps the in-kernel one
+static bool deferred_reduce() {
+    static const bool inl = getenv("GICP_LIN_INLINE_REDUCE") != nullptr;
+    return !inl;
+}
 // |dv| + |dw| * 20 m (a typical range of the scan points): the step's point motion
 static double step_displacement(const double* d) {
     return std::sqrt(d[3] * d[3] + d[4] * d[4] + d[5] * d[5]) + 20.0 * std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
@@ -1181,25 +1187,32 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
                 bv.n_active = n_active;
                 bv.out_stride = 32;
                 int64_t nbl = bs.nb;
+                // this kind's entries as a {first block, compact start} list (pinned
+                // staging, one region per kind): the deferred reduction's entries
+                // and, when only part of the entries is active, the compacted block
+                // table (expanded on the device) that launches only their blocks
+                int2* cl = (int2*)(mb->h + rows + 256 + (size_t)std::max(E, B) * sizeof(Pose)) +
+                           (size_t)(kind - 1) * (E + 1);
+                int nce = 0, acc = 0;
+                for (int e = 0; e < E; ++e)
+                    if (eact[e]) {
+                        cl[nce++] = make_int2(bs.eblk[e], acc);
+                        acc += bs.eblk[e + 1] - bs.eblk[e];
+                    }
+                cl[nce] = make_int2(0, acc);
+                r = check_cuda(cudaMemcpyAsync(bs.clist, cl, (nce + 1) * sizeof(int2), cudaMemcpyHostToDevice, s),
+                               "H2D");
+                if (r) return r;
                 if (n_active < E) {
-                    // only this kind's entries' blocks are launched: their {first block,
-                    // compact start} list goes up (pinned staging, one region per kind)
-                    // and expands on the device
-                    int2* cl = (int2*)(mb->h + rows + 256 + (size_t)std::max(E, B) * sizeof(Pose)) +
-                               (size_t)(kind - 1) * (E + 1);
-                    int nce = 0, acc = 0;
-                    for (int e = 0; e < E; ++e)
-                        if (eact[e]) {
-                            cl[nce++] = make_int2(bs.eblk[e], acc);
-                            acc += bs.eblk[e + 1] - bs.eblk[e];
-                        }
-                    cl[nce] = make_int2(0, acc);
-                    r = check_cuda(cudaMemcpyAsync(bs.clist, cl, (nce + 1) * sizeof(int2), cudaMemcpyHostToDevice, s),
-                                   "H2D");
-                    if (!r) r = launch_compact_btab(bs.btab, bs.clist, nce, acc, bs.ctab, s);
+                    r = launch_compact_btab(bs.btab, bs.clist, nce, acc, bs.ctab, s);
                     if (r) return r;
                     bv.btab = bs.ctab;
                     nbl = acc;
+                }
+                if (deferred_reduce()) {
+                    bv.elist = bs.clist;
+                    bv.n_e = nce;
+                    bv.btab_full = bs.btab;
                 }
                 bs.ls.seq = ++seq;
                 last_seq = bs.ls.seq;

@@ -245,6 +245,12 @@ struct BatchView {
     int n_scans = 1;
     int n_active = 1;
     int out_stride = 0;
+    // deferred reduction (gicp_align_batched): the launch's active entries as
+    // {first block in the full table, -}; the kernels only write their block partials
+    // and k_lin_reduce sums each entry's partials (the same fixed order) afterwards
+    const int2* elist = nullptr;
+    int n_e = 0;
+    const int4* btab_full = nullptr;
 };
 
 struct LinScratch {
