@@ -1137,7 +1137,15 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             st[b].rc = GICP_EDEGENERATE;
         }
     }
-    const double coarse_thr = coarse_threshold(tgt);
+    // the level-1 cube stage after the first evaluation: the split evaluation (>= 1M
+    // points, linearize.cu) settles far points in its cooperative full pass, so there
+    // only the first evaluation (pose error unknown) takes it (C4 dual launch 0.89 ->
+    // 0.86 ms against the single-align threshold); GICP_LIN_COARSE_FIRST=0 not even that
+    int64_t split_min = 1 << 20;
+    if (const char* e = getenv("GICP_LIN_SPLIT_MIN")) split_min = atoll(e);
+    const bool split_path = ns >= split_min;
+    const double coarse_thr = split_path ? 1e300 : coarse_threshold(tgt);
+    static const bool coarse_first = !(getenv("GICP_LIN_COARSE_FIRST") && atoi(getenv("GICP_LIN_COARSE_FIRST")) == 0);
     // GICP_DEBUG_ALIGN_HOST: rounds, their device-wait time and the host time between them
     const bool host_trace = getenv("GICP_DEBUG_ALIGN_HOST") != nullptr;
     using clk = std::chrono::steady_clock;
@@ -1160,7 +1168,7 @@ static int align_batched_impl(const float* src, const float* src_cov, const int6
             pst[b] = make_pose(trial ? q.Tn : q.T, trial ? q.pn : q.piv);
             pst[b].active = 1;
             pst[b].cur = q.cur;
-            pst[b].coarse = q.disp > coarse_thr;  // per registration
+            pst[b].coarse = q.disp > coarse_thr && (coarse_first || !split_path);  // per registration (§4.3)
         }
         for (int e = 0; e < E; ++e) n_any += pst[reg(e)].active && offsets[e + 1] > offsets[e];
         int r = GICP_OK;
