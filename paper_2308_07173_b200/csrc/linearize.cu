@@ -949,6 +949,9 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
 #ifndef GICP_SEARCH_MINB
 #define GICP_SEARCH_MINB 4  // 64 registers: more warps spill, and measured slower (4: 1.64, 5: 2.04, 8: 2.22 ms)
 #endif
+#ifndef GICP_SEARCH_MINB_LEAN
+#define GICP_SEARCH_MINB_LEAN 5  // the lean pass: 48 registers (4: 0.860, 5: 0.845, 6: 0.870 ms C4 dual)
+#endif
 #ifndef GICP_SEARCH_UNROLL
 #define GICP_SEARCH_UNROLL 4  // with the lean first pass (dual launch): 4: 1.12, 2: 1.15 ms
 #endif
@@ -971,7 +974,7 @@ constexpr int64_t kSplitMinPoints = GICP_SPLIT_MIN;
 // qcount[1]); points it cannot settle go to queue2 (qcount[2], claimed through
 // qcount[3]) for the full search (LEAN = false)
 template <bool LEAN>
-__global__ void __launch_bounds__(kSearchBlock, GICP_SEARCH_MINB)
+__global__ void __launch_bounds__(kSearchBlock, LEAN ? GICP_SEARCH_MINB_LEAN : GICP_SEARCH_MINB)
     k_lin_search(const float4* __restrict__ pts, Levels lvs, int64_t nt, float r2, int32_t* __restrict__ corr_a,
                  int32_t* __restrict__ corr_b, float4* __restrict__ cache_a, float4* __restrict__ cache_b,
                  const float4* __restrict__ queue, float4* __restrict__ queue2, unsigned* __restrict__ qcount,
