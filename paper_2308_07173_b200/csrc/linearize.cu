@@ -859,9 +859,13 @@ __global__ void __launch_bounds__(kLinBlock, ERROR_ONLY ? GICP_TRIAL_MINB : GICP
 // terms in the same order: the result is bitwise the fused kernel's.
 // ---------------------------------------------------------------------------
 
+#ifndef GICP_CERT_PPT
+#define GICP_CERT_PPT 4  // (1: 0.840, 2: 0.837, 4: 0.811 ms C4 dual)
+#endif
+constexpr int kCertPPT = GICP_CERT_PPT;  // points per thread of k_lin_cert
 // queue entry: the search point and w = i | coarse << 30 | (write base buffers) << 31
 template <bool DUAL>
-__global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict__ src, int64_t ns,
+__global__ void __launch_bounds__(kLinBlock / kCertPPT) k_lin_cert(const float* __restrict__ src, int64_t ns,
                                                         const float4* __restrict__ pts, Pose P, float r2, int coarse_ok,
                                                         int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old,
                                                         BatchView bv, float4* __restrict__ cache_new,
@@ -892,46 +896,72 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
         cache_old = ccur;
         wbase = sP.cur ? 1u : 0u;
     }
-    const int64_t i = p0 + (int64_t)blk * kPPB + threadIdx.x;
-    const bool active = i < pend;
-    float sx = 0.f, sy = 0.f, sz = 0.f;
-    bool cached = false;
-    if (active) {
-        // the point, its certificate and its previous correspondence: independent
-        // loads, issued together
-        const double px = LDS_(src + 3 * i), py = LDS_(src + 3 * i + 1), pz = LDS_(src + 3 * i + 2);
-        const float4 cc = (DUAL && cache_old) ? LDS_(cache_old + i) : make_float4(0.f, 0.f, 0.f, -1.f);
-        const int bj = (DUAL && cache_old) ? LDS_(corr_old + i) : 0;
+    // kCertPPT points per thread (i, i + threads, ...): every load of all of them is
+    // issued before any is used (the kernel streams ~60 B a point, latency-bound)
+    constexpr int T = kLinBlock / kCertPPT;
+    int64_t ii[kCertPPT];
+    bool act[kCertPPT], cached[kCertPPT];
+    double px[kCertPPT], py[kCertPPT], pz[kCertPPT];
+    float4 cc[kCertPPT];
+    int bj[kCertPPT];
+    float sx[kCertPPT], sy[kCertPPT], sz[kCertPPT];
+#pragma unroll
+    for (int u = 0; u < kCertPPT; ++u) {
+        ii[u] = p0 + (int64_t)blk * kPPB + threadIdx.x + u * T;
+        act[u] = ii[u] < pend;
+        cached[u] = false;
+        cc[u] = make_float4(0.f, 0.f, 0.f, -1.f);
+        bj[u] = 0;
+        px[u] = py[u] = pz[u] = 0.0;
+        if (act[u]) {
+            const int64_t i = ii[u];
+            px[u] = LDS_(src + 3 * i);
+            py[u] = LDS_(src + 3 * i + 1);
+            pz[u] = LDS_(src + 3 * i + 2);
+            if (DUAL && cache_old) {
+                cc[u] = LDS_(cache_old + i);
+                bj[u] = LDS_(corr_old + i);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kCertPPT; ++u) {
+        sx[u] = sy[u] = sz[u] = 0.f;
+        if (!act[u]) continue;
         double pp[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
-            pp[a] = __fma_rn(sP.R[3 * a + 2], pz, __fma_rn(sP.R[3 * a + 1], py, __fma_rn(sP.R[3 * a], px, sP.t[a])));
-        sx = (float)pp[0];
-        sy = (float)pp[1];
-        sz = (float)pp[2];
+            pp[a] = __fma_rn(sP.R[3 * a + 2], pz[u], __fma_rn(sP.R[3 * a + 1], py[u], __fma_rn(sP.R[3 * a], px[u], sP.t[a])));
+        sx[u] = (float)pp[0];
+        sy[u] = (float)pp[1];
+        sz[u] = (float)pp[2];
         if (DUAL && cache_old) {
-            if (cc.w > 0.0f) {
-                const double ex = (double)sx - cc.x, ey = (double)sy - cc.y, ez = (double)sz - cc.z;
-                cached = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc.w;
+            if (cc[u].w > 0.0f) {
+                const double ex = (double)sx[u] - cc[u].x, ey = (double)sy[u] - cc[u].y, ez = (double)sz[u] - cc[u].z;
+                cached[u] = sqrt(ex * ex + ey * ey + ez * ez) < (double)cc[u].w;
             }
-            if (cached) {  // the certified pair (inside the gate by construction of rho)
-                STS_(corr + i, bj);
-                STS_(cache_new + i, cc);
+            if (cached[u]) {  // the certified pair (inside the gate by construction of rho)
+                STS_(corr + ii[u], bj[u]);
+                STS_(cache_new + ii[u], cc[u]);
             }
         }
     }
     // one queue reservation per block (the counter is a single address: per-warp
-    // atomics serialise at the L2); the warps' slots follow in warp order
-    const bool push = active && !cached;
-    const unsigned m = __ballot_sync(0xffffffffu, push);
+    // atomics serialise at the L2); slots follow in (point slot, warp) order
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __shared__ unsigned wcnt[kLinBlock / 32], bbase;
-    if (lane == 0) wcnt[wid] = (unsigned)__popc(m);
+    constexpr int NW = T / 32;
+    __shared__ unsigned wcnt[kCertPPT * NW], bbase;
+    unsigned m[kCertPPT];
+#pragma unroll
+    for (int u = 0; u < kCertPPT; ++u) {
+        m[u] = __ballot_sync(0xffffffffu, act[u] && !cached[u]);
+        if (lane == 0) wcnt[u * NW + wid] = (unsigned)__popc(m[u]);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned tot = 0;
 #pragma unroll
-        for (int w = 0; w < kLinBlock / 32; ++w) {
+        for (int w = 0; w < kCertPPT * NW; ++w) {
             const unsigned c = wcnt[w];
             wcnt[w] = tot;
             tot += c;
@@ -939,10 +969,14 @@ __global__ void __launch_bounds__(kLinBlock) k_lin_cert(const float* __restrict_
         bbase = tot ? atomicAdd(qcount, tot) : 0u;
     }
     __syncthreads();
-    const unsigned base = bbase + wcnt[wid];
-    if (push) {
-        const unsigned w = (unsigned)i | ((sP.coarse && coarse_ok) ? (1u << 30) : 0u) | (wbase << 31);
-        STS_(queue + base + __popc(m & ((1u << lane) - 1u)), make_float4(sx, sy, sz, __uint_as_float(w)));
+#pragma unroll
+    for (int u = 0; u < kCertPPT; ++u) {
+        if (act[u] && !cached[u]) {
+            const unsigned base = bbase + wcnt[u * NW + wid];
+            const unsigned w = (unsigned)ii[u] | ((sP.coarse && coarse_ok) ? (1u << 30) : 0u) | (wbase << 31);
+            STS_(queue + base + __popc(m[u] & ((1u << lane) - 1u)),
+                 make_float4(sx[u], sy[u], sz[u], __uint_as_float(w)));
+        }
     }
 }
 
@@ -1363,11 +1397,11 @@ int launch_linearize_core(const float* src, const float* src_cov, int64_t ns, co
         int rc = check_cuda(cudaMemsetAsync(scr.qcount, 0, 4 * sizeof(unsigned), s), "memset");
         if (rc) return rc;
         if (dual)
-            k_lin_cert<true><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
+            k_lin_cert<true><<<(unsigned)nb, kLinBlock / kCertPPT, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
                                                                  corr_old, bvq, scr.cache_new, scr.cache_old,
                                                                  scr.queue, scr.qcount);
         else
-            k_lin_cert<false><<<(unsigned)nb, kLinBlock, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
+            k_lin_cert<false><<<(unsigned)nb, kLinBlock / kCertPPT, 0, s>>>(src, ns, tgt->pts, P, r2, lvs.coarse_ok ? 1 : 0, corr,
                                                                   corr_old, bvq, scr.cache_new, scr.cache_old,
                                                                   scr.queue, scr.qcount);
         static int grid = 0, grid2 = 0;
