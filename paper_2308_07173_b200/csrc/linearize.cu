@@ -55,6 +55,9 @@ __device__ unsigned long long g_lprof[80];  // [0..3] stage counts, [4] max sear
 #define LDS_(p) (*(p))
 #define STS_(p, v) (*(p) = (v))
 #endif
+#ifndef GICP_TERMS_MINB
+#define GICP_TERMS_MINB GICP_LIN_MINB  // the terms kernel (split evaluation; 4: 0.809, 5: 0.870, 6: 0.922 ms -- spills)
+#endif
 #ifndef GICP_TRIAL_MINB
 #define GICP_TRIAL_MINB 8  // the trial (error-only) terms kernel: 32 registers (4: 0.132, 6: 0.114, 8: 0.111 ms)
 #endif
@@ -755,7 +758,7 @@ __global__ void __launch_bounds__(kLinBlock, GICP_LIN_MINB) k_linearize(const fl
 // read directly, and that target point and covariance) is issued before the block
 // waits for its pose, whose copy into shared memory is spread over the first threads.
 template <bool ERROR_ONLY, bool DUAL, bool PRE>
-__global__ void __launch_bounds__(kLinBlock, ERROR_ONLY ? GICP_TRIAL_MINB : GICP_LIN_MINB)
+__global__ void __launch_bounds__(kLinBlock, ERROR_ONLY ? GICP_TRIAL_MINB : GICP_TERMS_MINB)
     k_lin_terms(const float* __restrict__ src, const float* __restrict__ src_cov, int64_t ns,
                 const float4* __restrict__ pts, int64_t nt, const float4* __restrict__ tgt_cov_sorted, Pose P,
                 const int32_t* __restrict__ corr, const int32_t* __restrict__ corr_old, double* __restrict__ partials,
